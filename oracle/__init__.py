@@ -1,0 +1,27 @@
+"""CPU ORACLE -- test infrastructure only.
+
+A plain, slow, obviously-correct CPU model of MemPool's block pool, prompt
+index and KV-block migration (§4 "Elastic Memory Pool", Table
+tbl-mempool-api P:261-290; §4.2 indexing P:326-337; §4.3 transfer workflow
+P:360-369; §5.2 aggregation P:549-550), with every place the paper is silent
+filled by the readings R1-R13 listed in DESIGN.md §3 (= SURVEY.md §8(c)).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2406_17565_b200``, ``libmempool.so``) never imports it and shares no
+code with it; the only shared module is ``workloads`` (seeded input
+generators, no method arithmetic).
+
+Parity status: see DESIGN.md §3.  Pinned: allocator (lowest-first, S:131-133
+examples, conservation), match/insert/delete (brute-force longest-prefix model,
+S:207, SPEC examples), migration bytes (closed form dst[d_j] == src[s_j],
+np.take cross-check), golden worked example.  Parity unpinned (our readings,
+pinned only by our own derivations): the LRU clock and tie-breaks (R7-R9),
+delete's terminal rule (R6), suffix/DEDUP semantics of transfer_with_insert
+(R3), eviction-before-OOM feasibility (R2).
+"""
+from .mempool_oracle import (  # noqa: F401
+    HBM, DRAM, MIXED, FREE, ACTIVE, INDEXED, ORPHAN,
+    FLAG_DST_GIVEN, FLAG_DEDUP, FLAG_INS_ERR_ON_CONFLICT, FLAG_MATCH_PIN,
+    MPError, OraclePool, transfer, transfer_with_insert,
+)

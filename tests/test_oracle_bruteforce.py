@@ -1,0 +1,113 @@
+"""Oracle index vs a brute-force set-of-sequences model:
+randomized insert / match / delete / evict sequences, <=100 stored sequences,
+lengths <= 512, B in {8, 16}.
+
+The brute-force model is a plain list of stored token sequences; it knows
+nothing about prefix maps.  It pins:
+  * match(q) == max over stored s of min(floor(lcp(q, s)/B), floor(|s|/B)) * B
+    while no evict has happened;
+  * insert idempotence, eviction safety, conservation;
+  * after evict, match lengths never grow and freed blocks are unreferenced.
+"""
+import numpy as np
+import pytest
+
+from oracle import HBM, FREE, OraclePool, FLAG_MATCH_PIN
+
+
+def lcp(a, b):
+    n = min(len(a), len(b))
+    i = 0
+    while i < n and a[i] == b[i]:
+        i += 1
+    return i
+
+
+def brute_match(stored, q, B):
+    best = 0
+    for s in stored:
+        best = max(best, min(lcp(q, s) // B, len(s) // B))
+    return best * B
+
+
+def gen_seq(rng, stored, vocab, maxlen):
+    if stored and rng.random() < 0.7:
+        base = stored[rng.integers(len(stored))]
+        cut = int(rng.integers(0, len(base) + 1))
+        tail = rng.integers(0, vocab, size=int(rng.integers(0, max(1, maxlen - cut + 1))))
+        return list(base[:cut]) + [int(t) for t in tail]
+    return [int(t) for t in rng.integers(0, vocab, size=int(rng.integers(0, maxlen + 1)))]
+
+
+def run_sequence(seed, B, n_ops, with_evict):
+    rng = np.random.default_rng(seed)
+    cap = 2048
+    pool = OraclePool(0, 1, 1, 8, B, n_hbm=cap, n_dram=0)
+    stored = []           # brute-force model: list of inserted (terminal) sequences
+    evicted_any = False
+    vocab = int(rng.integers(2, 6))
+    for _ in range(n_ops):
+        op = rng.random()
+        if op < 0.45 and len(stored) < 100:
+            s = gen_seq(rng, stored, vocab, 512 if rng.random() < 0.2 else 96)
+            k = len(s) // B
+            if pool.free_count(HBM) < k + 1:
+                continue
+            addrs = pool.alloc_mem(k, HBM)
+            pool.insert(np.array(s, np.int32), addrs)
+            # S:208 idempotence: re-insert of the final mapping is a no-op
+            if k:
+                _, final = pool.match(np.array(s, np.int32))
+                snap = pool.dump_index()
+                pool.insert(np.array(s, np.int32), final)
+                assert [x[:3] + x[4:] for x in pool.dump_index()] == \
+                       [x[:3] + x[4:] for x in snap]
+            # the index keys on the block-truncated sequence (R1)
+            if k and s[: k * B] not in stored:
+                stored.append(s[: k * B])
+        elif op < 0.75:
+            q = gen_seq(rng, stored, vocab, 128)
+            mt, addrs = pool.match(np.array(q, np.int32))
+            assert len(addrs) * B == mt
+            if not evicted_any:
+                assert mt == brute_match(stored, q, B)
+            else:
+                assert mt <= brute_match(stored, q, B)
+            for a in addrs:
+                assert pool.state[HBM][a[2]] == "indexed"
+        elif op < 0.9 and stored:
+            s = stored.pop(int(rng.integers(len(stored))))
+            pool.delete(np.array(s, np.int32))
+        elif with_evict:
+            before = pool.dump_index()
+            freed = pool.evict(int(rng.integers(1, 8)), HBM)
+            evicted_any = evicted_any or bool(freed)
+            for a in freed:
+                assert pool.state[HBM][a[2]] == FREE
+                assert all(i != a[2] for _k, _m, i, *_ in pool.dump_index())
+            assert len(pool.dump_index()) == len(before) - len(freed)
+        pool.check_invariants()
+        used = sum(1 for x in pool.state[HBM] if x != FREE)
+        assert used + pool.free_count(HBM) == cap
+        assert used == len(pool.index)   # every allocated block is indexed here
+
+
+@pytest.mark.parametrize("B", [8, 16])
+@pytest.mark.parametrize("with_evict", [False, True])
+def test_random_sequences(B, with_evict):
+    for seed in range(60):
+        run_sequence(seed * 7 + B, B, 40, with_evict)
+
+
+def test_pin_blocks_eviction():
+    """S:209 eviction safety: pinned blocks are never freed or swapped."""
+    pool = OraclePool(0, 1, 1, 8, 8, n_hbm=16, n_dram=4)
+    a = pool.alloc_mem(4, HBM)
+    s = np.arange(32, dtype=np.int32)
+    pool.insert(s, a)
+    pool.match(s, flags=FLAG_MATCH_PIN)
+    assert pool.evict(10, HBM) == []
+    pool.delete(s)                      # unlinked but pinned -> orphans
+    assert all(pool.state[HBM][x[2]] == "orphan" for x in a)
+    pool.unpin(a)
+    assert all(pool.state[HBM][x[2]] == FREE for x in a)
