@@ -1,0 +1,255 @@
+/*
+ * mempool.h -- C-ABI of libmempool.so: the KV-block migration hot path of
+ * MemServe's elastic memory pool (MemPool), rebuilt for B200 (sm_100a).
+ *
+ * Source of every entry point: PAPER.md Table tbl-mempool-api (P:261-290,
+ * "Elastic Memory Pool APIs. Type can be HBM-only, DRAM-only, or mixed. Each
+ * address encodes instance ID. Transfer flags can control on-demand
+ * allocation."), §4.2 indexing, §4.3 transfer workflow
+ * (P:360-369), §5.2 block aggregation; SPEC.md signatures/errors
+ * (S:125-203).  Where the paper is silent the behaviour follows the
+ * readings R1-R13 in DESIGN.md §3.
+ *
+ * Conventions (apply to every function):
+ *  - All array arguments are HOST pointers owned by the caller; the library
+ *    never keeps a caller pointer past the call, except the slab and DRAM
+ *    pointers given to mp_pool_create, which must outlive the pool.
+ *  - A negative mp_status means NO state change (all-or-nothing) and output
+ *    counts/arrays are written only on MP_OK.  MP_ERR_CUDA is the exception:
+ *    a CUDA failure leaves the pool in an unspecified state (call
+ *    mp_last_error() for the CUDA message and destroy the pool).
+ *  - One caller thread per pool at a time; a transfer uses both
+ *    pools and must not race with calls on either.
+ *  - Every call is synchronous: it returns after all device work it issued
+ *    has completed (transfers: after the receiver's insert).
+ *  - Layout: the HBM pool of an instance is 2*L "slabs" (K_0, V_0, K_1, V_1,
+ *    ...), each hbm_blocks chunks of c = B*H*D*elem bytes (vLLM's per-layer
+ *    paged layout: "two blocks per LLM layer").  Block id b is chunk b
+ *    of every slab.  The DRAM pool and all staging buffers use the
+ *    AGGREGATED layout: block i is one contiguous Pb = 2*L*c byte
+ *    region, ordered layer-major, K before V (reading R11).
+ */
+#ifndef MEMPOOL_H
+#define MEMPOOL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mp_pool mp_pool; /* opaque; one per serving instance */
+
+/* Block address ("Each address encodes instance ID"):
+ * bits [63:40] instance id, [39:32] medium (0 = HBM, 1 = DRAM), [31:0] index. */
+typedef uint64_t mp_addr;
+typedef int32_t mp_token; /* token ids */
+
+#define MP_ADDR(inst, medium, idx)                                              \
+  ((((uint64_t)(uint32_t)(inst)) << 40) | (((uint64_t)(medium) & 0xFF) << 32) | \
+   (uint64_t)(uint32_t)(idx))
+#define MP_ADDR_INST(a) ((int32_t)((a) >> 40))
+#define MP_ADDR_MEDIUM(a) ((int32_t)(((a) >> 32) & 0xFF))
+#define MP_ADDR_INDEX(a) ((int32_t)((a)&0xFFFFFFFFu))
+
+typedef enum { MP_HBM = 0, MP_DRAM = 1, MP_MIXED = 2 } mp_medium;
+
+typedef enum {
+  MP_OK = 0,
+  MP_ERR_OOM = -1,             /* S:129 OutOfMemory (after eviction attempt) */
+  MP_ERR_DOUBLE_FREE = -2,     /* S:139 DoubleFree */
+  MP_ERR_INVALID_ADDR = -3,    /* S:139 InvalidAddr: wrong instance / medium / range */
+  MP_ERR_ADDR_COUNT = -4,      /* S:149 AddrCountMismatch */
+  MP_ERR_CONFLICT = -5,        /* S:149 ConflictingMapping (MP_INS_ERR_ON_CONFLICT only) */
+  MP_ERR_NO_DRAM = -6,         /* S:189 NoDramCapacity */
+  MP_ERR_DST_OOM = -7,         /* S:255 DstOutOfMemory */
+  MP_ERR_DST_UNREACHABLE = -8, /* S:255 DstUnreachable: instance not connected */
+  MP_ERR_PRECONDITION = -9,    /* S:202 precondition violated (wrong state/medium) */
+  MP_ERR_PREFIX_MISSING = -10, /* R3: receiver lacks the prefix a suffix send needs */
+  MP_ERR_CONFIG = -11,         /* bad argument / incompatible pools */
+  MP_ERR_BUFFER_TOO_SMALL = -12,
+  MP_ERR_CUDA = -13,
+  MP_ERR_NCCL = -14,
+  MP_ERR_INTERNAL = -15        /* self-check failed (e.g. device allocator vs host shadow) */
+} mp_status;
+
+/* ---- flags ("Transfer flags can control on-demand allocation") ---- */
+#define MP_XFER_DST_GIVEN (1u << 0) /* dst_addrs is an INPUT: skip the allocation step */
+#define MP_XFER_DEDUP (1u << 1)     /* receiver matches first, moves only what it lacks (R3) */
+#define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
+#define MP_MATCH_PIN (1u << 5)      /* match: pin matched blocks until mp_unpin (R12) */
+/* Transport selection (benchmarks / comparisons; default AUTO = FUSED). */
+#define MP_XFER_PATH_SHIFT 8
+#define MP_XFER_PATH_MASK (0xFu << MP_XFER_PATH_SHIFT)
+#define MP_XFER_PATH_AUTO (0u << MP_XFER_PATH_SHIFT)
+#define MP_XFER_PATH_FUSED (1u << MP_XFER_PATH_SHIFT)  /* one gather->store kernel, no staging (A6f) */
+#define MP_XFER_PATH_STAGED (2u << MP_XFER_PATH_SHIFT) /* pack -> copy -> unpack (A4, A5, A6) */
+#define MP_XFER_PATH_CE (3u << MP_XFER_PATH_SHIFT)     /* copy engines, one memcpy per chunk (library baseline) */
+/* Swap transport selection (mp_swap_out / mp_swap_in flags argument). */
+#define MP_SWAP_ZERO_COPY (1u << 0) /* SM loads/stores straight to mapped pinned DRAM */
+#define MP_SWAP_CE (2u << 0)        /* pack into device staging + copy-engine D2H/H2D */
+
+typedef struct {
+  int32_t instance_id;  /* < 2^24; encoded in every mp_addr */
+  int32_t device;       /* CUDA ordinal of this instance's HBM */
+  int32_t layers;       /* L   (1..256) */
+  int32_t kv_heads;     /* H */
+  int32_t head_dim;     /* D */
+  int32_t elem_bytes;   /* 2 for fp16/bf16 KV */
+  int32_t block_tokens; /* B (16 in the paper) */
+  int32_t verify;       /* 1: cross-check device allocator ids against the host shadow */
+  int64_t hbm_blocks;   /* N_hbm (< 2^31) */
+  int64_t dram_blocks;  /* N_dram (may be 0) */
+  /* 2*layers device pointers (K_0, V_0, K_1, ...), each >= hbm_blocks*c bytes,
+   * 16-byte aligned, caller-owned (e.g. torch tensors); NULL: the library
+   * allocates one region of 2*L*hbm_blocks*c bytes with cudaMalloc. */
+  void* const* slabs;
+  /* pinned (cudaHostAlloc / cudaHostRegister) host region of dram_blocks*Pb
+   * bytes, caller-owned; NULL: the library cudaHostAllocs it. */
+  void* dram_base;
+  int64_t staging_bytes; /* device staging for the STAGED path (0: 256 MiB) */
+  int32_t staging_slots; /* ring depth (0: 4) */
+  int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = 4 x SMs) */
+} mp_pool_config;
+
+typedef struct {
+  int64_t chunk_bytes, block_bytes; /* c and Pb */
+  int64_t hbm_blocks, dram_blocks, hbm_free, dram_free;
+  int64_t index_blocks;             /* blocks owned by the prompt index */
+  uint64_t clock;                   /* R7 logical clock */
+  uint64_t epoch;                   /* fill counter (content model) */
+  int32_t instance_id, device, layers, block_tokens;
+} mp_pool_info;
+
+typedef struct {
+  uint64_t kernel_launches;   /* migration kernels launched (all flows) */
+  uint64_t bytes_moved;       /* algorithmic payload bytes moved (all flows) */
+  uint64_t blocks_moved;
+  double kernel_ms;           /* summed CUDA-event time of migration kernels (profiling on) */
+  uint64_t timed_launches;    /* launches included in kernel_ms */
+  uint64_t timed_bytes;       /* payload bytes of those launches */
+  uint64_t aux_launches;      /* allocator / free / fill kernels launched */
+} mp_stats;
+
+typedef struct {
+  int32_t kind;        /* 0 = transfer, 1 = transfer_with_insert */
+  int32_t src_instance;
+  int64_t n_addrs;     /* destination addrs delivered with the message */
+  int64_t priv_len;
+} mp_recv_msg;
+
+/* ------------------------------ lifecycle ------------------------------ */
+mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out);
+void mp_pool_destroy(mp_pool* pool);
+/* In-process link (both directions): after this, each pool can name the other
+ * as dst_instance.  Different devices: enables CUDA peer access (NVLink P2P).
+ * Instance ids must differ; shapes (L, H, D, elem, B) must match. */
+mp_status mp_connect(mp_pool* a, mp_pool* b);
+mp_status mp_pool_info_get(const mp_pool* pool, mp_pool_info* out);
+const char* mp_status_str(mp_status s);
+const char* mp_last_error(void); /* thread-local detail of the last failure */
+
+/* ------------------------- memory API ------------------------ */
+/* alloc_mem(size, type, id): the n lowest-index free blocks, ascending; MIXED
+ * takes HBM first then DRAM; on shortage evicts unreferenced
+ * historical blocks of that medium first, else MP_ERR_OOM.  HBM ids
+ * come from the device bitmap allocator.  requester_id is recorded as the
+ * allocating instance.  out: n addrs. */
+mp_status mp_alloc_mem(mp_pool* pool, int64_t n, int32_t type, int32_t requester_id,
+                       mp_addr* out);
+/* free_mem(addrList): only caller-owned (active) blocks; DOUBLE_FREE for a
+ * free block or a repeated addr; PRECONDITION for index-owned blocks. */
+mp_status mp_free_mem(mp_pool* pool, const mp_addr* addrs, int64_t n);
+
+/* ------------------------- index API ------------------------- */
+/* insert(tokenList, addrList, flags): n_addr must be floor(n_tok/B) or
+ * ceil(n_tok/B) (a trailing partial-block addr is ignored); existing prefixes
+ * keep their mapping and the caller's duplicate block is freed (R4);
+ * n_dup_freed (nullable) receives how many were freed. */
+mp_status mp_insert(mp_pool* pool, const mp_token* tokens, int64_t n_tok, const mp_addr* addrs,
+                    int64_t n_addr, uint32_t flags, int64_t* n_dup_freed);
+/* match(tokenList): longest stored block-aligned prefix (R5).  out receives
+ * matched_tokens/B addrs (cap >= floor(n_tok/B) required, else
+ * BUFFER_TOO_SMALL).  MP_MATCH_PIN pins them (R12). */
+mp_status mp_match(mp_pool* pool, const mp_token* tokens, int64_t n_tok, uint32_t flags,
+                   mp_addr* out, int64_t cap, int64_t* matched_tokens);
+mp_status mp_unpin(mp_pool* pool, const mp_addr* addrs, int64_t n);
+/* delete(tokenList): R6 (terminal marker rule); no-op if absent. */
+mp_status mp_delete(mp_pool* pool, const mp_token* tokens, int64_t n_tok);
+/* evict: up to n LRU leaves of `medium` (R8); out_freed cap >= n. */
+mp_status mp_evict(mp_pool* pool, int64_t n, int32_t medium, mp_addr* out_freed,
+                   int64_t* n_freed);
+
+/* --------------------------- swap API ------------------------ */
+/* swap_out(num_blocks): R9 frontier-LRU victims -> pinned DRAM (aggregated
+ * layout), index rewritten, HBM freed.  out_old/out_new: cap >= n. */
+mp_status mp_swap_out(mp_pool* pool, int64_t n, uint32_t flags, mp_addr* out_old,
+                      mp_addr* out_new, int64_t* n_moved);
+/* swap_in(addrList): every addr an allocated DRAM block (else PRECONDITION);
+ * new HBM ids lowest-first in input order (R10).  out_new: n addrs. */
+mp_status mp_swap_in(mp_pool* pool, const mp_addr* addrs, int64_t n, uint32_t flags,
+                     mp_addr* out_new);
+
+/* ------------------------ distributed API -------------------- */
+/* transfer(id, srcAddrList, dstAddrList, flags, private): (1) allocation at
+ * the receiver unless MP_XFER_DST_GIVEN, (2) transmission of layers
+ * [layer_begin, layer_end) of every block (A4-A6 / A10), (3) `private`
+ * (priv, priv_len bytes) queued at the receiver (mp_recv_poll).  src addrs
+ * must be HBM blocks of `src` (R13).  dst_addrs: n entries, output unless
+ * DST_GIVEN. */
+mp_status mp_transfer(mp_pool* src, int32_t dst_instance, const mp_addr* src_addrs, int64_t n,
+                      mp_addr* dst_addrs, uint32_t flags, int32_t layer_begin, int32_t layer_end,
+                      const void* priv, int64_t priv_len);
+/* transfer_with_insert(id, tokenList, srcAddrList, dstAddrList, flags,
+ * private): src addrs cover the LAST n of the ceil(n_tok/B) blocks of tokens
+ * (R3); the receiver allocates, receives and inserts, all layers.
+ * dst_addrs (output, ceil(n_tok/B) entries) receives the final receiver addr
+ * of every block; with MP_XFER_DST_GIVEN it is an INPUT of n entries.
+ * n_moved (nullable): blocks actually moved (fewer with MP_XFER_DEDUP). */
+mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_instance, const mp_token* tokens,
+                                  int64_t n_tok, const mp_addr* src_addrs, int64_t n,
+                                  mp_addr* dst_addrs, uint32_t flags, const void* priv,
+                                  int64_t priv_len, int64_t* n_moved);
+/* Receiver side of `private` delivery: pops the oldest message.  Returns
+ * MP_ERR_PRECONDITION when the queue is empty; BUFFER_TOO_SMALL (message kept)
+ * when priv_cap < priv_len or addr_cap < n_addrs. */
+mp_status mp_recv_poll(mp_pool* dst, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,
+                       mp_addr* addrs, int64_t addr_cap);
+
+/* ---------------- building blocks (A4 pack / A6 unpack) ------------------ */
+/* Gather layers [l0, l1) of n HBM blocks into device buffer `staging`
+ * (aggregated layout [n][l1-l0][2][c]); unpack is the inverse scatter into
+ * caller-owned (active) HBM blocks.  `staging` is a device pointer on the
+ * pool's device of >= n*(l1-l0)*2*c bytes. */
+mp_status mp_pack(mp_pool* pool, const mp_addr* addrs, int64_t n, int32_t l0, int32_t l1,
+                  void* staging);
+mp_status mp_unpack(mp_pool* pool, const void* staging, const mp_addr* addrs, int64_t n,
+                    int32_t l0, int32_t l1);
+
+/* ------------------------- measurement / debug --------------------------- */
+/* Profiling on: every migration kernel is bracketed by CUDA events on its
+ * launching stream; mp_stats accumulates their durations. */
+mp_status mp_profile(mp_pool* pool, int32_t enable);
+mp_status mp_stats_get(const mp_pool* pool, mp_stats* out);
+mp_status mp_stats_reset(mp_pool* pool);
+/* Synthetic KV write (stand-in for the engine's prefill; content model of
+ * DESIGN.md §4): one epoch per call; word t of chunk j of block b becomes
+ * splitmix64(seed ^ splitmix64(inst<<40 | epoch<<14 | b) ^ (j*c/8 + t)).
+ * addrs: allocated HBM blocks, index < 2^14. */
+mp_status mp_debug_fill(mp_pool* pool, const mp_addr* addrs, int64_t n, uint64_t seed);
+/* Copy one block (HBM or DRAM) to host in the aggregated layout (Pb bytes). */
+mp_status mp_debug_read_block(mp_pool* pool, mp_addr addr, void* host_out, int64_t cap);
+/* Sorted text dump of the index, one line per block:
+ * "<depth>\t<medium>\t<idx>\t<last_access>\t<ref>\t<terminal>\t<tok,tok,...>"
+ * where the tokens are the full prefix.  len receives the byte length
+ * (without NUL); BUFFER_TOO_SMALL if cap <= len. */
+mp_status mp_debug_dump_index(mp_pool* pool, char* buf, int64_t cap, int64_t* len);
+/* Host shadow block states (0 free, 1 active, 2 indexed, 3 orphan). */
+mp_status mp_debug_block_states(mp_pool* pool, int32_t medium, uint8_t* out, int64_t cap);
+/* Device bitmap (bit = 1: free) copied to host, (hbm_blocks+31)/32 words. */
+mp_status mp_debug_bitmap(mp_pool* pool, uint32_t* out, int64_t cap_words);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMPOOL_H */

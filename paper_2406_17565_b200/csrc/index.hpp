@@ -1,0 +1,311 @@
+// index.hpp -- host-side prompt index (BASELINE.json north_star item 5).
+//
+// PAPER.md §4.2: MemPool "utilizes the radix tree proposed by
+// SGLang" extended to "reference data located anywhere in the system" (HBM or
+// DRAM) with block granularity equal to the engine's ("our radix tree nodes
+// point to KV cache blocks of 16 tokens").  Here every node is one B-token
+// chunk (block-chunk-keyed radix tree): children are found through a hash of
+// (parent, chunk tokens) with token-by-token equality confirmation, so a walk
+// of k blocks costs k hash probes.
+//
+// Policies where the paper is silent: R5 match, R6 delete
+// (terminal markers), R7 logical clock, R8 leaf-LRU evict with (last_access,
+// block index) tie-break, R9 HBM-frontier LRU for swap-out victims.  The two
+// candidate sets are kept incrementally so a pick is O(log n).
+#pragma once
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+namespace mpi {
+
+struct Node {
+  Node* parent = nullptr;
+  std::vector<Node*> kids;       // children (any medium)
+  int32_t pos_in_parent = -1;    // index in parent->kids
+  std::vector<int32_t> chunk;    // the B tokens of this block
+  uint64_t hkey = 0;             // key in the child hash map
+  int32_t medium = 0, idx = -1;  // where the KV block lives ("anywhere")
+  uint64_t last_access = 0;      // R7
+  int32_t ref = 0;               // R12 pins
+  bool terminal = false;         // R6
+  int32_t n_hbm_kids = 0;
+  uint64_t id = 0;
+  // membership in the candidate sets
+  bool in_leaf = false, in_front = false;
+  int32_t leaf_medium = 0;
+  std::pair<uint64_t, int32_t> leaf_key{0, 0}, front_key{0, 0};
+};
+
+using Key = std::pair<uint64_t, int32_t>;  // (last_access, block index)
+
+class Index {
+ public:
+  explicit Index(int B, int64_t n_hbm, int64_t n_dram) : B_(B) {
+    owner_[0].assign((size_t)n_hbm, nullptr);
+    owner_[1].assign((size_t)n_dram, nullptr);
+    root_.id = next_id_++;
+  }
+  ~Index() { clear(); }
+  Index(const Index&) = delete;
+  Index& operator=(const Index&) = delete;
+
+  int block_tokens() const { return B_; }
+  uint64_t clock() const { return clock_; }
+  uint64_t tick() { return ++clock_; }
+  size_t size() const { return size_; }
+  Node* owner(int medium, int32_t idx) const { return owner_[medium][(size_t)idx]; }
+
+  // Existing nodes of prefixes 1..k (stops at the first missing one).
+  std::vector<Node*> path(const int32_t* toks, int64_t k) const {
+    std::vector<Node*> out;
+    const Node* p = &root_;
+    for (int64_t i = 0; i < k; ++i) {
+      Node* c = find_child(p, toks + i * B_);
+      if (!c) break;
+      out.push_back(c);
+      p = c;
+    }
+    return out;
+  }
+
+  // R5 without side effects.
+  int64_t peek(const int32_t* toks, int64_t n_tok) const {
+    return (int64_t)path(toks, n_tok / B_).size();
+  }
+
+  // R5 + R7 (+ R12 when pin): touches matched nodes with a fresh tick.
+  std::vector<Node*> match(const int32_t* toks, int64_t n_tok, bool pin) {
+    const uint64_t t = tick();
+    std::vector<Node*> p = path(toks, n_tok / B_);
+    for (Node* n : p) {
+      n->last_access = t;
+      if (pin) ++n->ref;
+      refresh(n);
+    }
+    return p;
+  }
+
+  void touch(Node* n, uint64_t t) {
+    n->last_access = t;
+    refresh(n);
+  }
+  void set_ref(Node* n, int32_t r) {
+    n->ref = r;
+    refresh(n);
+  }
+
+  // New child under parent (nullptr = root) for chunk toks.
+  Node* add(Node* parent, const int32_t* toks, int medium, int32_t idx, uint64_t t) {
+    Node* p = parent ? parent : &root_;
+    Node* n = new Node();
+    n->parent = p;
+    n->chunk.assign(toks, toks + B_);
+    n->hkey = mix(p->id, hash_chunk(toks));
+    n->medium = medium;
+    n->idx = idx;
+    n->last_access = t;
+    n->id = next_id_++;
+    n->pos_in_parent = (int32_t)p->kids.size();
+    p->kids.push_back(n);
+    if (medium == 0) ++p->n_hbm_kids;
+    map_.emplace(n->hkey, n);
+    owner_[medium][(size_t)idx] = n;
+    ++size_;
+    refresh(p);
+    refresh(n);
+    return n;
+  }
+
+  // Unlink a childless node; returns its (medium, idx, ref).
+  void unlink(Node* n) {
+    Node* p = n->parent;
+    auto range = map_.equal_range(n->hkey);
+    for (auto it = range.first; it != range.second; ++it)
+      if (it->second == n) {
+        map_.erase(it);
+        break;
+      }
+    Node* last = p->kids.back();
+    p->kids[(size_t)n->pos_in_parent] = last;
+    last->pos_in_parent = n->pos_in_parent;
+    p->kids.pop_back();
+    if (n->medium == 0) --p->n_hbm_kids;
+    drop_from_sets(n);
+    owner_[n->medium][(size_t)n->idx] = nullptr;
+    --size_;
+    refresh(p);
+    delete n;
+  }
+
+  // Move a node's KV to another medium/block (swap): keeps its place in the tree.
+  void rebind(Node* n, int medium, int32_t idx) {
+    Node* p = n->parent;
+    owner_[n->medium][(size_t)n->idx] = nullptr;
+    if (n->medium == 0) --p->n_hbm_kids;
+    n->medium = medium;
+    n->idx = idx;
+    if (medium == 0) ++p->n_hbm_kids;
+    owner_[medium][(size_t)idx] = n;
+    refresh(n);
+    refresh(p);
+  }
+
+  // R8: least (last_access, idx) leaf of `medium` with ref == 0, or nullptr.
+  Node* lru_leaf(int medium) const {
+    if (leaves_[medium].empty()) return nullptr;
+    return owner_[medium][(size_t)leaves_[medium].begin()->second];
+  }
+  // R9: least (last_access, idx) HBM node with ref == 0 and no HBM child.
+  Node* lru_frontier() const {
+    if (front_.empty()) return nullptr;
+    return owner_[0][(size_t)front_.begin()->second];
+  }
+
+  // Number of nodes of `medium` that repeated leaf eviction could remove:
+  // medium matches, ref == 0, not on `pinned_path`, and every child is
+  // itself eventually evictable (R2 feasibility).
+  int64_t evictable(int medium, const std::vector<Node*>& pinned_path) const {
+    std::vector<const Node*> order;
+    std::vector<const Node*> stack{&root_};
+    while (!stack.empty()) {
+      const Node* n = stack.back();
+      stack.pop_back();
+      order.push_back(n);
+      for (const Node* c : n->kids) stack.push_back(c);
+    }
+    std::unordered_map<const Node*, bool> ok;
+    ok.reserve(order.size() * 2);
+    int64_t count = 0;
+    for (auto it = order.rbegin(); it != order.rend(); ++it) {
+      const Node* n = *it;
+      if (n == &root_) continue;
+      bool e = n->medium == medium && n->ref == 0 &&
+               std::find(pinned_path.begin(), pinned_path.end(), n) == pinned_path.end();
+      for (const Node* c : n->kids)
+        if (!ok[c]) e = false;
+      ok[n] = e;
+      if (e) ++count;
+    }
+    return count;
+  }
+
+  // Sorted text dump (mempool.h mp_debug_dump_index).
+  std::string dump() const {
+    std::vector<std::pair<std::vector<int32_t>, std::string>> rows;
+    std::vector<std::pair<const Node*, std::vector<int32_t>>> stack;
+    for (const Node* c : root_.kids) stack.push_back({c, {}});
+    while (!stack.empty()) {
+      auto [n, pre] = stack.back();
+      stack.pop_back();
+      pre.insert(pre.end(), n->chunk.begin(), n->chunk.end());
+      std::string line = std::to_string(pre.size() / (size_t)B_) + "\t" + std::to_string(n->medium) +
+                         "\t" + std::to_string(n->idx) + "\t" + std::to_string(n->last_access) +
+                         "\t" + std::to_string(n->ref) + "\t" + (n->terminal ? "1" : "0") + "\t";
+      for (size_t i = 0; i < pre.size(); ++i) {
+        if (i) line += ",";
+        line += std::to_string(pre[i]);
+      }
+      line += "\n";
+      rows.push_back({pre, line});
+      for (const Node* c : n->kids) stack.push_back({c, pre});
+    }
+    std::sort(rows.begin(), rows.end(),
+              [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::string out;
+    for (auto& r : rows) out += r.second;
+    return out;
+  }
+
+  void clear() {
+    std::vector<Node*> stack(root_.kids.begin(), root_.kids.end());
+    while (!stack.empty()) {
+      Node* n = stack.back();
+      stack.pop_back();
+      for (Node* c : n->kids) stack.push_back(c);
+      delete n;
+    }
+    root_.kids.clear();
+    root_.n_hbm_kids = 0;
+    map_.clear();
+    leaves_[0].clear();
+    leaves_[1].clear();
+    front_.clear();
+    for (auto& o : owner_) std::fill(o.begin(), o.end(), nullptr);
+    size_ = 0;
+  }
+
+  Node* root() { return &root_; }
+
+ private:
+  static uint64_t hash_chunk_n(const int32_t* t, int n) {
+    uint64_t h = 1469598103934665603ull;
+    for (int i = 0; i < n; ++i) {
+      h ^= (uint32_t)t[i];
+      h *= 1099511628211ull;
+      h ^= h >> 29;
+    }
+    return h;
+  }
+  uint64_t hash_chunk(const int32_t* t) const { return hash_chunk_n(t, B_); }
+  static uint64_t mix(uint64_t a, uint64_t b) {
+    uint64_t z = a * 0x9E3779B97F4A7C15ull ^ (b + 0x632BE59BD9B4E019ull + (a << 6) + (a >> 2));
+    z ^= z >> 31;
+    return z;
+  }
+
+  Node* find_child(const Node* p, const int32_t* toks) const {
+    auto range = map_.equal_range(mix(p->id, hash_chunk(toks)));
+    for (auto it = range.first; it != range.second; ++it) {
+      Node* c = it->second;
+      if (c->parent == p && std::memcmp(c->chunk.data(), toks, sizeof(int32_t) * B_) == 0)
+        return c;
+    }
+    return nullptr;
+  }
+
+  void drop_from_sets(Node* n) {
+    if (n->in_leaf) {
+      leaves_[n->leaf_medium].erase(n->leaf_key);
+      n->in_leaf = false;
+    }
+    if (n->in_front) {
+      front_.erase(n->front_key);
+      n->in_front = false;
+    }
+  }
+
+  void refresh(Node* n) {
+    if (n == &root_) return;
+    drop_from_sets(n);
+    if (n->ref == 0 && n->kids.empty()) {
+      n->leaf_key = {n->last_access, n->idx};
+      n->leaf_medium = n->medium;
+      leaves_[n->medium].insert(n->leaf_key);
+      n->in_leaf = true;
+    }
+    if (n->ref == 0 && n->medium == 0 && n->n_hbm_kids == 0) {
+      n->front_key = {n->last_access, n->idx};
+      front_.insert(n->front_key);
+      n->in_front = true;
+    }
+  }
+
+  int B_;
+  Node root_;
+  std::unordered_multimap<uint64_t, Node*> map_;
+  std::set<Key> leaves_[2];
+  std::set<Key> front_;
+  std::vector<Node*> owner_[2];
+  uint64_t clock_ = 0;
+  uint64_t next_id_ = 1;
+  size_t size_ = 0;
+};
+
+}  // namespace mpi

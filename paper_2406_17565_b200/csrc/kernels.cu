@@ -1,0 +1,226 @@
+// kernels.cu -- sm_100a kernels of libmempool.
+//
+//  * migrate_kernel : the KV-block gather/scatter of the migration path --
+//    pack (A4, pool -> aggregated staging), unpack (A6, staging -> pool), the
+//    fused gather -> (peer) store (A6f, pool -> pool, P2P over NVLink when the
+//    destination slabs live on a peer GPU) and swap (A8/A9, pool <-> mapped
+//    pinned DRAM).  HBM-bound: every chunk is a contiguous run of c bytes
+//    (c = B*H*D*2 = 128 KiB at Llama-2-7B), so each warp streams 4 KiB
+//    pieces with 8 independent 16-byte loads in flight per lane.
+//  * alloc_kernel / free_kernel : the device-resident block allocator
+//    (BASELINE.json north_star item 1) over a bitmap, lowest-first.
+//  * fill_kernel : test/bench-only synthetic KV writer (content model).
+#include "kernels.cuh"
+
+namespace mpk {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kVec = 8;                      // 16-byte vectors per lane per unit
+constexpr int kUnitBytes = 32 * kVec * 16;   // 4 KiB per warp-unit
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <bool kSrcPool, bool kDstPool>
+__global__ void __launch_bounds__(kThreads) migrate_kernel(Endpoint src, Endpoint dst, int j0,
+                                                           int nj, long long chunk,
+                                                           unsigned units_per_chunk,
+                                                           unsigned total_units) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned warp = (blockIdx.x * (unsigned)kThreads + threadIdx.x) >> 5;
+  const unsigned nwarps = (gridDim.x * (unsigned)kThreads) >> 5;
+  const bool full_units = (chunk % kUnitBytes) == 0;
+  for (unsigned u = warp; u < total_units; u += nwarps) {
+    const unsigned ch = u / units_per_chunk;
+    const unsigned part = u - ch * units_per_chunk;
+    const unsigned i = ch / (unsigned)nj;
+    const unsigned jr = ch - i * (unsigned)nj;
+    const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
+    const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
+    const char* sp = kSrcPool ? (const char*)__ldg((const unsigned long long*)(src.slabs + j0 + jr)) + sid * chunk
+                              : src.base + sid * src.stride + (long long)jr * chunk;
+    char* dp = kDstPool ? (char*)__ldg((const unsigned long long*)(dst.slabs + j0 + jr)) + did * chunk
+                        : dst.base + did * dst.stride + (long long)jr * chunk;
+    const long long off = (long long)part * kUnitBytes + lane * 16;
+    uint4 v[kVec];
+    if (full_units) {
+#pragma unroll
+      for (int k = 0; k < kVec; ++k) v[k] = ld_stream(sp + off + k * 512);
+#pragma unroll
+      for (int k = 0; k < kVec; ++k) st_stream(dp + off + k * 512, v[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kVec; ++k)
+        if (off + k * 512 < chunk) v[k] = ld_stream(sp + off + k * 512);
+#pragma unroll
+      for (int k = 0; k < kVec; ++k)
+        if (off + k * 512 < chunk) st_stream(dp + off + k * 512, v[k]);
+    }
+  }
+}
+
+// Single CTA of 1024 threads: popcount per thread-range of words, block-wide
+// exclusive scan, then every thread emits its lowest set bits in order, so
+// the ids come out ascending (R2 lowest-first).
+__global__ void __launch_bounds__(1024) alloc_kernel(uint32_t* bitmap, int nwords, int n,
+                                                     int* out_dev, int* out_host, int* err) {
+  __shared__ int warp_tot[32];
+  const int t = threadIdx.x;
+  const int wpt = (nwords + blockDim.x - 1) / blockDim.x;
+  const int w0 = min(nwords, t * wpt), w1 = min(nwords, w0 + wpt);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(bitmap[w]);
+  // inclusive warp scan
+  const int lane = t & 31, wid = t >> 5;
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_tot[lane] = s;  // inclusive scan of warp totals
+  }
+  __syncthreads();
+  const int base = x - cnt + (wid > 0 ? warp_tot[wid - 1] : 0);
+  const int total = warp_tot[(blockDim.x >> 5) - 1];
+  if (t == 0 && total < n) *err = 1;
+  if (total < n) return;
+  int k = base;
+  for (int w = w0; w < w1 && k < n; ++w) {
+    uint32_t bits = bitmap[w];
+    uint32_t taken = 0;
+    while (bits && k < n) {
+      const int b = __ffs(bits) - 1;
+      const int id = w * 32 + b;
+      out_dev[k] = id;
+      if (out_host) out_host[k] = id;
+      ++k;
+      taken |= 1u << b;
+      bits &= bits - 1;
+    }
+    bitmap[w] &= ~taken;
+  }
+}
+
+__global__ void free_kernel(uint32_t* bitmap, const int* ids, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int id = ids[i];
+    atomicOr(bitmap + (id >> 5), 1u << (id & 31));
+  }
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_kernel(char* const* slabs, const int* ids, int nchunks, long long chunk,
+                            unsigned long long seed, unsigned long long inst,
+                            unsigned long long epoch, unsigned long long total_pairs) {
+  const unsigned long long pairs_per_chunk = (unsigned long long)chunk / 16;
+  const unsigned long long words_per_chunk = (unsigned long long)chunk / 8;
+  for (unsigned long long g = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       g < total_pairs; g += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long p = g % pairs_per_chunk;
+    const unsigned long long cj = g / pairs_per_chunk;
+    const unsigned long long j = cj % nchunks;
+    const unsigned long long i = cj / nchunks;
+    const unsigned long long b = (unsigned long long)ids[i];
+    const unsigned long long tag = (inst << 40) | (epoch << 14) | b;
+    const unsigned long long base = seed ^ splitmix64(tag);
+    const unsigned long long t = 2 * p;
+    const unsigned long long w0 = splitmix64(base ^ (j * words_per_chunk + t));
+    const unsigned long long w1 = splitmix64(base ^ (j * words_per_chunk + t + 1));
+    ulonglong2* dst = (ulonglong2*)(slabs[j] + b * chunk) + p;
+    *dst = make_ulonglong2(w0, w1);
+  }
+}
+
+}  // namespace
+
+int sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) v = 148;
+  return v > 0 ? v : 148;
+}
+
+cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
+                           long long chunk, int max_ctas, cudaStream_t stream) {
+  if (n <= 0 || nj <= 0) return cudaSuccess;
+  const unsigned units_per_chunk = (unsigned)((chunk + kUnitBytes - 1) / kUnitBytes);
+  const unsigned long long total = (unsigned long long)n * nj * units_per_chunk;
+  if (total >= (1ull << 32)) return cudaErrorInvalidValue;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int cap = max_ctas > 0 ? max_ctas : 4 * sm_count(dev);
+  const unsigned long long want = (total + (kThreads / 32) - 1) / (kThreads / 32);
+  const int grid = (int)(want < (unsigned long long)cap ? want : (unsigned long long)cap);
+  const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
+  if (sp && dp)
+    migrate_kernel<true, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
+                                                              units_per_chunk, (unsigned)total);
+  else if (sp)
+    migrate_kernel<true, false><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
+                                                               units_per_chunk, (unsigned)total);
+  else if (dp)
+    migrate_kernel<false, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
+                                                               units_per_chunk, (unsigned)total);
+  else
+    migrate_kernel<false, false><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
+                                                                units_per_chunk, (unsigned)total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,
+                         int* err, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  alloc_kernel<<<1, 1024, 0, stream>>>(bitmap, nwords, n, out_dev, out_host, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_free(uint32_t* bitmap, const int* ids, int n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (n + 255) / 256 < 148 ? (n + 255) / 256 : 148;
+  free_kernel<<<grid, 256, 0, stream>>>(bitmap, ids, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(char* const* slabs, const int* ids, int n, int nchunks, long long chunk,
+                        unsigned long long seed, unsigned long long inst,
+                        unsigned long long epoch, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned long long total = (unsigned long long)n * nchunks * (chunk / 16);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long want = (total + 255) / 256;
+  const unsigned long long cap = 8ull * sm_count(dev);
+  fill_kernel<<<(int)(want < cap ? want : cap), 256, 0, stream>>>(slabs, ids, nchunks, chunk,
+                                                                  seed, inst, epoch, total);
+  return cudaGetLastError();
+}
+
+}  // namespace mpk

@@ -1,0 +1,49 @@
+// kernels.cuh -- launchers of the sm_100a kernels of libmempool (internal).
+//
+// Data-movement only: no tensor cores (BASELINE.json north_star "pure data
+// movement path").  All kernels are written for B200: 148 SMs, 16-byte
+// vector loads with L1::no_allocate, grids sized in multiples of the SM count.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpk {
+
+// One side of a block copy.
+//   POOL side: chunk j of block b lives at slabs[j] + b * chunk   (per-layer
+//              paged layout, "two blocks per LLM layer").
+//   AGG side : chunk jr (relative to the copied layer range) of block b lives
+//              at base + b * stride + jr * chunk  (aggregated layout).
+// ids == nullptr means the identity (block i of the copy is id i).
+struct Endpoint {
+  char* const* slabs;  // device array of 2L slab pointers (POOL), else nullptr
+  char* base;          // AGG base (device or mapped pinned host), else nullptr
+  long long stride;    // AGG bytes per block
+  const int* ids;      // device array of n ids or nullptr
+};
+
+// dst.chunk(ids_d[i], j) = src.chunk(ids_s[i], j) for i < n, j in [j0, j0+nj).
+// max_ctas <= 0: auto (4 CTAs per SM).
+cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
+                           long long chunk, int max_ctas, cudaStream_t stream);
+
+// Lowest-first allocation of n blocks from a bitmap (bit = 1: free).  Writes
+// the ids ascending into out_dev (device) and out_host (mapped pinned host,
+// may be nullptr), clears their bits.  *err (device) := 1 if fewer than n
+// were free (the host shadow makes this impossible; checked in verify mode).
+cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,
+                         int* err, cudaStream_t stream);
+
+// Sets the bits of ids[0..n) (device array).
+cudaError_t launch_free(uint32_t* bitmap, const int* ids, int n, cudaStream_t stream);
+
+// Synthetic KV write of n blocks (content model):
+// word t of chunk j of block b = splitmix64(seed ^ splitmix64(inst<<40 |
+// epoch<<14 | b) ^ (j * chunk/8 + t)).
+cudaError_t launch_fill(char* const* slabs, const int* ids, int n, int nchunks, long long chunk,
+                        unsigned long long seed, unsigned long long inst,
+                        unsigned long long epoch, cudaStream_t stream);
+
+int sm_count(int device);
+
+}  // namespace mpk

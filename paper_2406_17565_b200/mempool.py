@@ -1,0 +1,397 @@
+"""Thin ctypes binding of libmempool.so (include/mempool.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+C++ runtime and sm_100a kernels.  There is no fallback -- importing this
+module fails loudly when the library is missing.
+
+Names follow the paper's MemPool API (PAPER.md Table tbl-mempool-api,
+P:261-290): alloc_mem, free_mem, insert, match, delete, swap_out, swap_in,
+transfer, transfer_with_insert (+ evict).
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libmempool.so")
+
+HBM, DRAM, MIXED = 0, 1, 2
+
+XFER_DST_GIVEN = 1 << 0
+XFER_DEDUP = 1 << 1
+INS_ERR_ON_CONFLICT = 1 << 4
+MATCH_PIN = 1 << 5
+PATH_AUTO = 0 << 8
+PATH_FUSED = 1 << 8
+PATH_STAGED = 2 << 8
+PATH_CE = 3 << 8
+SWAP_ZERO_COPY = 1
+SWAP_CE = 2
+
+STATUS = {
+    0: "OK", -1: "OOM", -2: "DOUBLE_FREE", -3: "INVALID_ADDR", -4: "ADDR_COUNT",
+    -5: "CONFLICT", -6: "NO_DRAM", -7: "DST_OOM", -8: "DST_UNREACHABLE",
+    -9: "PRECONDITION", -10: "PREFIX_MISSING", -11: "CONFIG", -12: "BUFFER_TOO_SMALL",
+    -13: "CUDA", -14: "NCCL", -15: "INTERNAL",
+}
+
+
+class MempoolError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{where}: MP_ERR_{self.name}" + (f" ({detail})" if detail else ""))
+
+
+def make_addr(inst: int, medium: int, idx: int) -> int:
+    return (inst << 40) | ((medium & 0xFF) << 32) | (idx & 0xFFFFFFFF)
+
+
+def addr_inst(a) -> int:
+    return int(a) >> 40
+
+
+def addr_medium(a) -> int:
+    return (int(a) >> 32) & 0xFF
+
+
+def addr_index(a) -> int:
+    return int(a) & 0xFFFFFFFF
+
+
+def addr_indices(addrs) -> np.ndarray:
+    return (np.asarray(addrs, np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
+
+
+def addr_media(addrs) -> np.ndarray:
+    return ((np.asarray(addrs, np.uint64) >> np.uint64(32)) & np.uint64(0xFF)).astype(np.int64)
+
+
+class PoolConfig(C.Structure):
+    _fields_ = [
+        ("instance_id", C.c_int32), ("device", C.c_int32), ("layers", C.c_int32),
+        ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("elem_bytes", C.c_int32),
+        ("block_tokens", C.c_int32), ("verify", C.c_int32),
+        ("hbm_blocks", C.c_int64), ("dram_blocks", C.c_int64),
+        ("slabs", C.POINTER(C.c_void_p)), ("dram_base", C.c_void_p),
+        ("staging_bytes", C.c_int64), ("staging_slots", C.c_int32), ("max_ctas", C.c_int32),
+    ]
+
+
+class PoolInfo(C.Structure):
+    _fields_ = [
+        ("chunk_bytes", C.c_int64), ("block_bytes", C.c_int64), ("hbm_blocks", C.c_int64),
+        ("dram_blocks", C.c_int64), ("hbm_free", C.c_int64), ("dram_free", C.c_int64),
+        ("index_blocks", C.c_int64), ("clock", C.c_uint64), ("epoch", C.c_uint64),
+        ("instance_id", C.c_int32), ("device", C.c_int32), ("layers", C.c_int32),
+        ("block_tokens", C.c_int32),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("kernel_launches", C.c_uint64), ("bytes_moved", C.c_uint64),
+        ("blocks_moved", C.c_uint64), ("kernel_ms", C.c_double),
+        ("timed_launches", C.c_uint64), ("timed_bytes", C.c_uint64),
+        ("aux_launches", C.c_uint64),
+    ]
+
+
+class RecvMsg(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("src_instance", C.c_int32), ("n_addrs", C.c_int64),
+                ("priv_len", C.c_int64)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+_U32 = C.c_uint32
+_U64 = C.c_uint64
+_PU64 = C.POINTER(C.c_uint64)
+_PI32 = C.POINTER(C.c_int32)
+_PI64 = C.POINTER(C.c_int64)
+
+# name -> (restype, argtypes); the list is also the export check of the tests.
+SIGNATURES = {
+    "mp_pool_create": (_I32, [C.POINTER(PoolConfig), C.POINTER(_P)]),
+    "mp_pool_destroy": (None, [_P]),
+    "mp_connect": (_I32, [_P, _P]),
+    "mp_pool_info_get": (_I32, [_P, C.POINTER(PoolInfo)]),
+    "mp_status_str": (C.c_char_p, [_I32]),
+    "mp_last_error": (C.c_char_p, []),
+    "mp_alloc_mem": (_I32, [_P, _I64, _I32, _I32, _PU64]),
+    "mp_free_mem": (_I32, [_P, _PU64, _I64]),
+    "mp_insert": (_I32, [_P, _PI32, _I64, _PU64, _I64, _U32, _PI64]),
+    "mp_match": (_I32, [_P, _PI32, _I64, _U32, _PU64, _I64, _PI64]),
+    "mp_unpin": (_I32, [_P, _PU64, _I64]),
+    "mp_delete": (_I32, [_P, _PI32, _I64]),
+    "mp_evict": (_I32, [_P, _I64, _I32, _PU64, _PI64]),
+    "mp_swap_out": (_I32, [_P, _I64, _U32, _PU64, _PU64, _PI64]),
+    "mp_swap_in": (_I32, [_P, _PU64, _I64, _U32, _PU64]),
+    "mp_transfer": (_I32, [_P, _I32, _PU64, _I64, _PU64, _U32, _I32, _I32, _P, _I64]),
+    "mp_transfer_with_insert": (_I32, [_P, _I32, _PI32, _I64, _PU64, _I64, _PU64, _U32, _P,
+                                       _I64, _PI64]),
+    "mp_recv_poll": (_I32, [_P, C.POINTER(RecvMsg), _P, _I64, _PU64, _I64]),
+    "mp_pack": (_I32, [_P, _PU64, _I64, _I32, _I32, _P]),
+    "mp_unpack": (_I32, [_P, _P, _PU64, _I64, _I32, _I32]),
+    "mp_profile": (_I32, [_P, _I32]),
+    "mp_stats_get": (_I32, [_P, C.POINTER(Stats)]),
+    "mp_stats_reset": (_I32, [_P]),
+    "mp_debug_fill": (_I32, [_P, _PU64, _I64, _U64]),
+    "mp_debug_read_block": (_I32, [_P, _U64, _P, _I64]),
+    "mp_debug_dump_index": (_I32, [_P, C.c_char_p, _I64, _PI64]),
+    "mp_debug_block_states": (_I32, [_P, _I32, C.POINTER(C.c_uint8), _I64]),
+    "mp_debug_bitmap": (_I32, [_P, C.POINTER(C.c_uint32), _I64]),
+}
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(
+            f"libmempool.so not found at {path}; build it with "
+            "`python -m paper_2406_17565_b200.build` (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = load_library()
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        detail = _lib.mp_last_error().decode() if st in (-13, -14, -15) else ""
+        raise MempoolError(st, where, detail)
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64).reshape(-1))
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+
+
+def _pu64(a: np.ndarray):
+    return a.ctypes.data_as(_PU64)
+
+
+def _pi32(a: np.ndarray):
+    return a.ctypes.data_as(_PI32)
+
+
+class Pool:
+    """One serving instance's MemPool."""
+
+    def __init__(self, instance_id: int, device: int, layers: int, kv_heads: int,
+                 head_dim: int, block_tokens: int, hbm_blocks: int, dram_blocks: int = 0,
+                 elem_bytes: int = 2, slabs=None, dram_base=None, staging_bytes: int = 0,
+                 staging_slots: int = 0, max_ctas: int = 0, verify: bool = False):
+        self.inst = instance_id
+        self.B = block_tokens
+        self.L = layers
+        self._slab_arr = None
+        cfg = PoolConfig(instance_id, device, layers, kv_heads, head_dim, elem_bytes,
+                         block_tokens, int(verify), hbm_blocks, dram_blocks, None,
+                         dram_base, staging_bytes, staging_slots, max_ctas)
+        if slabs is not None:
+            assert len(slabs) == 2 * layers
+            self._slab_arr = (C.c_void_p * len(slabs))(*[int(s) for s in slabs])
+            cfg.slabs = C.cast(self._slab_arr, C.POINTER(C.c_void_p))
+        h = C.c_void_p()
+        _check(_lib.mp_pool_create(C.byref(cfg), C.byref(h)), "mp_pool_create")
+        self._h = h
+        info = self.info()
+        self.chunk_bytes = info.chunk_bytes
+        self.block_bytes = info.block_bytes
+        self.hbm_blocks = info.hbm_blocks
+        self.dram_blocks = info.dram_blocks
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.mp_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> PoolInfo:
+        o = PoolInfo()
+        _check(_lib.mp_pool_info_get(self._h, C.byref(o)), "mp_pool_info_get")
+        return o
+
+    # -------------------------------------------------------------- memory API
+    def alloc_mem(self, n: int, medium: int = HBM, requester: int = None) -> np.ndarray:
+        out = np.zeros(max(n, 1), np.uint64)
+        req = self.inst if requester is None else requester
+        _check(_lib.mp_alloc_mem(self._h, n, medium, req, _pu64(out)), "alloc_mem")
+        return out[:n]
+
+    def free_mem(self, addrs):
+        a = _u64(addrs)
+        _check(_lib.mp_free_mem(self._h, _pu64(a), len(a)), "free_mem")
+
+    # --------------------------------------------------------------- index API
+    def insert(self, tokens, addrs, flags: int = 0) -> int:
+        t, a = _i32(tokens), _u64(addrs)
+        dup = C.c_int64(0)
+        _check(_lib.mp_insert(self._h, _pi32(t), len(t), _pu64(a), len(a), flags,
+                              C.byref(dup)), "insert")
+        return dup.value
+
+    def match(self, tokens, flags: int = 0):
+        t = _i32(tokens)
+        out = np.zeros(max(len(t) // self.B, 1), np.uint64)
+        mt = C.c_int64(0)
+        _check(_lib.mp_match(self._h, _pi32(t), len(t), flags, _pu64(out), len(out),
+                             C.byref(mt)), "match")
+        return mt.value, out[: mt.value // self.B]
+
+    def unpin(self, addrs):
+        a = _u64(addrs)
+        _check(_lib.mp_unpin(self._h, _pu64(a), len(a)), "unpin")
+
+    def delete(self, tokens):
+        t = _i32(tokens)
+        _check(_lib.mp_delete(self._h, _pi32(t), len(t)), "delete")
+
+    def evict(self, n: int, medium: int = HBM) -> np.ndarray:
+        out = np.zeros(max(n, 1), np.uint64)
+        k = C.c_int64(0)
+        _check(_lib.mp_evict(self._h, n, medium, _pu64(out), C.byref(k)), "evict")
+        return out[: k.value]
+
+    # ---------------------------------------------------------------- swap API
+    def swap_out(self, n: int, flags: int = 0):
+        old = np.zeros(max(n, 1), np.uint64)
+        new = np.zeros(max(n, 1), np.uint64)
+        k = C.c_int64(0)
+        _check(_lib.mp_swap_out(self._h, n, flags, _pu64(old), _pu64(new), C.byref(k)),
+               "swap_out")
+        return old[: k.value], new[: k.value]
+
+    def swap_in(self, addrs, flags: int = 0) -> np.ndarray:
+        a = _u64(addrs)
+        out = np.zeros(max(len(a), 1), np.uint64)
+        _check(_lib.mp_swap_in(self._h, _pu64(a), len(a), flags, _pu64(out)), "swap_in")
+        return out[: len(a)]
+
+    # --------------------------------------------------------- distributed API
+    def transfer(self, dst_instance: int, src_addrs, dst_addrs=None, flags: int = 0,
+                 layer_begin: int = 0, layer_end: int = None, priv: bytes = b"") -> np.ndarray:
+        s = _u64(src_addrs)
+        if dst_addrs is not None:
+            d = _u64(dst_addrs).copy()
+            flags |= XFER_DST_GIVEN
+        else:
+            d = np.zeros(max(len(s), 1), np.uint64)
+        le = self.L if layer_end is None else layer_end
+        pb = C.create_string_buffer(bytes(priv), len(priv)) if priv else None
+        _check(_lib.mp_transfer(self._h, dst_instance, _pu64(s), len(s), _pu64(d), flags,
+                                layer_begin, le, pb, len(priv)), "transfer")
+        return d[: len(s)]
+
+    def transfer_with_insert(self, dst_instance: int, tokens, src_addrs, dst_addrs=None,
+                             flags: int = 0, priv: bytes = b""):
+        t, s = _i32(tokens), _u64(src_addrs)
+        ceil_b = -(-len(t) // self.B)
+        if dst_addrs is not None:
+            d = _u64(dst_addrs)
+            d = np.concatenate([d, np.zeros(max(0, ceil_b - len(d)), np.uint64)])
+            flags |= XFER_DST_GIVEN
+        else:
+            d = np.zeros(max(ceil_b, 1), np.uint64)
+        moved = C.c_int64(0)
+        pb = C.create_string_buffer(bytes(priv), len(priv)) if priv else None
+        _check(_lib.mp_transfer_with_insert(self._h, dst_instance, _pi32(t), len(t), _pu64(s),
+                                            len(s), _pu64(d), flags, pb, len(priv),
+                                            C.byref(moved)), "transfer_with_insert")
+        return d[:ceil_b], moved.value
+
+    def recv_poll(self):
+        m = RecvMsg()
+        st = _lib.mp_recv_poll(self._h, C.byref(m), None, 0, None, 0)
+        if st == -9:
+            return None
+        if st not in (0, -12):
+            _check(st, "recv_poll")
+        pb = C.create_string_buffer(max(m.priv_len, 1))
+        ad = np.zeros(max(m.n_addrs, 1), np.uint64)
+        _check(_lib.mp_recv_poll(self._h, C.byref(m), pb, m.priv_len, _pu64(ad), len(ad)),
+               "recv_poll")
+        return m.kind, m.src_instance, pb.raw[: m.priv_len], ad[: m.n_addrs]
+
+    # ----------------------------------------------------- building blocks
+    def pack(self, addrs, layer_begin: int, layer_end: int, staging_ptr: int):
+        a = _u64(addrs)
+        _check(_lib.mp_pack(self._h, _pu64(a), len(a), layer_begin, layer_end,
+                            C.c_void_p(staging_ptr)), "pack")
+
+    def unpack(self, staging_ptr: int, addrs, layer_begin: int, layer_end: int):
+        a = _u64(addrs)
+        _check(_lib.mp_unpack(self._h, C.c_void_p(staging_ptr), _pu64(a), len(a), layer_begin,
+                              layer_end), "unpack")
+
+    # ---------------------------------------------------- measurement / debug
+    def profile(self, enable: bool = True):
+        _check(_lib.mp_profile(self._h, int(enable)), "profile")
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(_lib.mp_stats_get(self._h, C.byref(s)), "stats")
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def stats_reset(self):
+        _check(_lib.mp_stats_reset(self._h), "stats_reset")
+
+    def debug_fill(self, addrs, seed: int):
+        a = _u64(addrs)
+        _check(_lib.mp_debug_fill(self._h, _pu64(a), len(a), seed), "debug_fill")
+
+    def debug_read_block(self, addr) -> np.ndarray:
+        out = np.zeros(self.block_bytes // 8, np.uint64)
+        _check(_lib.mp_debug_read_block(self._h, int(addr), out.ctypes.data_as(C.c_void_p),
+                                        self.block_bytes), "debug_read_block")
+        return out.reshape(2 * self.L, -1)
+
+    def dump_index(self):
+        n = C.c_int64(0)
+        _lib.mp_debug_dump_index(self._h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(_lib.mp_debug_dump_index(self._h, buf, n.value + 1, C.byref(n)), "dump_index")
+        rows = []
+        for line in buf.value.decode().splitlines():
+            depth, med, idx, la, ref, term, toks = line.split("\t")
+            rows.append((tuple(int(x) for x in toks.split(",")), int(med), int(idx), int(la),
+                         int(ref), term == "1"))
+        return sorted(rows)
+
+    def block_states(self, medium: int = HBM) -> np.ndarray:
+        n = self.hbm_blocks if medium == HBM else self.dram_blocks
+        out = np.zeros(max(n, 1), np.uint8)
+        _check(_lib.mp_debug_block_states(self._h, medium,
+                                          out.ctypes.data_as(C.POINTER(C.c_uint8)), len(out)),
+               "block_states")
+        return out[:n]
+
+    def bitmap(self) -> np.ndarray:
+        nw = (self.hbm_blocks + 31) // 32
+        out = np.zeros(nw, np.uint32)
+        _check(_lib.mp_debug_bitmap(self._h, out.ctypes.data_as(C.POINTER(C.c_uint32)), nw),
+               "bitmap")
+        return out
+
+
+def connect(a: Pool, b: Pool):
+    _check(_lib.mp_connect(a.handle, b.handle), "connect")

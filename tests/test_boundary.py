@@ -1,0 +1,57 @@
+"""CPU checks of the C-ABI boundary: libmempool.so loads, exports every symbol
+include/mempool.h declares, the binding covers exactly that set, and calls
+that need no GPU behave (status strings; pool creation fails cleanly with no
+device).  No compute calls -- those are the -m gpu parity tests."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mempool.h")
+
+
+def declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mp_[a-z0-9_]+)\s*\(", src)) - {"mp_addr"})
+
+
+def test_header_declares_paper_api():
+    names = declared()
+    for api in ("alloc_mem", "free_mem", "insert", "match", "delete", "swap_out", "swap_in",
+                "transfer", "transfer_with_insert", "evict"):
+        assert f"mp_{api}" in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2406_17565_b200 import mempool as M
+    lib = ctypes.CDLL(M.LIB_PATH)
+    for name in declared():
+        assert hasattr(lib, name), name
+    assert sorted(M.SIGNATURES) == declared()
+
+
+def test_status_strings_and_no_device():
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    assert M._lib.mp_status_str(0) == b"MP_OK"
+    assert M._lib.mp_status_str(-10) == b"MP_ERR_PREFIX_MISSING"
+    for k, v in M.STATUS.items():
+        assert M._lib.mp_status_str(k).decode().endswith(v)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by -m gpu")
+    with pytest.raises(M.MempoolError) as e:
+        M.Pool(0, 0, 2, 2, 64, 16, 64)
+    assert e.value.name in ("CUDA", "CONFIG")
+
+
+def test_bad_config_rejected_before_cuda():
+    from paper_2406_17565_b200 import mempool as M
+    with pytest.raises(M.MempoolError) as e:
+        M.Pool(0, 0, 0, 2, 64, 16, 64)            # zero layers
+    assert e.value.name == "CONFIG"
+    with pytest.raises(M.MempoolError) as e:
+        M.Pool(0, 0, 2, 1, 1, 1, 64, elem_bytes=1)  # chunk 1 byte: not 16-B aligned
+    assert e.value.name == "CONFIG"

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by
+element -- block ids, returned addrs, moved counts, error names, clocks, index
+dumps, device bitmap, and every byte of every written block (integer compare).
+
+Tiny config (BASELINE.json configs[0]) golden run + randomized op sequences
+that cross several kernel tiles and ragged tails, on 1 GPU (two pools on
+cuda:0: the loopback transport)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2406_17565_b200 import mempool as M
+from tests.twin import Twin, connect, transfer, transfer_with_insert
+from workloads.configs import TINY, KVShape
+from workloads.traces import golden_prompts
+
+pytestmark = pytest.mark.gpu
+
+PATHS = [M.PATH_FUSED, M.PATH_STAGED, M.PATH_CE]
+
+
+def golden_pair(dedup, path, n_dram=64):
+    P = Twin(0, TINY, 64, n_dram)
+    D = Twin(1, TINY, 64, n_dram)
+    connect(P, D)
+    S, p1, p2, p3 = golden_prompts()
+    res = []
+    for p in (p1, p2, p3):
+        mt, matched = P.match(p)
+        new = P.alloc(-(-len(p) // 16) - len(matched))
+        P.fill(new)
+        P.insert(p, (matched + new)[: len(p) // 16])
+        res.append(transfer_with_insert(P, D, p, matched + new,
+                                        oflags=O.FLAG_DEDUP if dedup else 0, path=path))
+    return P, D, res
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("dedup", [False, True])
+def test_golden_tiny(dedup, path):
+    P, D, res = golden_pair(dedup, path)
+    P.check_state()
+    D.check_state()
+    moved = [r[1] for r in res]
+    assert moved == ([4, 3, 1] if dedup else [4, 5, 3])
+    # private delivery
+    msgs = []
+    while True:
+        m = D.g.recv_poll()
+        if m is None:
+            break
+        msgs.append(m)
+    assert len(msgs) == 3 and all(k == 1 and s == 0 for k, s, _p, _a in msgs)
+
+
+def test_golden_swap_evict():
+    P, D, _ = golden_pair(False, M.PATH_FUSED)
+    S, p1, p2, p3 = golden_prompts()
+    moved = P.swap_out(2)
+    assert [(o[2], n[2]) for o, n in moved] == [(2, 0), (5, 1)]
+    P.match(p1)
+    P.match(p2)
+    P.check_state()
+    assert P.swap_in([(0, O.DRAM, 0)]) == [(0, O.HBM, 2)]
+    P.check_state()
+    assert P.evict(1, O.HBM) != []
+    P.check_state()
+
+
+def test_private_and_transfer_layers():
+    P = Twin(0, TINY, 64)
+    D = Twin(1, TINY, 64)
+    connect(P, D)
+    src = P.alloc(5)
+    P.fill(src)
+    dst = D.alloc(5)
+    D.fill(dst)
+    for path in PATHS:
+        transfer(P, D, src, dst, oflags=O.FLAG_DST_GIVEN, l0=1, l1=2, priv=b"layer-1", path=path)
+        D.check_state()
+    out = transfer(P, D, src, priv=b"\x00req\xff")
+    D.check_state()
+    kinds = []
+    while True:
+        m = D.g.recv_poll()
+        if m is None:
+            break
+        kinds.append(m)
+    assert kinds[-1][2] == b"\x00req\xff"
+    assert [M.addr_index(a) for a in kinds[-1][3]] == [x[2] for x in out]
+
+
+def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24):
+    rng = np.random.default_rng(seed)
+    P = Twin(0, shape, n_hbm, n_dram)
+    D = Twin(1, shape, n_hbm, n_dram)
+    connect(P, D)
+    B = shape.block_tokens
+    pools = {0: P, 1: D}
+    seqs = []
+    vocab = 4
+
+    def gen():
+        if seqs and rng.random() < 0.7:
+            base = seqs[rng.integers(len(seqs))]
+            cut = int(rng.integers(0, len(base) + 1))
+            return np.concatenate([base[:cut], rng.integers(0, vocab, int(rng.integers(0, 4 * B)),
+                                                          dtype=np.int32)]).astype(np.int32)
+        return rng.integers(0, vocab, int(rng.integers(1, 6 * B)), dtype=np.int32)
+
+    for step in range(n_ops):
+        X = pools[int(rng.integers(2))]
+        Y = D if X is P else P
+        op = rng.random()
+        try:
+            if op < 0.22:
+                # engine-style prefill: match, alloc the rest, fill, insert
+                t = gen()
+                mt, matched = X.match(t)
+                new = X.alloc(-(-len(t) // B) - len(matched))
+                X.fill(new)
+                X.insert(t, (matched + new)[: len(t) // B])
+                seqs.append(t)
+            elif op < 0.40 and seqs:
+                t = seqs[rng.integers(len(seqs))]
+                mt, addrs = X.match(t)
+                if addrs:
+                    k = int(rng.integers(0, len(addrs) + 1))
+                    fl = int(rng.choice([0, O.FLAG_DEDUP, O.FLAG_INS_ERR_ON_CONFLICT]))
+                    transfer_with_insert(X, Y, t[: len(addrs) * B], addrs[k:] if k else addrs,
+                                         oflags=fl, priv=bytes([step % 256]), path=path)
+            elif op < 0.50:
+                a = X.alloc(int(rng.integers(0, 4)))
+                if a and rng.random() < 0.5:
+                    X.fill(a)
+                if a and rng.random() < 0.5:
+                    transfer(X, Y, a, priv=b"x", path=path,
+                             l0=0, l1=shape.layers)
+                elif a:
+                    X.free(a)
+            elif op < 0.58 and seqs:
+                X.delete(seqs[rng.integers(len(seqs))])
+            elif op < 0.64:
+                X.evict(int(rng.integers(1, 4)), int(rng.integers(2)))
+            elif op < 0.74:
+                X.swap_out(int(rng.integers(1, 6)))
+            elif op < 0.82:
+                dram = [(X.inst, O.DRAM, i) for i, s in enumerate(X.o.state[O.DRAM])
+                        if s in (O.INDEXED, O.ACTIVE)]
+                if dram:
+                    k = int(rng.integers(1, min(4, len(dram)) + 1))
+                    pick = [dram[j] for j in rng.choice(len(dram), k, replace=False)]
+                    X.swap_in(pick)
+            elif op < 0.88 and seqs:
+                t = seqs[rng.integers(len(seqs))]
+                _, addrs = X.match(t, O.FLAG_MATCH_PIN)
+                if addrs and rng.random() < 0.7:
+                    X.unpin(addrs)
+            elif op < 0.94:
+                # invalid ops must fail identically and change nothing
+                bad = [(X.inst, O.HBM, int(rng.integers(0, n_hbm)))]
+                X.free(bad)
+            else:
+                st = [(X.inst, O.HBM, i) for i, s in enumerate(X.o.state[O.HBM]) if s == O.ACTIVE]
+                if st:
+                    dst = Y.alloc(min(len(st), 2))
+                    transfer(X, Y, st[: len(dst)], dst, oflags=O.FLAG_DST_GIVEN,
+                             l0=int(rng.integers(0, shape.layers)), l1=shape.layers, path=path)
+        except O.MPError:
+            pass
+        if step % 25 == 24:
+            P.check_state()
+            D.check_state()
+    P.check_state()
+    D.check_state()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_random_ops_tiny(path):
+    for seed in range(3):
+        random_ops(seed, TINY, 300, path)
+
+
+def test_random_ops_ragged_chunk():
+    # chunk = 8*3*24*2 = 1152 B: not a multiple of the kernel's 4 KiB warp
+    # unit -> exercises the predicated tail; B = 8
+    shape = KVShape("ragged", 3, 3, 24, 8)
+    random_ops(11, shape, 300, M.PATH_FUSED)
+    random_ops(12, shape, 150, M.PATH_STAGED)
+
+
+def test_pack_unpack_np_take():
+    import torch
+    shape = KVShape("pk", 4, 4, 64, 16)     # c = 8 KiB: two 4 KiB units per chunk
+    P = Twin(0, shape, 40)
+    a = P.alloc(23)
+    P.fill(a)
+    rng = np.random.default_rng(3)
+    sel = [a[i] for i in rng.permutation(23)[:17]]
+    c = shape.chunk_bytes
+    for l0, l1 in ((0, 4), (1, 3), (2, 3)):
+        nj = 2 * (l1 - l0)
+        stg = torch.zeros(17 * nj * c // 8, dtype=torch.int64, device="cuda:0")
+        P.g.pack(M.np.array([M.make_addr(0, 0, x[2]) for x in sel], np.uint64), l0, l1,
+                 stg.data_ptr())
+        got = stg.cpu().numpy().view(np.uint64).reshape(17, nj, c // 8)
+        for i, x in enumerate(sel):
+            want = P.o.block_bytes(x)[2 * l0: 2 * l1]
+            np.testing.assert_array_equal(got[i], want)
+        # unpack o pack == identity on fresh blocks
+        fresh = P.alloc(17)
+        P.g.unpack(stg.data_ptr(), M.np.array([M.make_addr(0, 0, x[2]) for x in fresh],
+                                              np.uint64), l0, l1)
+        for i, x in enumerate(fresh):
+            blk = P.g.debug_read_block(M.make_addr(0, 0, x[2]))
+            np.testing.assert_array_equal(blk[2 * l0: 2 * l1], got[i])
+        P.free(fresh)
