@@ -20,8 +20,15 @@
  *    mp_last_error() for the CUDA message and destroy the pool).
  *  - One caller thread per pool at a time; a transfer uses both
  *    pools and must not race with calls on either.
- *  - Every call is synchronous: it returns after all device work it issued
- *    has completed (transfers: after the receiver's insert).
+ *  - Calls are synchronous by default: they return after the device work
+ *    they issued has completed (transfers: after the data landed and the
+ *    receiver inserted).  With MP_XFER_ASYNC a transfer returns once
+ *    its work is enqueued on the pools' streams (host-side bookkeeping -- the
+ *    receiver's allocation, insert and `private` delivery -- is already done);
+ *    mp_sync(pool) waits for it.  Every later call on either pool is
+ *    stream-ordered after it, and mp_alloc_mem drains the pool before handing
+ *    blocks to the caller.  Frees of HBM blocks are applied to the device
+ *    bitmap lazily, stream-ordered before the pool's next allocation.
  *  - Layout: the HBM pool of an instance is 2*L "slabs" (K_0, V_0, K_1, V_1,
  *    ...), each hbm_blocks chunks of c = B*H*D*elem bytes (vLLM's per-layer
  *    paged layout: "two blocks per LLM layer").  Block id b is chunk b
@@ -76,6 +83,7 @@ typedef enum {
 /* ---- flags ("Transfer flags can control on-demand allocation") ---- */
 #define MP_XFER_DST_GIVEN (1u << 0) /* dst_addrs is an INPUT: skip the allocation step */
 #define MP_XFER_DEDUP (1u << 1)     /* receiver matches first, moves only what it lacks (R3) */
+#define MP_XFER_ASYNC (1u << 2)     /* return once enqueued; complete with mp_sync (see above) */
 #define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
 #define MP_MATCH_PIN (1u << 5)      /* match: pin matched blocks until mp_unpin (R12) */
 /* Transport selection (benchmarks / comparisons; default AUTO = FUSED). */
@@ -109,7 +117,7 @@ typedef struct {
   void* dram_base;
   int64_t staging_bytes; /* device staging for the STAGED path (0: 256 MiB) */
   int32_t staging_slots; /* ring depth (0: 4) */
-  int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = 4 x SMs) */
+  int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = one full wave) */
 } mp_pool_config;
 
 typedef struct {
@@ -146,6 +154,10 @@ void mp_pool_destroy(mp_pool* pool);
  * Instance ids must differ; shapes (L, H, D, elem, B) must match. */
 mp_status mp_connect(mp_pool* a, mp_pool* b);
 mp_status mp_pool_info_get(const mp_pool* pool, mp_pool_info* out);
+/* Wait for every device operation issued on this pool (including
+ * MP_XFER_ASYNC transfers that execute on its stream).  In verify mode also
+ * checks every device allocation against the host shadow (MP_ERR_INTERNAL). */
+mp_status mp_sync(mp_pool* pool);
 const char* mp_status_str(mp_status s);
 const char* mp_last_error(void); /* thread-local detail of the last failure */
 

@@ -1,6 +1,6 @@
 """Build libmempool.so in-tree (sm_100a only).
 
-    python -m paper_2406_17565_b200.build
+    python paper_2406_17565_b200/build.py [--force] [-v]
 
 nvcc cross-compiles on a CPU-only box; the .so travels to the GPU box with the
 repo snapshot.  The library links the CUDA runtime statically, so it does not
@@ -16,8 +16,8 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libmempool.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["mempool.cpp", "kernels.cu"]
-HEADERS = ["kernels.cuh", "index.hpp"]
+SOURCES = ["pool.cpp", "api_memory_index.cpp", "api_transfer.cpp", "api_swap.cpp", "kernels.cu"]
+HEADERS = ["kernels.cuh", "index.hpp", "pool.hpp"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -1,0 +1,322 @@
+// api_transfer.cpp -- distributed API of MemPool: transfer and
+// transfer_with_insert (Table tbl-mempool-api; workflow P:360-365:
+// allocation at the receiver, transmission, insertion, ok), the private-field
+// delivery and the three transports of the transmission step:
+//   FUSED  (A6f) one gather->store kernel from the source pool's scattered
+//          chunks straight into the destination blocks (P2P stores over NVLink
+//          when the pools are on different GPUs); no staging, 2*Pb HBM bytes
+//          per block at loopback;
+//   STAGED (A4-A6) pack into aggregated staging slots, one
+//          contiguous copy per slot, unpack; a ring of slots overlaps the three;
+//   CE     one copy-engine memcpy per (block, layer, K/V) chunk: the paper's
+//          discrete per-block transfer, kept as a library baseline.
+// Readings R3, R4, R12, R13.
+#include <algorithm>
+#include <cstring>
+
+#include "pool.hpp"
+
+namespace mp {
+namespace {
+
+mp_status validate_src(mp_pool* src, const mp_addr* a, int64_t n, std::vector<int32_t>* ids) {
+  ids->resize((size_t)n);
+  std::vector<uint8_t> mark((size_t)src->n_hbm, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int m = 0;
+    int32_t idx = 0;
+    if (!decode(src, a[i], &m, &idx)) return MP_ERR_INVALID_ADDR;
+    if (m != MP_HBM) return MP_ERR_PRECONDITION;  // R13
+    const uint8_t s = src->st[MP_HBM][(size_t)idx];
+    if (!(s == ST_ACTIVE || s == ST_INDEXED) || mark[(size_t)idx]) return MP_ERR_PRECONDITION;
+    mark[(size_t)idx] = 1;
+    (*ids)[(size_t)i] = idx;
+  }
+  return MP_OK;
+}
+
+mp_status validate_dst_given(mp_pool* dst, const mp_addr* a, int64_t n,
+                             std::vector<int32_t>* ids) {
+  if (!a) return MP_ERR_ADDR_COUNT;
+  ids->resize((size_t)n);
+  std::vector<uint8_t> mark((size_t)dst->n_hbm, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int m = 0;
+    int32_t idx = 0;
+    if (!decode(dst, a[i], &m, &idx)) return MP_ERR_INVALID_ADDR;
+    if (m != MP_HBM || dst->st[MP_HBM][(size_t)idx] != ST_ACTIVE || mark[(size_t)idx])
+      return MP_ERR_PRECONDITION;
+    mark[(size_t)idx] = 1;
+    (*ids)[(size_t)i] = idx;
+  }
+  return MP_OK;
+}
+
+mp_status check_compatible(mp_pool* src, mp_pool* dst) {
+  if (dst == src || src->L != dst->L || src->chunk != dst->chunk || src->B != dst->B)
+    return MP_ERR_CONFIG;
+  return MP_OK;
+}
+
+mp_pool* peer_of(mp_pool* src, int32_t inst) {
+  auto it = src->peers.find(inst);
+  return it == src->peers.end() ? nullptr : it->second;
+}
+
+// The transmission step.  Copies chunks [j0, j0+nj) of source blocks `sids`
+// into destination blocks `dids`; d_dst is the destination allocator's device
+// table of the same ids (on dst's device) or nullptr.  Enqueued after all
+// earlier work of both pools and before their later work; STAGED completes
+// before returning, the others are stream-ordered.
+mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                   const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj,
+                   uint32_t path) {
+  const int64_t n = (int64_t)sids.size();
+  if (n == 0) return MP_OK;
+  if (path == MP_XFER_PATH_AUTO) path = MP_XFER_PATH_FUSED;
+  const bool same_dev = src->dev == dst->dev;
+  if (path == MP_XFER_PATH_FUSED && same_dev) {
+    TRY(link(src, dst));
+    DevGuard g(dst->dev);
+    int* ds = nullptr;
+    TRY(upload_ids(dst, sids, &ds));
+    const int* dd = d_dst;
+    if (!dd) {
+      int* t = nullptr;
+      TRY(upload_ids(dst, dids, &t));
+      dd = t;
+    }
+    TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, ds),
+                             pool_ep(dst->d_slabs, dd), n, j0, nj));
+    dst->stats.blocks_moved += (uint64_t)n;
+    return link(dst, src);
+  }
+  if (path == MP_XFER_PATH_FUSED) {
+    // Push over NVLink: the source GPU gathers its chunks and stores them
+    // straight into the peer pool's blocks (no staging).
+    auto it = src->peer_tables.find(dst->inst);
+    if (it == src->peer_tables.end()) return MP_ERR_DST_UNREACHABLE;
+    TRY(link(dst, src));
+    DevGuard g(src->dev);
+    int *ds = nullptr, *dd = nullptr;
+    TRY(upload_ids(src, sids, &ds));
+    TRY(upload_ids(src, dids, &dd));
+    TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
+                             pool_ep(it->second, dd), n, j0, nj));
+    src->stats.blocks_moved += (uint64_t)n;
+    return link(src, dst);
+  }
+  if (path == MP_XFER_PATH_CE) {
+    TRY(link(dst, src));
+    DevGuard g(src->dev);
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = j0; j < j0 + nj; ++j)
+        CK(cudaMemcpyAsync(dst->slabs[(size_t)j] + (int64_t)dids[(size_t)i] * dst->chunk,
+                           src->slabs[(size_t)j] + (int64_t)sids[(size_t)i] * src->chunk,
+                           (size_t)src->chunk, cudaMemcpyDefault, src->stream));
+    src->stats.bytes_moved += (uint64_t)(n * nj * src->chunk);
+    src->stats.blocks_moved += (uint64_t)n;
+    return link(src, dst);
+  }
+  if (path == MP_XFER_PATH_STAGED) {
+    const int64_t per_block = (int64_t)nj * src->chunk;
+    const int S = std::max(1, std::min(src->staging_slots, dst->staging_slots));
+    const int64_t slot_bytes = std::min(src->staging_bytes, dst->staging_bytes) / S;
+    const int64_t k = slot_bytes / per_block;
+    if (k <= 0) {
+      set_err("staging slot smaller than one block");
+      return MP_ERR_CONFIG;
+    }
+    TRY(link(dst, src));
+    int *ds = nullptr, *dd = nullptr;
+    {
+      DevGuard g(src->dev);
+      TRY(upload_ids(src, sids, &ds));
+    }
+    {
+      DevGuard g(dst->dev);
+      if (d_dst) {
+        dd = const_cast<int*>(d_dst);
+      } else {
+        TRY(upload_ids(dst, dids, &dd));
+      }
+    }
+    const int64_t nslots = (n + k - 1) / k;
+    for (int64_t s = 0; s < nslots; ++s) {
+      const int r = (int)(s % S);
+      const int64_t b0 = s * k, nb = std::min(k, n - b0);
+      char* sslot = src->staging + r * slot_bytes;
+      char* dslot = dst->staging + r * slot_bytes;
+      {
+        DevGuard g(src->dev);
+        if (s >= S) CK(cudaStreamWaitEvent(src->stream, dst->slot_ev[(size_t)r], 0));
+        TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds + b0),
+                                 agg_ep(sslot, per_block, nullptr), nb, j0, nj));
+        CK(cudaEventRecord(src->slot_ev[(size_t)r], src->stream));
+        CK(cudaStreamWaitEvent(src->copy_stream, src->slot_ev[(size_t)r], 0));
+        CK(cudaMemcpyAsync(dslot, sslot, (size_t)(nb * per_block), cudaMemcpyDefault,
+                           src->copy_stream));
+        CK(cudaEventRecord(src->slot_ev[(size_t)r], src->copy_stream));
+      }
+      {
+        DevGuard g(dst->dev);
+        CK(cudaStreamWaitEvent(dst->stream, src->slot_ev[(size_t)r], 0));
+        TRY(launch_migrate_timed(dst, dst->stream, agg_ep(dslot, per_block, nullptr),
+                                 pool_ep(dst->d_slabs, dd + b0), nb, j0, nj));
+        CK(cudaEventRecord(dst->slot_ev[(size_t)r], dst->stream));
+      }
+    }
+    {
+      DevGuard g(dst->dev);
+      TRY(sync(dst));
+    }
+    {
+      DevGuard g(src->dev);
+      TRY(sync(src));
+    }
+    src->stats.blocks_moved += (uint64_t)n;
+    return MP_OK;
+  }
+  set_err("unknown transfer path");
+  return MP_ERR_CONFIG;
+}
+
+mp_status finish(mp_pool* src, mp_pool* dst, uint32_t flags) {
+  if (flags & MP_XFER_ASYNC) return MP_OK;
+  {
+    DevGuard g(dst->dev);
+    TRY(sync(dst));
+  }
+  DevGuard g(src->dev);
+  return sync(src);
+}
+
+}  // namespace
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" {
+
+mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t n, mp_addr* da,
+                      uint32_t flags, int32_t l0, int32_t l1, const void* priv, int64_t priv_len) {
+  if (!src || n < 0 || (n > 0 && (!sa || !da)) || priv_len < 0 || (priv_len > 0 && !priv))
+    return MP_ERR_CONFIG;
+  mp_pool* dst = peer_of(src, dst_inst);
+  if (!dst) return MP_ERR_DST_UNREACHABLE;
+  TRY(check_compatible(src, dst));
+  if (!(0 <= l0 && l0 < l1 && l1 <= src->L) || (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
+  std::vector<int32_t> sids, dids;
+  TRY(validate_src(src, sa, n, &sids));
+  const bool dst_given = (flags & MP_XFER_DST_GIVEN) != 0;
+  if (dst_given) TRY(validate_dst_given(dst, da, n, &dids));
+  const std::vector<mpi::Node*> none;
+  if (!dst_given && !can_make_room(dst, n, MP_HBM, none)) return MP_ERR_DST_OOM;
+  // ---- (1) allocation at the receiver ----
+  int* d_dst = nullptr;
+  if (!dst_given) {
+    DevGuard g(dst->dev);
+    if (dst->nfree[MP_HBM] < n) evict_internal(dst, n - dst->nfree[MP_HBM], MP_HBM, nullptr);
+    TRY(alloc_hbm(dst, n, src->inst, &dids, &d_dst));
+  }
+  // ---- (2) transmission ----
+  TRY(transmit(src, dst, sids, dids, d_dst, 2 * l0, 2 * (l1 - l0), flags & MP_XFER_PATH_MASK));
+  TRY(finish(src, dst, flags));
+  if (!dst_given)
+    for (int64_t i = 0; i < n; ++i) da[i] = enc(dst, MP_HBM, dids[(size_t)i]);
+  Msg msg{0, src->inst, {}, {}};
+  if (priv_len) msg.priv.assign((const uint8_t*)priv, (const uint8_t*)priv + priv_len);
+  msg.addrs.assign(da, da + n);
+  dst->inbox.push_back(std::move(msg));
+  return MP_OK;
+}
+
+mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token* toks,
+                                  int64_t n_tok, const mp_addr* sa, int64_t m, mp_addr* da,
+                                  uint32_t flags, const void* priv, int64_t priv_len,
+                                  int64_t* n_moved) {
+  if (!src || n_tok < 0 || (n_tok > 0 && !toks) || m < 0 || (m > 0 && !sa) || !da ||
+      priv_len < 0 || (priv_len > 0 && !priv))
+    return MP_ERR_CONFIG;
+  mp_pool* dst = peer_of(src, dst_inst);
+  if (!dst) return MP_ERR_DST_UNREACHABLE;
+  TRY(check_compatible(src, dst));
+  const bool dst_given = (flags & MP_XFER_DST_GIVEN) != 0;
+  const bool dedup = (flags & MP_XFER_DEDUP) != 0;
+  if (dst_given && dedup) return MP_ERR_CONFIG;
+  const int64_t B = dst->B, ceil_b = (n_tok + B - 1) / B, floor_b = n_tok / B;
+  if (m > ceil_b) return MP_ERR_ADDR_COUNT;
+  std::vector<int32_t> sids, given;
+  TRY(validate_src(src, sa, m, &sids));
+  if (dst_given) TRY(validate_dst_given(dst, da, m, &given));
+  const int64_t q = ceil_b - m;
+  const bool need_match = dedup || q > 0;
+  std::vector<mpi::Node*> peek;
+  if (need_match) peek = dst->index->path(toks, floor_b);
+  const int64_t k_match = (int64_t)peek.size();
+  if (k_match < q) return MP_ERR_PREFIX_MISSING;
+  const int64_t skip = dedup ? k_match - q : 0;
+  const int64_t nm = m - skip;
+  if (flags & MP_INS_ERR_ON_CONFLICT) {
+    const int64_t k_exist = need_match ? k_match : dst->index->peek(toks, n_tok);
+    if (k_exist > q + skip) return MP_ERR_CONFLICT;
+  }
+  if (!dst_given && !can_make_room(dst, nm, MP_HBM, peek)) return MP_ERR_DST_OOM;
+  // ---- mutations start here ----
+  // receiver-side match, pinned while the receiver allocates (R3, R12)
+  std::vector<mpi::Node*> matched;
+  if (need_match) matched = dst->index->match(toks, n_tok, /*pin=*/true);
+  // ---- (1) allocation at the receiver ----
+  std::vector<int32_t> dids;
+  int* d_dst = nullptr;
+  if (dst_given) {
+    dids = given;
+  } else {
+    DevGuard g(dst->dev);
+    if (dst->nfree[MP_HBM] < nm) evict_internal(dst, nm - dst->nfree[MP_HBM], MP_HBM, nullptr);
+    TRY(alloc_hbm(dst, nm, src->inst, &dids, &d_dst));
+  }
+  // ---- (2) transmission of all layers ----
+  std::vector<int32_t> moved_src(sids.begin() + skip, sids.end());
+  TRY(transmit(src, dst, moved_src, dids, d_dst, 0, src->nch, flags & MP_XFER_PATH_MASK));
+  // ---- (3) insertion at the receiver ----
+  std::vector<mp_addr> full;
+  full.reserve((size_t)ceil_b);
+  for (int64_t i = 0; i < q + skip; ++i)
+    full.push_back(enc(dst, matched[(size_t)i]->medium, matched[(size_t)i]->idx));
+  for (int64_t i = 0; i < nm; ++i) full.push_back(enc(dst, MP_HBM, dids[(size_t)i]));
+  int64_t dup = 0;
+  TRY(insert_internal(dst, toks, n_tok, full.data(), (int64_t)full.size(),
+                      flags & MP_INS_ERR_ON_CONFLICT, &dup));
+  unpin_nodes(dst, matched);
+  TRY(finish(src, dst, flags));
+  // ---- ok: the receiver's final address of every block ----
+  std::vector<mpi::Node*> fin = dst->index->path(toks, floor_b);
+  for (int64_t i = 0; i < floor_b; ++i)
+    da[i] = enc(dst, fin[(size_t)i]->medium, fin[(size_t)i]->idx);
+  if (ceil_b > floor_b) da[floor_b] = full[(size_t)floor_b];
+  if (n_moved) *n_moved = nm;
+  Msg msg{1, src->inst, {}, {}};
+  if (priv_len) msg.priv.assign((const uint8_t*)priv, (const uint8_t*)priv + priv_len);
+  msg.addrs.assign(da, da + ceil_b);
+  dst->inbox.push_back(std::move(msg));
+  return MP_OK;
+}
+
+mp_status mp_recv_poll(mp_pool* p, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,
+                       mp_addr* addrs, int64_t addr_cap) {
+  if (!p || !out) return MP_ERR_CONFIG;
+  if (p->inbox.empty()) return MP_ERR_PRECONDITION;
+  Msg& m = p->inbox.front();
+  out->kind = m.kind;
+  out->src_instance = m.src;
+  out->n_addrs = (int64_t)m.addrs.size();
+  out->priv_len = (int64_t)m.priv.size();
+  if (priv_cap < out->priv_len || addr_cap < out->n_addrs) return MP_ERR_BUFFER_TOO_SMALL;
+  if (!m.priv.empty()) std::memcpy(priv_buf, m.priv.data(), m.priv.size());
+  if (!m.addrs.empty()) std::memcpy(addrs, m.addrs.data(), m.addrs.size() * sizeof(mp_addr));
+  p->inbox.pop_front();
+  return MP_OK;
+}
+
+}  // extern "C"

@@ -35,7 +35,7 @@ __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
 }
 
 template <bool kSrcPool, bool kDstPool>
-__global__ void __launch_bounds__(kThreads) migrate_kernel(Endpoint src, Endpoint dst, int j0,
+__global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endpoint dst, int j0,
                                                            int nj, long long chunk,
                                                            unsigned units_per_chunk,
                                                            unsigned total_units) {
@@ -176,10 +176,25 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   if (total >= (1ull << 32)) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int cap = max_ctas > 0 ? max_ctas : 4 * sm_count(dev);
+  const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
+  // One full wave: resident CTAs per SM x SM count (148 on B200), so no CTA
+  // waits for a second wave; the grid-stride loop spreads the units.
+  static int cached_cap[64] = {0};  // per device: resident CTAs x SMs
+  int cap = max_ctas;
+  if (cap <= 0) {
+    if (dev < 64 && cached_cap[dev] > 0) {
+      cap = cached_cap[dev];
+    } else {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, migrate_kernel<true, true>,
+                                                    kThreads, 0);
+      if (per_sm <= 0) per_sm = 1;
+      cap = per_sm * sm_count(dev);
+      if (dev < 64) cached_cap[dev] = cap;
+    }
+  }
   const unsigned long long want = (total + (kThreads / 32) - 1) / (kThreads / 32);
   const int grid = (int)(want < (unsigned long long)cap ? want : (unsigned long long)cap);
-  const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
   if (sp && dp)
     migrate_kernel<true, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
                                                               units_per_chunk, (unsigned)total);

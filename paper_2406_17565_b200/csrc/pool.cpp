@@ -1,0 +1,488 @@
+// pool.cpp -- pool lifecycle, the host shadow of the device allocator, the
+// id arena, stream ordering and profiling (see pool.hpp for the model).
+#include "pool.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace mp {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_err(const std::string& s) { g_err = s; }
+const std::string& get_err() { return g_err; }
+
+// ----------------------------------------------------------------- arena
+int* arena_take(mp_pool* p, int64_t n, int** host) {
+  n = std::max<int64_t>(n, 1);
+  if (n > p->ar.cap) return nullptr;
+  if (p->ar.used + n > p->ar.cap) {
+    if (drain(p) != MP_OK) return nullptr;
+    p->ar.used = 0;
+  }
+  int* d = p->ar.d + p->ar.used;
+  *host = p->ar.h + p->ar.used;
+  p->ar.used += n;
+  return d;
+}
+
+mp_status upload_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d_out) {
+  int* h = nullptr;
+  int* d = arena_take(p, (int64_t)ids.size(), &h);
+  if (!d) {
+    set_err("id arena exhausted");
+    return MP_ERR_INTERNAL;
+  }
+  if (!ids.empty()) {
+    std::memcpy(h, ids.data(), ids.size() * sizeof(int32_t));
+    CK(cudaMemcpyAsync(d, h, ids.size() * sizeof(int32_t), cudaMemcpyHostToDevice, p->stream));
+  }
+  *d_out = d;
+  return MP_OK;
+}
+
+// ------------------------------------------------------- sync / ordering
+mp_status flush_frees(mp_pool* p) {
+  if (p->pending_free.empty()) return MP_OK;
+  std::vector<int32_t> ids;
+  ids.swap(p->pending_free);
+  int* d = nullptr;
+  TRY(upload_ids(p, ids, &d));
+  CK(mpk::launch_free(p->d_bitmap, d, (int)ids.size(), p->stream));
+  p->stats.aux_launches += 1;
+  return MP_OK;
+}
+
+mp_status drain(mp_pool* p) {
+  CK(cudaStreamSynchronize(p->stream));
+  for (const TimedLaunch& t : p->timed) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p->tev[2 * (size_t)t.pair], p->tev[2 * (size_t)t.pair + 1]));
+    p->stats.kernel_ms += ms;
+    p->stats.timed_launches += 1;
+    p->stats.timed_bytes += t.bytes;
+  }
+  p->timed.clear();
+  if (!p->pending_verify.empty()) {
+    int err = 0;
+    CK(cudaMemcpy(&err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<PendingVerify> pv;
+    pv.swap(p->pending_verify);
+    if (err) {
+      set_err("device allocator ran short of free blocks");
+      return MP_ERR_INTERNAL;
+    }
+    for (const PendingVerify& v : pv)
+      for (size_t i = 0; i < v.want.size(); ++i)
+        if (v.host[i] != v.want[i]) {
+          set_err("device allocator disagrees with the host shadow (lowest-first)");
+          return MP_ERR_INTERNAL;
+        }
+  }
+  return MP_OK;
+}
+
+mp_status sync(mp_pool* p) {
+  TRY(flush_frees(p));
+  return drain(p);
+}
+
+mp_status link(mp_pool* signal, mp_pool* waiter) {
+  if (signal == waiter) return MP_OK;
+  {
+    DevGuard g(signal->dev);
+    CK(cudaEventRecord(signal->ev_order, signal->stream));
+  }
+  DevGuard g(waiter->dev);
+  CK(cudaStreamWaitEvent(waiter->stream, signal->ev_order, 0));
+  return MP_OK;
+}
+
+bool decode(const mp_pool* p, mp_addr a, int* med, int32_t* idx) {
+  if (MP_ADDR_INST(a) != p->inst) return false;
+  const int m = MP_ADDR_MEDIUM(a);
+  if (m != MP_HBM && m != MP_DRAM) return false;
+  const int64_t i = (int64_t)(a & 0xFFFFFFFFu);
+  if (i >= (m == MP_HBM ? p->n_hbm : p->n_dram)) return false;
+  *med = m;
+  *idx = (int32_t)i;
+  return true;
+}
+
+// ------------------------------------------------------------- allocator
+void free_block(mp_pool* p, int med, int32_t idx) {
+  p->st[med][(size_t)idx] = ST_FREE;
+  p->alloc_by[med][(size_t)idx] = -1;
+  ++p->nfree[med];
+  if (med == MP_HBM) {
+    p->hfree[(size_t)idx >> 6] |= 1ull << (idx & 63);
+    p->pending_free.push_back(idx);  // device bitmap: stream-ordered, lazily
+  } else {
+    p->dram_free.insert(idx);
+  }
+}
+
+// R8: evict up to n LRU leaves of `med`; appends freed ids.
+void evict_internal(mp_pool* p, int64_t n, int med, std::vector<int32_t>* freed) {
+  for (int64_t k = 0; k < n; ++k) {
+    mpi::Node* v = p->index->lru_leaf(med);
+    if (!v) break;
+    const int32_t idx = v->idx;
+    p->index->unlink(v);
+    free_block(p, med, idx);
+    if (freed) freed->push_back(idx);
+  }
+}
+
+// R2 feasibility: free + eventually-evictable (excluding the pinned path) >= n.
+bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>& pinned) {
+  if (p->nfree[med] >= n) return true;
+  return p->nfree[med] + p->index->evictable(med, pinned) >= n;
+}
+
+mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,
+                    int** d_ids) {
+  ids->clear();
+  if (n > p->nfree[MP_HBM]) {
+    set_err("alloc_hbm: host shadow short");
+    return MP_ERR_INTERNAL;
+  }
+  if (n == 0) {
+    *d_ids = nullptr;
+    return MP_OK;
+  }
+  for (size_t w = 0; w < p->hfree.size() && (int64_t)ids->size() < n; ++w) {
+    uint64_t bits = p->hfree[w];
+    while (bits && (int64_t)ids->size() < n) {
+      const int b = __builtin_ctzll(bits);
+      bits &= bits - 1;
+      const int32_t id = (int32_t)(w * 64 + (size_t)b);
+      p->hfree[w] &= ~(1ull << b);
+      p->st[MP_HBM][(size_t)id] = ST_ACTIVE;
+      p->alloc_by[MP_HBM][(size_t)id] = requester;
+      ids->push_back(id);
+    }
+  }
+  p->nfree[MP_HBM] -= n;
+  TRY(flush_frees(p));  // the device bitmap must see every earlier free first
+  int* h = nullptr;
+  int* d = arena_take(p, n, &h);
+  if (!d) {
+    set_err("id arena exhausted");
+    return MP_ERR_INTERNAL;
+  }
+  CK(mpk::launch_alloc(p->d_bitmap, p->nwords, (int)n, d, p->verify ? h : nullptr, p->d_err,
+                       p->stream));
+  p->stats.aux_launches += 1;
+  if (p->verify) p->pending_verify.push_back({h, *ids});
+  *d_ids = d;
+  return MP_OK;
+}
+
+std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester) {
+  std::vector<int32_t> out;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t id = *p->dram_free.begin();
+    p->dram_free.erase(p->dram_free.begin());
+    p->st[MP_DRAM][(size_t)id] = ST_ACTIVE;
+    p->alloc_by[MP_DRAM][(size_t)id] = requester;
+    out.push_back(id);
+  }
+  p->nfree[MP_DRAM] -= n;
+  return out;
+}
+
+// ------------------------------------------------------------ migration
+mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
+                               const mpk::Endpoint& b, int64_t n, int j0, int nj) {
+  if (n <= 0) return MP_OK;
+  const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)p->chunk;
+  const bool timed = p->profiling && s == p->stream;
+  int pair = -1;
+  if (timed) {
+    if ((int)p->timed.size() >= kTimedPairs) TRY(drain(p));
+    pair = p->tev_next;
+    p->tev_next = (p->tev_next + 1) % kTimedPairs;
+    CK(cudaEventRecord(p->tev[2 * (size_t)pair], s));
+  }
+  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, p->chunk, p->max_ctas, s));
+  if (timed) {
+    CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
+    p->timed.push_back({pair, bytes});
+  }
+  p->stats.kernel_launches += 1;
+  p->stats.bytes_moved += bytes;
+  return MP_OK;
+}
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" {
+
+const char* mp_status_str(mp_status s) {
+  switch (s) {
+    case MP_OK: return "MP_OK";
+    case MP_ERR_OOM: return "MP_ERR_OOM";
+    case MP_ERR_DOUBLE_FREE: return "MP_ERR_DOUBLE_FREE";
+    case MP_ERR_INVALID_ADDR: return "MP_ERR_INVALID_ADDR";
+    case MP_ERR_ADDR_COUNT: return "MP_ERR_ADDR_COUNT";
+    case MP_ERR_CONFLICT: return "MP_ERR_CONFLICT";
+    case MP_ERR_NO_DRAM: return "MP_ERR_NO_DRAM";
+    case MP_ERR_DST_OOM: return "MP_ERR_DST_OOM";
+    case MP_ERR_DST_UNREACHABLE: return "MP_ERR_DST_UNREACHABLE";
+    case MP_ERR_PRECONDITION: return "MP_ERR_PRECONDITION";
+    case MP_ERR_PREFIX_MISSING: return "MP_ERR_PREFIX_MISSING";
+    case MP_ERR_CONFIG: return "MP_ERR_CONFIG";
+    case MP_ERR_BUFFER_TOO_SMALL: return "MP_ERR_BUFFER_TOO_SMALL";
+    case MP_ERR_CUDA: return "MP_ERR_CUDA";
+    case MP_ERR_NCCL: return "MP_ERR_NCCL";
+    case MP_ERR_INTERNAL: return "MP_ERR_INTERNAL";
+  }
+  return "MP_ERR_UNKNOWN";
+}
+
+const char* mp_last_error(void) { return get_err().c_str(); }
+
+void mp_pool_destroy(mp_pool* p) {
+  if (!p) return;
+  {
+    DevGuard g(p->dev);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    for (auto& kv : p->peers) {
+      mp_pool* q = kv.second;
+      q->peers.erase(p->inst);
+      auto it = q->peer_tables.find(p->inst);
+      if (it != q->peer_tables.end()) {
+        DevGuard g2(q->dev);
+        if (q->stream) cudaStreamSynchronize(q->stream);
+        cudaFree(it->second);
+        q->peer_tables.erase(it);
+      }
+    }
+    for (auto& kv : p->peer_tables) cudaFree(kv.second);
+    if (p->own_slab_region) cudaFree(p->own_slab_region);
+    if (p->d_slabs) cudaFree(p->d_slabs);
+    if (p->d_bitmap) cudaFree(p->d_bitmap);
+    if (p->d_err) cudaFree(p->d_err);
+    if (p->ar.d) cudaFree(p->ar.d);
+    if (p->ar.h) cudaFreeHost(p->ar.h);
+    if (p->own_dram && p->dram) cudaFreeHost(p->dram);
+    if (p->staging) cudaFree(p->staging);
+    if (p->ev_order) cudaEventDestroy(p->ev_order);
+    for (auto e : p->slot_ev) cudaEventDestroy(e);
+    for (auto e : p->tev) cudaEventDestroy(e);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  }
+  delete p->index;
+  delete p;
+}
+
+mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
+  if (!cfg || !out) return MP_ERR_CONFIG;
+  if (cfg->layers < 1 || cfg->layers > 256 || cfg->kv_heads < 1 || cfg->head_dim < 1 ||
+      cfg->elem_bytes < 1 || cfg->block_tokens < 1 || cfg->hbm_blocks < 1 ||
+      cfg->hbm_blocks >= (1ll << 31) || cfg->dram_blocks < 0 || cfg->dram_blocks >= (1ll << 31) ||
+      cfg->instance_id < 0 || cfg->instance_id >= (1 << 24)) {
+    set_err("invalid pool config");
+    return MP_ERR_CONFIG;
+  }
+  const int64_t chunk =
+      (int64_t)cfg->block_tokens * cfg->kv_heads * cfg->head_dim * cfg->elem_bytes;
+  if (chunk % 16 != 0) {
+    set_err("chunk bytes must be a multiple of 16");
+    return MP_ERR_CONFIG;
+  }
+  mp_pool* p = new mp_pool();
+  p->inst = cfg->instance_id;
+  p->dev = cfg->device;
+  p->L = cfg->layers;
+  p->H = cfg->kv_heads;
+  p->D = cfg->head_dim;
+  p->elem = cfg->elem_bytes;
+  p->B = cfg->block_tokens;
+  p->verify = cfg->verify != 0;
+  p->chunk = chunk;
+  p->nch = 2 * cfg->layers;
+  p->Pb = chunk * p->nch;
+  p->n_hbm = cfg->hbm_blocks;
+  p->n_dram = cfg->dram_blocks;
+  p->max_ctas = cfg->max_ctas;
+  p->staging_slots = cfg->staging_slots > 0 ? cfg->staging_slots : 4;
+  p->staging_bytes = cfg->staging_bytes > 0 ? cfg->staging_bytes : (256ll << 20);
+  p->index = new mpi::Index(p->B, p->n_hbm, p->n_dram);
+  for (int m = 0; m < 2; ++m) {
+    const int64_t n = m == 0 ? p->n_hbm : p->n_dram;
+    p->st[m].assign((size_t)n, ST_FREE);
+    p->alloc_by[m].assign((size_t)n, -1);
+    p->nfree[m] = n;
+  }
+  p->hfree.assign((size_t)((p->n_hbm + 63) / 64), ~0ull);
+  if (p->n_hbm % 64) p->hfree.back() = (1ull << (p->n_hbm % 64)) - 1ull;
+  for (int32_t i = 0; i < (int32_t)p->n_dram; ++i) p->dram_free.insert(p->dram_free.end(), i);
+  auto fail = [&](mp_status s) {
+    mp_pool_destroy(p);
+    return s;
+  };
+#define CKC(x)                                                  \
+  do {                                                          \
+    cudaError_t e_ = (x);                                       \
+    if (e_ != cudaSuccess) {                                    \
+      set_err(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+      return fail(MP_ERR_CUDA);                                 \
+    }                                                           \
+  } while (0)
+  int ndev = 0;
+  CKC(cudaGetDeviceCount(&ndev));
+  if (cfg->device < 0 || cfg->device >= ndev) {
+    set_err("device ordinal out of range");
+    return fail(MP_ERR_CONFIG);
+  }
+  DevGuard g(p->dev);
+  CKC(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming));
+  p->slot_ev.resize((size_t)p->staging_slots);
+  for (auto& e : p->slot_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  p->tev.resize(2 * (size_t)kTimedPairs);
+  for (auto& e : p->tev) CKC(cudaEventCreate(&e));
+  p->slabs.resize((size_t)p->nch);
+  if (cfg->slabs) {
+    for (int j = 0; j < p->nch; ++j) {
+      p->slabs[(size_t)j] = (char*)cfg->slabs[j];
+      if (!p->slabs[(size_t)j] || ((uintptr_t)p->slabs[(size_t)j] & 15)) {
+        set_err("slab pointers must be non-null and 16-byte aligned");
+        return fail(MP_ERR_CONFIG);
+      }
+    }
+  } else {
+    const size_t bytes = (size_t)p->nch * (size_t)p->n_hbm * (size_t)chunk;
+    CKC(cudaMalloc(&p->own_slab_region, bytes));
+    for (int j = 0; j < p->nch; ++j)
+      p->slabs[(size_t)j] = (char*)p->own_slab_region + (size_t)j * p->n_hbm * chunk;
+  }
+  CKC(cudaMalloc(&p->d_slabs, sizeof(char*) * p->nch));
+  CKC(cudaMemcpy(p->d_slabs, p->slabs.data(), sizeof(char*) * p->nch, cudaMemcpyHostToDevice));
+  p->nwords = (int)((p->n_hbm + 31) / 32);
+  std::vector<uint32_t> bm((size_t)p->nwords, 0xFFFFFFFFu);
+  if (p->n_hbm % 32) bm.back() = (1u << (p->n_hbm % 32)) - 1u;
+  CKC(cudaMalloc(&p->d_bitmap, sizeof(uint32_t) * p->nwords));
+  CKC(cudaMemcpy(p->d_bitmap, bm.data(), sizeof(uint32_t) * p->nwords, cudaMemcpyHostToDevice));
+  CKC(cudaMalloc(&p->d_err, sizeof(int)));
+  CKC(cudaMemset(p->d_err, 0, sizeof(int)));
+  p->ar.cap = 16 * std::max<int64_t>(std::max(p->n_hbm, p->n_dram), 4096);
+  CKC(cudaMalloc(&p->ar.d, sizeof(int) * p->ar.cap));
+  CKC(cudaHostAlloc(&p->ar.h, sizeof(int) * p->ar.cap, cudaHostAllocMapped | cudaHostAllocPortable));
+  if (p->n_dram > 0) {
+    if (cfg->dram_base) {
+      p->dram = (char*)cfg->dram_base;
+    } else {
+      CKC(cudaHostAlloc(&p->dram, (size_t)p->n_dram * (size_t)p->Pb,
+                        cudaHostAllocMapped | cudaHostAllocPortable));
+      p->own_dram = true;
+    }
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, p->dram, 0) != cudaSuccess) {
+      cudaGetLastError();
+      set_err("dram_base is not pinned (cudaHostAlloc / cudaHostRegister required)");
+      return fail(MP_ERR_CONFIG);
+    }
+    p->dram_dev = (char*)dp;
+  }
+  CKC(cudaMalloc(&p->staging, (size_t)p->staging_bytes));
+#undef CKC
+  *out = p;
+  return MP_OK;
+}
+
+mp_status mp_connect(mp_pool* a, mp_pool* b) {
+  if (!a || !b || a == b || a->inst == b->inst) return MP_ERR_CONFIG;
+  if (a->L != b->L || a->chunk != b->chunk || a->B != b->B) {
+    set_err("pools have different KV shapes");
+    return MP_ERR_CONFIG;
+  }
+  if (a->dev != b->dev) {
+    int ab = 0, ba = 0;
+    CK(cudaDeviceCanAccessPeer(&ab, a->dev, b->dev));
+    CK(cudaDeviceCanAccessPeer(&ba, b->dev, a->dev));
+    if (!ab || !ba) {
+      set_err("no CUDA peer access between the two devices");
+      return MP_ERR_DST_UNREACHABLE;
+    }
+    for (int dir = 0; dir < 2; ++dir) {
+      mp_pool* x = dir ? b : a;
+      mp_pool* y = dir ? a : b;
+      DevGuard g(x->dev);
+      cudaError_t e = cudaDeviceEnablePeerAccess(y->dev, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else
+        CK(e);
+    }
+  }
+  for (int dir = 0; dir < 2; ++dir) {
+    mp_pool* x = dir ? b : a;
+    mp_pool* y = dir ? a : b;
+    DevGuard g(x->dev);
+    char** t = nullptr;
+    CK(cudaMalloc(&t, sizeof(char*) * y->nch));
+    CK(cudaMemcpy(t, y->slabs.data(), sizeof(char*) * y->nch, cudaMemcpyHostToDevice));
+    auto it = x->peer_tables.find(y->inst);
+    if (it != x->peer_tables.end()) cudaFree(it->second);
+    x->peer_tables[y->inst] = t;
+    x->peers[y->inst] = y;
+  }
+  return MP_OK;
+}
+
+mp_status mp_pool_info_get(const mp_pool* p, mp_pool_info* o) {
+  if (!p || !o) return MP_ERR_CONFIG;
+  o->chunk_bytes = p->chunk;
+  o->block_bytes = p->Pb;
+  o->hbm_blocks = p->n_hbm;
+  o->dram_blocks = p->n_dram;
+  o->hbm_free = p->nfree[0];
+  o->dram_free = p->nfree[1];
+  o->index_blocks = (int64_t)p->index->size();
+  o->clock = p->index->clock();
+  o->epoch = p->epoch;
+  o->instance_id = p->inst;
+  o->device = p->dev;
+  o->layers = p->L;
+  o->block_tokens = p->B;
+  return MP_OK;
+}
+
+mp_status mp_sync(mp_pool* p) {
+  if (!p) return MP_ERR_CONFIG;
+  DevGuard g(p->dev);
+  return sync(p);
+}
+
+mp_status mp_profile(mp_pool* p, int32_t enable) {
+  if (!p) return MP_ERR_CONFIG;
+  DevGuard g(p->dev);
+  if (!enable && p->profiling) TRY(drain(p));
+  p->profiling = enable != 0;
+  return MP_OK;
+}
+
+mp_status mp_stats_get(const mp_pool* p, mp_stats* o) {
+  if (!p || !o) return MP_ERR_CONFIG;
+  *o = p->stats;
+  return MP_OK;
+}
+
+mp_status mp_stats_reset(mp_pool* p) {
+  if (!p) return MP_ERR_CONFIG;
+  DevGuard g(p->dev);
+  TRY(drain(p));
+  p->stats = mp_stats{};
+  return MP_OK;
+}
+
+}  // extern "C"

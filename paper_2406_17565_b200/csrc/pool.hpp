@@ -1,0 +1,172 @@
+// pool.hpp -- internal state of one MemPool instance (mp_pool) and the
+// runtime helpers shared by the C-ABI translation units.
+//
+// Execution model (B200-first):
+//  * every pool owns one CUDA stream; all device work of the pool (allocator,
+//    free, migration kernels, fills) is stream-ordered on it, so host-side
+//    bookkeeping never waits for the device except where a result must be
+//    host-visible (the call's return for synchronous calls, mp_sync for
+//    MP_XFER_ASYNC transfers);
+//  * the HBM allocator is device-resident (bitmap + alloc_kernel writing the
+//    destination block table in HBM, read directly by the migration kernel);
+//    the host keeps an exact shadow of it (same lowest-first rule, R2) so the
+//    prompt index can be updated without a device round trip.  In verify mode
+//    every device allocation is checked against the shadow at the next sync;
+//  * cross-pool work (a transfer) is ordered with events: the executing
+//    stream waits for the other pool's stream before the copy and the other
+//    pool's stream waits for the copy after it.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <deque>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/mempool.h"
+#include "index.hpp"
+#include "kernels.cuh"
+
+namespace mp {
+
+void set_err(const std::string& s);
+const std::string& get_err();
+
+enum : uint8_t { ST_FREE = 0, ST_ACTIVE = 1, ST_INDEXED = 2, ST_ORPHAN = 3 };
+
+struct DevGuard {
+  int prev = -1, want;
+  explicit DevGuard(int d) : want(d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
+#define CK(x)                                                                 \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess) {                                                  \
+      ::mp::set_err(std::string(#x) + ": " + cudaGetErrorString(e_));         \
+      return MP_ERR_CUDA;                                                     \
+    }                                                                         \
+  } while (0)
+
+#define TRY(x)                  \
+  do {                          \
+    mp_status s_ = (x);         \
+    if (s_ != MP_OK) return s_; \
+  } while (0)
+
+struct Msg {
+  int32_t kind, src;
+  std::vector<uint8_t> priv;
+  std::vector<mp_addr> addrs;
+};
+
+// Ring arena of int32 ids: a device buffer and a mapped pinned mirror of the
+// same size.  Uploads are staged through the mirror; wrapping drains the
+// stream first, so a region is never rewritten while a copy may read it.
+struct Arena {
+  int* d = nullptr;
+  int* h = nullptr;
+  int64_t cap = 0, used = 0;
+};
+
+struct TimedLaunch {
+  int pair;
+  uint64_t bytes;
+};
+
+struct PendingVerify {
+  const int* host;  // device allocator output (mapped mirror)
+  std::vector<int32_t> want;
+};
+
+}  // namespace mp
+
+struct mp_pool {
+  // shape
+  int32_t inst = 0, dev = 0, L = 0, H = 0, D = 0, elem = 0, B = 0;
+  bool verify = false;
+  int64_t chunk = 0, Pb = 0, n_hbm = 0, n_dram = 0;
+  int nch = 0;
+  int max_ctas = 0;
+  // device memory
+  std::vector<char*> slabs;
+  void* own_slab_region = nullptr;
+  char** d_slabs = nullptr;
+  uint32_t* d_bitmap = nullptr;
+  int nwords = 0;
+  int* d_err = nullptr;
+  mp::Arena ar;
+  char* dram = nullptr;      // host pointer of the pinned DRAM pool
+  char* dram_dev = nullptr;  // device-visible (mapped) pointer
+  bool own_dram = false;
+  char* staging = nullptr;
+  int64_t staging_bytes = 0;
+  int staging_slots = 4;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaEvent_t ev_order = nullptr;
+  std::vector<cudaEvent_t> slot_ev;
+  // profiling: a ring of (start, end) event pairs per migration launch
+  bool profiling = false;
+  std::vector<cudaEvent_t> tev;
+  std::vector<mp::TimedLaunch> timed;
+  int tev_next = 0;
+  mp_stats stats{};
+  // host shadow of block ownership
+  std::vector<uint8_t> st[2];
+  std::vector<int32_t> alloc_by[2];
+  int64_t nfree[2] = {0, 0};
+  std::vector<uint64_t> hfree;             // HBM shadow bitmap (bit = 1: free)
+  std::set<int32_t> dram_free;             // host-managed pinned DRAM allocator
+  std::map<int32_t, int32_t> orphan_ref[2];
+  std::vector<int32_t> pending_free;       // HBM ids to set in the device bitmap
+  std::vector<mp::PendingVerify> pending_verify;
+  mpi::Index* index = nullptr;
+  uint64_t epoch = 0;
+  std::map<int32_t, mp_pool*> peers;
+  std::map<int32_t, char**> peer_tables;   // peer's slab table, on this device
+  std::deque<mp::Msg> inbox;
+};
+
+namespace mp {
+
+constexpr int kTimedPairs = 512;
+
+int* arena_take(mp_pool* p, int64_t n, int** host);
+mp_status upload_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d_out);
+mp_status flush_frees(mp_pool* p);
+mp_status drain(mp_pool* p);  // stream sync + timing + verification
+mp_status sync(mp_pool* p);   // flush_frees + drain
+mp_status link(mp_pool* signal, mp_pool* waiter);  // waiter's stream waits for signal's
+
+bool decode(const mp_pool* p, mp_addr a, int* med, int32_t* idx);
+inline mp_addr enc(const mp_pool* p, int med, int32_t idx) { return MP_ADDR(p->inst, med, idx); }
+
+void free_block(mp_pool* p, int med, int32_t idx);
+void evict_internal(mp_pool* p, int64_t n, int med, std::vector<int32_t>* freed);
+bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>& pinned);
+// Lowest-first HBM allocation: host shadow ids + the device allocator writing
+// the same ids into HBM (d_ids) for the kernels that follow on the stream.
+mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,
+                    int** d_ids);
+std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
+
+mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
+                               const mpk::Endpoint& b, int64_t n, int j0, int nj);
+inline mpk::Endpoint pool_ep(char** slabs, const int* ids) { return {slabs, nullptr, 0, ids}; }
+inline mpk::Endpoint agg_ep(char* base, long long stride, const int* ids) {
+  return {nullptr, base, stride, ids};
+}
+
+mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const mp_addr* addrs,
+                          int64_t n_addr, uint32_t flags, int64_t* n_dup);
+void unpin_nodes(mp_pool* p, const std::vector<mpi::Node*>& nodes);
+
+}  // namespace mp

@@ -20,6 +20,7 @@ HBM, DRAM, MIXED = 0, 1, 2
 
 XFER_DST_GIVEN = 1 << 0
 XFER_DEDUP = 1 << 1
+XFER_ASYNC = 1 << 2
 INS_ERR_ON_CONFLICT = 1 << 4
 MATCH_PIN = 1 << 5
 PATH_AUTO = 0 << 8
@@ -118,6 +119,7 @@ SIGNATURES = {
     "mp_pool_destroy": (None, [_P]),
     "mp_connect": (_I32, [_P, _P]),
     "mp_pool_info_get": (_I32, [_P, C.POINTER(PoolInfo)]),
+    "mp_sync": (_I32, [_P]),
     "mp_status_str": (C.c_char_p, [_I32]),
     "mp_last_error": (C.c_char_p, []),
     "mp_alloc_mem": (_I32, [_P, _I64, _I32, _I32, _PU64]),
@@ -150,7 +152,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     if not os.path.exists(path):
         raise ImportError(
             f"libmempool.so not found at {path}; build it with "
-            "`python -m paper_2406_17565_b200.build` (there is no CPU fallback)")
+            "`python paper_2406_17565_b200/build.py` (there is no CPU fallback)")
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
@@ -225,6 +227,10 @@ class Pool:
     @property
     def handle(self):
         return self._h
+
+    def sync(self):
+        """Wait for all device work issued on this pool (mp_sync)."""
+        _check(_lib.mp_sync(self._h), "sync")
 
     def info(self) -> PoolInfo:
         o = PoolInfo()

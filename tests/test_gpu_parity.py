@@ -17,6 +17,8 @@ from workloads.traces import golden_prompts
 pytestmark = pytest.mark.gpu
 
 PATHS = [M.PATH_FUSED, M.PATH_STAGED, M.PATH_CE]
+# stream-ordered (MP_XFER_ASYNC) variants: results must not depend on the sync
+PATHS_ASYNC = [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_CE | M.XFER_ASYNC]
 
 
 def golden_pair(dedup, path, n_dram=64):
@@ -35,7 +37,7 @@ def golden_pair(dedup, path, n_dram=64):
     return P, D, res
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS + PATHS_ASYNC)
 @pytest.mark.parametrize("dedup", [False, True])
 def test_golden_tiny(dedup, path):
     P, D, res = golden_pair(dedup, path)
@@ -175,7 +177,7 @@ def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24):
     D.check_state()
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS + PATHS_ASYNC)
 def test_random_ops_tiny(path):
     for seed in range(3):
         random_ops(seed, TINY, 300, path)
