@@ -129,8 +129,8 @@ def run_ours(args, rank, world, dist):
     B, Pb = shape.block_tokens, shape.block_bytes
     seed = seed_for(1) + 1000 * rank
     n_blocks = args.pool_blocks
-    P = make_pool(M, torch, 2 * rank, dev, shape, n_blocks)
-    D = make_pool(M, torch, 2 * rank + 1, dev, shape, n_blocks)
+    P = make_pool(M, torch, 2 * rank, dev, shape, n_blocks, copy_kernel=args.copy_kernel)
+    D = make_pool(M, torch, 2 * rank + 1, dev, shape, n_blocks, copy_kernel=args.copy_kernel)
     M.connect(P, D)
 
     # ---- untimed setup: the prefill instance's cache (PD-Caching-1 step 2)
@@ -283,32 +283,34 @@ def side_measurements(M, torch, P, D, shape, seed, peak, args):
     """Standalone pack / unpack (A4/A6, HBM roofline) and swap (A8/A9)."""
     out = {}
     Pb = shape.block_bytes
-    n = 128   # 2048-token prompt (P:863) = 1 GiB at 7B
-    free = D.info().hbm_free
-    if free >= 2 * n:
-        a = D.alloc_mem(n)
-        D.debug_fill(a, seed)
-        perm = np.random.default_rng(seed).permutation(n)
-        a = a[perm]
-        stg = torch.empty(n * Pb, dtype=torch.uint8, device=P._region.device)
-        b = D.alloc_mem(n)
-        for name, fn in (("pack", lambda: D.pack(a, 0, shape.layers, stg.data_ptr())),
-                         ("unpack", lambda: D.unpack(stg.data_ptr(), b, 0, shape.layers))):
+    n = 128   # 2048-token prompt (P:863) = 1 GiB at 7B: 8x the 126 MB L2
+    dev = torch.cuda.current_device()
+    del P, D
+    for ck, ck_name in ((1, "vector"), (2, "bulk")):
+        X = make_pool(M, torch, 200 + ck, dev, shape, 2 * n + 8, copy_kernel=ck)
+        a = X.alloc_mem(n)
+        X.debug_fill(a, seed)
+        a = a[np.random.default_rng(seed).permutation(n)]      # scattered ids
+        stg = torch.empty(n * Pb, dtype=torch.uint8, device=f"cuda:{dev}")
+        b = X.alloc_mem(n)
+        for name, fn in (("pack", lambda: X.pack(a, 0, shape.layers, stg.data_ptr())),
+                         ("unpack", lambda: X.unpack(stg.data_ptr(), b, 0, shape.layers))):
             for _ in range(3):
                 fn()
-            D.stats_reset()
-            D.profile(True)
+            X.stats_reset()
+            X.profile(True)
             for _ in range(10):
                 fn()
-            D.profile(False)
-            s = D.stats()
+            X.profile(False)
+            s = X.stats()
             kms = s["kernel_ms"] / s["timed_launches"]
             ach = 2.0 * n * Pb / (kms * 1e-3) / 1e9
-            out[name] = {"blocks": n, "GBps_payload": round(n * Pb / (kms * 1e-3) / 1e9, 1),
-                         "hbm_GBps_rw": round(ach, 1), "frac_of_hbm": round(ach / peak, 4),
-                         "avg_kernel_ms": round(kms, 4)}
-        D.free_mem(np.concatenate([a, b]))
-        del stg
+            out[f"{name}_{ck_name}"] = {
+                "blocks": n, "GBps_payload": round(n * Pb / (kms * 1e-3) / 1e9, 1),
+                "hbm_GBps_rw": round(ach, 1), "frac_of_hbm": round(ach / peak, 4),
+                "avg_kernel_ms": round(kms, 4)}
+        X.close()
+        del stg, X
     # swap sweep point: a separate small pool with pinned DRAM
     if not args.no_swap:
         try:
@@ -409,6 +411,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool-blocks", type=int, default=4096)
     ap.add_argument("--batch-blocks", type=int, default=1024)
+    ap.add_argument("--copy-kernel", type=int, default=0,
+                    help="0 auto, 1 vector LD/ST, 2 bulk cp.async (TMA) copy engine")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

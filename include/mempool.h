@@ -118,6 +118,8 @@ typedef struct {
   int64_t staging_bytes; /* device staging for the STAGED path (0: 256 MiB) */
   int32_t staging_slots; /* ring depth (0: 4) */
   int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = one full wave) */
+  int32_t copy_kernel;   /* device<->device copy engine: 0 auto, 1 vector LD/ST, 2 bulk (TMA) */
+  int32_t reserved0;
 } mp_pool_config;
 
 typedef struct {

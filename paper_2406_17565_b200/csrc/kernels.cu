@@ -72,6 +72,138 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA engine) variant of the same gather/scatter.  One elected
+// lane per CTA drives a ring of kStages shared-memory stages:
+//   cp.async.bulk global -> shared  (completes on an mbarrier, tx-count bytes)
+//   cp.async.bulk shared -> global  (bulk_group; wait_group.read frees a stage)
+// so each SM keeps (kStages-1) x kPiece bytes of loads plus the stores in
+// flight with a handful of instructions; the copy itself never touches the
+// register file.  Work unit = one kPiece-byte piece of one chunk (the last
+// piece of a chunk may be shorter; chunks are multiples of 16 B).
+constexpr int kPiece = 16384;
+constexpr int kStages = 4;
+constexpr int kBulkThreads = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <bool kSrcPool, bool kDstPool>
+__device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& dst, int j0, int nj,
+                                          long long chunk, unsigned pieces_per_chunk, unsigned u,
+                                          const char** sp, char** dp, uint32_t* bytes) {
+  const unsigned ch = u / pieces_per_chunk;
+  const unsigned part = u - ch * pieces_per_chunk;
+  const unsigned i = ch / (unsigned)nj;
+  const unsigned jr = ch - i * (unsigned)nj;
+  const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
+  const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
+  const long long off = (long long)part * kPiece;
+  *sp = (kSrcPool ? (const char*)__ldg((const unsigned long long*)(src.slabs + j0 + jr)) + sid * chunk
+                  : src.base + sid * src.stride + (long long)jr * chunk) +
+        off;
+  *dp = (kDstPool ? (char*)__ldg((const unsigned long long*)(dst.slabs + j0 + jr)) + did * chunk
+                  : dst.base + did * dst.stride + (long long)jr * chunk) +
+        off;
+  const long long rest = chunk - off;
+  *bytes = (uint32_t)(rest < kPiece ? rest : kPiece);
+}
+
+template <bool kSrcPool, bool kDstPool>
+__global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(Endpoint src, Endpoint dst,
+                                                                    int j0, int nj,
+                                                                    long long chunk,
+                                                                    unsigned pieces_per_chunk,
+                                                                    unsigned total_units) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[kStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  // units of this CTA: u_k = blockIdx.x + k * gridDim.x
+  const unsigned n_mine =
+      blockIdx.x < total_units ? (total_units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const char* sp;
+  char* dp;
+  uint32_t bytes;
+  char* dsts[kStages];
+  uint32_t lens[kStages];
+  for (unsigned k = 0; k < n_mine && k < (unsigned)kStages; ++k) {
+    unit_addr<kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
+                                  blockIdx.x + k * gridDim.x, &sp, &dp, &bytes);
+    dsts[k] = dp;
+    lens[k] = bytes;
+    mbar_expect_tx(&bars[k], bytes);
+    bulk_load(smem + (size_t)k * kPiece, sp, bytes, &bars[k]);
+  }
+  for (unsigned k = 0; k < n_mine; ++k) {
+    const unsigned s = k % kStages;
+    mbar_wait(&bars[s], (k / kStages) & 1u);
+    bulk_store(dsts[s], smem + (size_t)s * kPiece, lens[s]);
+    // refill the stage the previous store used, once that store has read it
+    if (k >= 1 && k - 1 + kStages < n_mine) {
+      bulk_wait_read<1>();
+      const unsigned r = (k - 1) % kStages;
+      unit_addr<kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
+                                    blockIdx.x + (k - 1 + kStages) * gridDim.x, &sp, &dp,
+                                    &bytes);
+      dsts[r] = dp;
+      lens[r] = bytes;
+      mbar_expect_tx(&bars[r], bytes);
+      bulk_load(smem + (size_t)r * kPiece, sp, bytes, &bars[r]);
+    }
+  }
+  bulk_wait_all();
+}
+
 // Single CTA of 1024 threads: popcount per thread-range of words, block-wide
 // exclusive scan, then every thread emits its lowest set bits in order, so
 // the ids come out ascending (R2 lowest-first).
@@ -168,9 +300,45 @@ int sm_count(int device) {
   return v > 0 ? v : 148;
 }
 
+template <bool kSrcPool, bool kDstPool>
+static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
+                               long long chunk, int max_ctas, cudaStream_t stream) {
+  const unsigned pieces = (unsigned)((chunk + kPiece - 1) / kPiece);
+  const unsigned long long total = (unsigned long long)n * nj * pieces;
+  if (total >= (1ull << 32)) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)kStages * kPiece;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cached_cap[64] = {0};  // per device (the smem attribute is per device too)
+  int cap = max_ctas;
+  if (dev >= 64 || cached_cap[dev] <= 0) {
+    cudaFuncSetAttribute(migrate_bulk_kernel<kSrcPool, kDstPool>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, migrate_bulk_kernel<kSrcPool, kDstPool>, kBulkThreads, smem);
+    if (per_sm <= 0) per_sm = 1;
+    if (dev < 64) cached_cap[dev] = per_sm * sm_count(dev);
+    if (cap <= 0) cap = per_sm * sm_count(dev);
+  } else if (cap <= 0) {
+    cap = cached_cap[dev];
+  }
+  const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
+  migrate_bulk_kernel<kSrcPool, kDstPool><<<grid, kBulkThreads, smem, stream>>>(
+      src, dst, j0, nj, chunk, pieces, (unsigned)total);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
-                           long long chunk, int max_ctas, cudaStream_t stream) {
+                           long long chunk, int max_ctas, cudaStream_t stream, int variant) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
+  if (variant == kCopyBulk) {
+    const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
+    if (sp && dp) return launch_bulk<true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+    if (sp) return launch_bulk<true, false>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+    if (dp) return launch_bulk<false, true>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+    return launch_bulk<false, false>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+  }
   const unsigned units_per_chunk = (unsigned)((chunk + kUnitBytes - 1) / kUnitBytes);
   const unsigned long long total = (unsigned long long)n * nj * units_per_chunk;
   if (total >= (1ull << 32)) return cudaErrorInvalidValue;

@@ -22,10 +22,15 @@ struct Endpoint {
   const int* ids;      // device array of n ids or nullptr
 };
 
+// Copy engines of the migration kernel.
+enum CopyVariant { kCopyAuto = 0, kCopyVector = 1, kCopyBulk = 2 };
+
 // dst.chunk(ids_d[i], j) = src.chunk(ids_s[i], j) for i < n, j in [j0, j0+nj).
-// max_ctas <= 0: auto (4 CTAs per SM).
+// variant kCopyVector: 16-byte vector loads/stores by every lane;
+// kCopyBulk: cp.async.bulk (TMA engine) ring through shared memory.
+// max_ctas <= 0: one full wave (occupancy x SMs).
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
-                           long long chunk, int max_ctas, cudaStream_t stream);
+                           long long chunk, int max_ctas, cudaStream_t stream, int variant);
 
 // Lowest-first allocation of n blocks from a bitmap (bit = 1: free).  Writes
 // the ids ascending into out_dev (device) and out_host (mapped pinned host,

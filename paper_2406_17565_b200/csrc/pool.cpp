@@ -37,7 +37,7 @@ mp_status upload_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d_out) {
   }
   if (!ids.empty()) {
     std::memcpy(h, ids.data(), ids.size() * sizeof(int32_t));
-    CK(cudaMemcpyAsync(d, h, ids.size() * sizeof(int32_t), cudaMemcpyHostToDevice, p->stream));
+    CK(cudaMemcpyAsync(d, h, ids.size() * sizeof(int32_t), cudaMemcpyHostToDevice, p->meta));
   }
   *d_out = d;
   return MP_OK;
@@ -50,12 +50,13 @@ mp_status flush_frees(mp_pool* p) {
   ids.swap(p->pending_free);
   int* d = nullptr;
   TRY(upload_ids(p, ids, &d));
-  CK(mpk::launch_free(p->d_bitmap, d, (int)ids.size(), p->stream));
+  CK(mpk::launch_free(p->d_bitmap, d, (int)ids.size(), p->meta));
   p->stats.aux_launches += 1;
   return MP_OK;
 }
 
 mp_status drain(mp_pool* p) {
+  CK(cudaStreamSynchronize(p->meta));
   CK(cudaStreamSynchronize(p->stream));
   for (const TimedLaunch& t : p->timed) {
     float ms = 0.f;
@@ -97,6 +98,12 @@ mp_status link(mp_pool* signal, mp_pool* waiter) {
   }
   DevGuard g(waiter->dev);
   CK(cudaStreamWaitEvent(waiter->stream, signal->ev_order, 0));
+  return MP_OK;
+}
+
+mp_status meta_fence(mp_pool* p) {
+  CK(cudaEventRecord(p->ev_meta, p->meta));
+  CK(cudaStreamWaitEvent(p->stream, p->ev_meta, 0));
   return MP_OK;
 }
 
@@ -174,7 +181,7 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
     return MP_ERR_INTERNAL;
   }
   CK(mpk::launch_alloc(p->d_bitmap, p->nwords, (int)n, d, p->verify ? h : nullptr, p->d_err,
-                       p->stream));
+                       p->meta));
   p->stats.aux_launches += 1;
   if (p->verify) p->pending_verify.push_back({h, *ids});
   *d_ids = d;
@@ -200,6 +207,7 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   if (n <= 0) return MP_OK;
   const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)p->chunk;
   const bool timed = p->profiling && s == p->stream;
+  if (s == p->stream) TRY(meta_fence(p));  // ids uploaded / allocated on meta
   int pair = -1;
   if (timed) {
     if ((int)p->timed.size() >= kTimedPairs) TRY(drain(p));
@@ -207,7 +215,12 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
     p->tev_next = (p->tev_next + 1) % kTimedPairs;
     CK(cudaEventRecord(p->tev[2 * (size_t)pair], s));
   }
-  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, p->chunk, p->max_ctas, s));
+  // The bulk (TMA) engine only for device <-> device copies; mapped pinned
+  // DRAM (swap) stays on the vector path.
+  const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
+  int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyVector : p->copy_kernel;
+  if (host_side) variant = mpk::kCopyVector;
+  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, p->chunk, p->max_ctas, s, variant));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});
@@ -251,6 +264,7 @@ void mp_pool_destroy(mp_pool* p) {
   if (!p) return;
   {
     DevGuard g(p->dev);
+    if (p->meta) cudaStreamSynchronize(p->meta);
     if (p->stream) cudaStreamSynchronize(p->stream);
     for (auto& kv : p->peers) {
       mp_pool* q = kv.second;
@@ -259,6 +273,7 @@ void mp_pool_destroy(mp_pool* p) {
       if (it != q->peer_tables.end()) {
         DevGuard g2(q->dev);
         if (q->stream) cudaStreamSynchronize(q->stream);
+        if (q->meta) cudaStreamSynchronize(q->meta);
         cudaFree(it->second);
         q->peer_tables.erase(it);
       }
@@ -273,9 +288,11 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->own_dram && p->dram) cudaFreeHost(p->dram);
     if (p->staging) cudaFree(p->staging);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
+    if (p->ev_meta) cudaEventDestroy(p->ev_meta);
     for (auto e : p->slot_ev) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->meta) cudaStreamDestroy(p->meta);
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   }
   delete p->index;
@@ -312,6 +329,13 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->n_hbm = cfg->hbm_blocks;
   p->n_dram = cfg->dram_blocks;
   p->max_ctas = cfg->max_ctas;
+  p->copy_kernel = cfg->copy_kernel;
+  if (p->copy_kernel < 0 || p->copy_kernel > 2) {
+    set_err("copy_kernel must be 0 (auto), 1 (vector) or 2 (bulk)");
+    delete p->index;
+    delete p;
+    return MP_ERR_CONFIG;
+  }
   p->staging_slots = cfg->staging_slots > 0 ? cfg->staging_slots : 4;
   p->staging_bytes = cfg->staging_bytes > 0 ? cfg->staging_bytes : (256ll << 20);
   p->index = new mpi::Index(p->B, p->n_hbm, p->n_dram);
@@ -345,7 +369,9 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   DevGuard g(p->dev);
   CKC(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&p->meta, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&p->ev_meta, cudaEventDisableTiming));
   p->slot_ev.resize((size_t)p->staging_slots);
   for (auto& e : p->slot_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   p->tev.resize(2 * (size_t)kTimedPairs);

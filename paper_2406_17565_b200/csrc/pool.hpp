@@ -96,6 +96,7 @@ struct mp_pool {
   int64_t chunk = 0, Pb = 0, n_hbm = 0, n_dram = 0;
   int nch = 0;
   int max_ctas = 0;
+  int copy_kernel = 0;  // mpk::CopyVariant for device<->device copies
   // device memory
   std::vector<char*> slabs;
   void* own_slab_region = nullptr;
@@ -110,8 +111,14 @@ struct mp_pool {
   char* staging = nullptr;
   int64_t staging_bytes = 0;
   int staging_slots = 4;
-  cudaStream_t stream = nullptr, copy_stream = nullptr;
-  cudaEvent_t ev_order = nullptr;
+  // `stream` carries the KV data movement; `meta` carries the allocator
+  // bitmap kernels and the id uploads, so the allocation of the next transfer
+  // overlaps the copy of the previous one.  A data kernel that consumes ids
+  // waits for `meta` (meta_fence) -- never the other way round: the bitmap is
+  // metadata, and a block handed out again is only written by later kernels
+  // of the data stream, which run after every earlier reader of it.
+  cudaStream_t stream = nullptr, meta = nullptr, copy_stream = nullptr;
+  cudaEvent_t ev_order = nullptr, ev_meta = nullptr;
   std::vector<cudaEvent_t> slot_ev;
   // profiling: a ring of (start, end) event pairs per migration launch
   bool profiling = false;
@@ -145,6 +152,7 @@ mp_status flush_frees(mp_pool* p);
 mp_status drain(mp_pool* p);  // stream sync + timing + verification
 mp_status sync(mp_pool* p);   // flush_frees + drain
 mp_status link(mp_pool* signal, mp_pool* waiter);  // waiter's stream waits for signal's
+mp_status meta_fence(mp_pool* p);                  // p->stream waits for p->meta
 
 bool decode(const mp_pool* p, mp_addr a, int* med, int32_t* idx);
 inline mp_addr enc(const mp_pool* p, int med, int32_t idx) { return MP_ADDR(p->inst, med, idx); }

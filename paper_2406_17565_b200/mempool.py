@@ -77,6 +77,7 @@ class PoolConfig(C.Structure):
         ("hbm_blocks", C.c_int64), ("dram_blocks", C.c_int64),
         ("slabs", C.POINTER(C.c_void_p)), ("dram_base", C.c_void_p),
         ("staging_bytes", C.c_int64), ("staging_slots", C.c_int32), ("max_ctas", C.c_int32),
+        ("copy_kernel", C.c_int32), ("reserved0", C.c_int32),
     ]
 
 
@@ -192,14 +193,15 @@ class Pool:
     def __init__(self, instance_id: int, device: int, layers: int, kv_heads: int,
                  head_dim: int, block_tokens: int, hbm_blocks: int, dram_blocks: int = 0,
                  elem_bytes: int = 2, slabs=None, dram_base=None, staging_bytes: int = 0,
-                 staging_slots: int = 0, max_ctas: int = 0, verify: bool = False):
+                 staging_slots: int = 0, max_ctas: int = 0, verify: bool = False,
+                 copy_kernel: int = 0):
         self.inst = instance_id
         self.B = block_tokens
         self.L = layers
         self._slab_arr = None
         cfg = PoolConfig(instance_id, device, layers, kv_heads, head_dim, elem_bytes,
                          block_tokens, int(verify), hbm_blocks, dram_blocks, None,
-                         dram_base, staging_bytes, staging_slots, max_ctas)
+                         dram_base, staging_bytes, staging_slots, max_ctas, copy_kernel, 0)
         if slabs is not None:
             assert len(slabs) == 2 * layers
             self._slab_arr = (C.c_void_p * len(slabs))(*[int(s) for s in slabs])

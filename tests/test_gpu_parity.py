@@ -92,10 +92,10 @@ def test_private_and_transfer_layers():
     assert [M.addr_index(a) for a in kinds[-1][3]] == [x[2] for x in out]
 
 
-def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24):
+def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0):
     rng = np.random.default_rng(seed)
-    P = Twin(0, shape, n_hbm, n_dram)
-    D = Twin(1, shape, n_hbm, n_dram)
+    P = Twin(0, shape, n_hbm, n_dram, copy_kernel=copy_kernel)
+    D = Twin(1, shape, n_hbm, n_dram, copy_kernel=copy_kernel)
     connect(P, D)
     B = shape.block_tokens
     pools = {0: P, 1: D}
@@ -183,12 +183,28 @@ def test_random_ops_tiny(path):
         random_ops(seed, TINY, 300, path)
 
 
-def test_random_ops_ragged_chunk():
+@pytest.mark.parametrize("path", [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_STAGED])
+def test_random_ops_bulk_copy_engine(path):
+    """The cp.async.bulk (TMA) copy engine, tiny chunks (4 KiB < one 16 KiB piece)."""
+    for seed in range(2):
+        random_ops(100 + seed, TINY, 300, path, copy_kernel=2)
+
+
+@pytest.mark.parametrize("copy_kernel", [1, 2])
+def test_random_ops_ragged_chunk(copy_kernel):
     # chunk = 8*3*24*2 = 1152 B: not a multiple of the kernel's 4 KiB warp
-    # unit -> exercises the predicated tail; B = 8
+    # unit / 16 KiB bulk piece -> exercises the predicated tail; B = 8
     shape = KVShape("ragged", 3, 3, 24, 8)
-    random_ops(11, shape, 300, M.PATH_FUSED)
-    random_ops(12, shape, 150, M.PATH_STAGED)
+    random_ops(11, shape, 300, M.PATH_FUSED, copy_kernel=copy_kernel)
+    random_ops(12, shape, 150, M.PATH_STAGED, copy_kernel=copy_kernel)
+
+
+@pytest.mark.parametrize("copy_kernel", [1, 2])
+def test_multi_piece_chunks(copy_kernel):
+    # chunk = 16*16*88*2 = 45056 B = 2.75 bulk pieces / 11 vector units
+    shape = KVShape("mp", 2, 16, 88, 16)
+    random_ops(21, shape, 120, M.PATH_FUSED | M.XFER_ASYNC, n_hbm=40, n_dram=8,
+               copy_kernel=copy_kernel)
 
 
 def test_pack_unpack_np_take():
