@@ -2,21 +2,23 @@
 """bench.py -- KV migration GB/s & blocks/s vs the HBM / NVLink roofline.
 
 BASELINE.json metric: "KV migration GB/s & blocks/s vs HBM/NVLink roofline at
-1/2/4/8 B200".  Workload (N=1): configs[1], Llama-2-7B-shaped KV (L=32, H=32,
+1/2/4/8 B200".  Workload: configs[1], Llama-2-7B-shaped KV (L=32, H=32,
 D=128, fp16, B=16 -> Pb = 8 MiB per token block), ShareGPT-like prompts,
-1P1D.  On one GPU the prefill (P) and decode (D) instances are two pools on
-cuda:0 and the "wire" is a device-local copy.
+1P1D per pair.  Placement (paper_2406_17565_b200/topology.py):
+N = 1 puts P and D as two pools on cuda:0 (the wire is a device-local copy);
+N > 1 (torchrun) runs one process per GPU, P_i = rank i and D_i = rank i+N/2,
+and P_i's fused kernel stores straight into D_i's IPC-mapped pool over NVLink.
 
 One STEP = one pass of the migration hot path over one batch of requests
 (PD-Caching-2, §5.1):
-    for each request: P.match(prompt)                          (A3)
+    for each request: P.match(prompt)                              (A3)
                       P.transfer_with_insert(D, prompt, src, DEDUP)
                         -> D: match, alloc (A2), gather->store (A6f), insert (A7)
     then D retires the batch: free_mem(partial blocks) + delete(prompts).
-value = payload bytes actually moved (blocks moved x Pb) / step time.
+value = payload bytes actually moved (blocks moved x Pb) / step time, summed
+over pairs, time = max over ranks (CUDA events).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Under torchrun (N>1) every rank runs its own P/D pair (weak scaling).
 """
 import argparse
 import json
@@ -37,6 +39,9 @@ from workloads import traces  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback
 NVLINK_GBS = 900.0          # nominal per direction per GPU (BJ:5)
+NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction
+METRIC = "KV migration GB/s (P->D transfer_with_insert payload)"
+DTYPE = "u16 (fp16 KV copied as opaque 16-bit words)"
 
 
 def load_peaks():
@@ -49,7 +54,7 @@ def load_peaks():
 
 
 # ----------------------------------------------------------------- workload
-def build_requests(shape, seed, hbm_blocks, fill_budget):
+def build_requests(shape, seed, fill_budget):
     """ShareGPT-like sessions until `fill_budget` blocks."""
     B = shape.block_tokens
     sessions = traces.sharegpt_like(seed, n_sessions=4096)
@@ -64,6 +69,21 @@ def build_requests(shape, seed, hbm_blocks, fill_budget):
         for t in s.turns:
             reqs.append((s.sid, t.prompt))
     return reqs
+
+
+def make_batches(reqs, partials, batch_blocks, B):
+    """Batches of whole sessions, each about batch_blocks prompt blocks."""
+    batches, cur, cur_blocks, last_sid = [], [], 0, None
+    for (sid, prompt), partial in zip(reqs, partials):
+        if sid != last_sid and cur_blocks >= batch_blocks:
+            batches.append(cur)
+            cur, cur_blocks = [], 0
+        cur.append((prompt, partial))
+        cur_blocks += -(-len(prompt) // B)
+        last_sid = sid
+    if cur:
+        batches.append(cur)
+    return batches
 
 
 class Clocks:
@@ -119,81 +139,117 @@ def make_pool(M, torch, inst, dev, shape, n_blocks, **kw):
     return p
 
 
-def run_ours(args, rank, world, dist):
-    import torch
-    from paper_2406_17565_b200 import mempool as M
-
-    dev = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(dev)
-    shape = LLAMA2_7B
-    B, Pb = shape.block_tokens, shape.block_bytes
-    seed = seed_for(1) + 1000 * rank
-    n_blocks = args.pool_blocks
-    P = make_pool(M, torch, 2 * rank, dev, shape, n_blocks, copy_kernel=args.copy_kernel)
-    D = make_pool(M, torch, 2 * rank + 1, dev, shape, n_blocks, copy_kernel=args.copy_kernel)
-    M.connect(P, D)
-
-    # ---- untimed setup: the prefill instance's cache (PD-Caching-1 step 2)
-    reqs = build_requests(shape, seed, n_blocks, int(n_blocks * 0.9))
-    req_src = []
+def populate_prefill(P, shape, seed, n_blocks):
+    """Untimed setup: the prefill instance's cache (PD-Caching-1 step 2)."""
+    B = shape.block_tokens
+    reqs = build_requests(shape, seed, int(n_blocks * 0.9))
+    partials = []
     for sid, prompt in reqs:
         mt, matched = P.match(prompt)
         new = P.alloc_mem(-(-len(prompt) // B) - len(matched))
         P.debug_fill(new, seed)
         full = np.concatenate([matched, new])
         P.insert(prompt, full[: len(prompt) // B])
-        partial = full[len(prompt) // B:]       # trailing partial block (active)
-        req_src.append((prompt, partial))
-    # batches of whole sessions, each about batch_blocks blocks
-    batches, cur, cur_blocks = [], [], 0
-    last_sid = None
-    for (sid, prompt), (_, partial) in zip(reqs, req_src):
-        if sid != last_sid and cur_blocks >= args.batch_blocks:
-            batches.append(cur)
-            cur, cur_blocks = [], 0
-        cur.append((prompt, partial))
-        cur_blocks += -(-len(prompt) // B)
-        last_sid = sid
-    if cur:
-        batches.append(cur)
+        partials.append(full[len(prompt) // B:])       # trailing partial block (active)
+    return reqs, partials
 
-    def step(bi, h2d_d2h=None):
+
+def run_ours(args, rank, world, dist):
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    from paper_2406_17565_b200.topology import role_of
+
+    role = role_of(rank, world)
+    dev = int(os.environ.get("LOCAL_RANK", 0)) if args.device < 0 else args.device
+    torch.cuda.set_device(dev)
+    shape = LLAMA2_7B
+    B, Pb = shape.block_tokens, shape.block_bytes
+    seed = seed_for(1) + 1000 * role.pair
+    n_blocks = args.pool_blocks
+    P = D = None
+    if role.kind in ("PD", "P"):
+        P = make_pool(M, torch, role.p_inst, dev, shape, n_blocks, copy_kernel=args.copy_kernel)
+    if role.kind in ("PD", "D"):
+        D = make_pool(M, torch, role.d_inst, dev, shape, n_blocks, copy_kernel=args.copy_kernel)
+    if role.kind == "PD":
+        M.connect(P, D)
+    else:
+        me = P if role.kind == "P" else D
+        blobs = M.exchange_handles(me)
+        me.import_peer(blobs[role.partner][1])
+        dist.barrier()
+    batches = None
+    if P is not None:
+        reqs, partials = populate_prefill(P, shape, seed, n_blocks)
+        batches = make_batches(reqs, partials, args.batch_blocks, B)
+
+    def p_step(bi, io=None):
+        """Prefill side of one step."""
         moved = 0
-        dst_partials = []
+        sent = []
         for prompt, partial in batches[bi % len(batches)]:
             mt, matched = P.match(prompt)
             src = np.concatenate([matched, partial])
-            final, nm = P.transfer_with_insert(D.inst, prompt, src,
-                                               flags=M.XFER_DEDUP | M.XFER_ASYNC)
+            priv = prompt.tobytes() if role.kind == "P" else b""
+            final, nm = P.transfer_with_insert(role.d_inst, prompt, src,
+                                               flags=M.XFER_DEDUP | M.XFER_ASYNC, priv=priv)
             moved += nm
-            dst_partials.append(final[len(prompt) // B:])
-            if h2d_d2h is not None:
-                h2d_d2h[0] += prompt.nbytes + src.nbytes
-                h2d_d2h[1] += final.nbytes
-        D.free_mem(np.concatenate(dst_partials))
-        for prompt, _ in batches[bi % len(batches)]:
+            sent.append((prompt, final))
+            if io is not None:
+                io[0] += prompt.nbytes + src.nbytes + len(priv)
+                io[1] += final.nbytes
+        return moved, sent
+
+    def d_retire(done):
+        """Decode side: the batch is retired (partials freed, prompts deleted)."""
+        D.free_mem(np.concatenate([f[len(p) // B:] for p, f in done]))
+        for prompt, _ in done:
             D.delete(prompt)
-        D.sync()      # the step ends when every block of the batch has landed
-        return moved
+
+    def step(bi, io=None):
+        if role.kind == "PD":
+            moved, sent = p_step(bi, io)
+            d_retire(sent)
+            D.sync()      # the step ends when every block of the batch has landed
+            return moved
+        if role.kind == "P":
+            moved, _ = p_step(bi, io)
+            P.send_mark(role.d_inst, bi)
+            P.sync()
+            return moved
+        served, mark = D.serve(timeout_ms=600_000, until_mark=True)
+        if mark != bi:
+            raise RuntimeError(f"decode rank {rank}: expected mark {bi}, got {mark}")
+        done = []
+        while True:
+            m = D.recv_poll()
+            if m is None:
+                break
+            done.append((np.frombuffer(m[2], dtype=np.int32), m[3]))
+        d_retire(done)
+        D.sync()
+        return 0
 
     def barrier():
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
 
+    timed_pool = D if role.kind == "PD" else (P if role.kind == "P" else D)
     st0, st1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
-                    if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
-                    else f"/tmp/clocks_rank{rank}.csv", dev)
+    out_dir = os.path.join(ROOT, "gpurun_out")
+    clocks = Clocks(os.path.join(out_dir if os.path.isdir(out_dir) else "/tmp",
+                                 f"clocks_rank{rank}.csv"), dev)
     moved = 0
     io = [0, 0]
     with clocks:
         for w in range(args.warmup):
             step(w)
         barrier()
-        D.stats_reset()
-        P.stats_reset()
-        D.profile(True)
+        for pl in (P, D):
+            if pl is not None:
+                pl.stats_reset()
+        timed_pool.profile(True)
         barrier()
         torch.cuda.profiler.start()     # ncu --profile-from-start off sees the timed region only
         st0.record()
@@ -206,86 +262,97 @@ def run_ours(args, rank, world, dist):
         torch.cuda.profiler.stop()
     ms = st0.elapsed_time(st1)
     wall_ms = (t1 - t0) * 1e3
-    D.profile(False)
-    sd, sp = D.stats(), P.stats()
-    # max over ranks
-    tms = torch.tensor([ms, wall_ms], dtype=torch.float64, device=f"cuda:{dev}")
-    tot = torch.tensor([float(moved)], dtype=torch.float64, device=f"cuda:{dev}")
+    timed_pool.profile(False)
+    st = timed_pool.stats()
+    launches = sum(pl.stats()["kernel_launches"] + pl.stats()["aux_launches"]
+                   for pl in (P, D) if pl is not None)
+    # whole job: time = max over ranks, blocks and launches = sum over ranks
+    rdev = f"cuda:{dev}" if args.dist_backend == "nccl" else "cpu"
+    tms = torch.tensor([ms, wall_ms], dtype=torch.float64, device=rdev)
+    tot = torch.tensor([float(moved), float(launches), float(io[0]), float(io[1])],
+                       dtype=torch.float64, device=rdev)
     if dist is not None:
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     ms, wall_ms = float(tms[0]), float(tms[1])
-    blocks_all = float(tot[0])
+    blocks_all, launches_all = float(tot[0]), int(tot[1])
     gbs = blocks_all * Pb / (ms * 1e-3) / 1e9
     blocks_s = blocks_all / (ms * 1e-3)
     e2e_gbs = blocks_all * Pb / (wall_ms * 1e-3) / 1e9
 
     peak, peak_src = load_peaks()
-    kernel_ms = sd["kernel_ms"] / max(sd["timed_launches"], 1)
-    bytes_per_launch = 2.0 * sd["timed_bytes"] / max(sd["timed_launches"], 1)  # read + write
-    achieved = bytes_per_launch / (kernel_ms * 1e-3) / 1e9 if kernel_ms > 0 else None
+    kernel_ms = st["kernel_ms"] / max(st["timed_launches"], 1)
+    payload_per_launch = st["timed_bytes"] / max(st["timed_launches"], 1)
+    if role.kind == "PD":
+        # loopback: the kernel reads Pb and writes Pb of HBM per block
+        alg = 2.0 * payload_per_launch
+        roof = {"kernel": "migrate_kernel<pool,pool> (fused gather->store, A6f), loopback",
+                "bound": "hbm", "peak": peak, "peak_source": peak_src}
+    else:
+        # across GPUs the bound is the NVLink direction P -> D: Pb per block
+        alg = payload_per_launch
+        roof = {"kernel": "migrate_kernel<pool,pool> (fused gather->peer store over NVLink)",
+                "bound": "nvlink", "peak": NVLINK_MEASURED_GBS,
+                "peak_source": "B200_PROFILING.md measured peer copy per direction "
+                               f"(nominal {NVLINK_GBS} GB/s)"}
+    achieved = alg / (kernel_ms * 1e-3) / 1e9 if kernel_ms > 0 else None
+    roof.update({
+        "achieved": round(achieved, 1) if achieved else None, "unit": "GB/s",
+        "frac": round(achieved / roof["peak"], 4) if achieved else None,
+        "traffic": None, "bytes_per_launch_algorithmic": alg,
+        "avg_launch_ms": round(kernel_ms, 5), "launches": int(st["timed_launches"]),
+        "share_of_step": round(st["kernel_ms"] / ms, 4) if ms > 0 else None})
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = side_measurements(M, torch, P, D, shape, seed, peak, args)
-    result = None
-    if rank == 0:
-        result = {
-            "metric": "KV migration GB/s (P->D transfer_with_insert payload)",
-            "value": round(gbs, 2),
-            "unit": "GB/s",
-            "blocks_per_s": round(blocks_s, 1),
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(ms / args.steps, 4),
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "u16 (fp16 KV copied as opaque 16-bit words)",
-            "data": "synthetic (seeded ShareGPT-like token traces; counter-based KV fill)",
-            "config": {
-                "workload": "configs[1]: Llama-2-7B-shaped KV (L32 H32 D128 fp16 B16, "
-                            "Pb=8 MiB) ShareGPT-like 1P1D, PD-Caching-2 P->D with DEDUP",
-                "placement": ("P and D as two pools on one GPU (loopback wire)" if world == 1
-                              else f"{world} independent loopback P/D pairs, one per GPU"),
-                "pool_blocks_per_instance": n_blocks,
-                "batch_blocks": args.batch_blocks,
-                "blocks_moved_total": int(blocks_all),
-                "l2": "inputs larger than L2 (each step moves GiBs of distinct blocks)",
-            },
-            "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s",
-                    "what": "host wall clock around the public Python API calls",
-                    "h2d_bytes_per_step": int(io[0] / args.steps),
-                    "d2h_bytes_per_step": int(io[1] / args.steps)},
-            "gpu_launches": int(sd["kernel_launches"] + sd["aux_launches"] +
-                                sp["kernel_launches"] + sp["aux_launches"]),
-            "roofline": {
-                "kernel": "migrate_kernel<pool,pool> (fused gather->store, A6f)",
-                "bound": "hbm",
-                "achieved": round(achieved, 1) if achieved else None,
-                "peak": peak,
-                "peak_source": peak_src,
-                "unit": "GB/s",
-                "frac": round(achieved / peak, 4) if achieved else None,
-                "traffic": None,
-                "bytes_per_launch_algorithmic": bytes_per_launch,
-                "avg_launch_ms": round(kernel_ms, 5),
-                "launches": int(sd["timed_launches"]),
-                "share_of_step": round(sd["kernel_ms"] / ms, 4) if ms > 0 else None,
-            },
-            "clocks": clocks.summary(),
-        }
-        result.update(extras)
+        extras = side_measurements(M, torch, shape, seed, peak, args)
+    if rank != 0:
+        return None
+    placement = ("P and D as two pools on one GPU (loopback wire)" if world == 1 else
+                 f"{world // 2}P{world // 2}D: P_i on GPU i, D_i on GPU i+{world // 2}, "
+                 "one process per GPU, one-sided NVLink stores into IPC-mapped peer pools")
+    result = {
+        "metric": METRIC,
+        "value": round(gbs, 2),
+        "unit": "GB/s",
+        "blocks_per_s": round(blocks_s, 1),
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": DTYPE,
+        "data": "synthetic (seeded ShareGPT-like token traces; counter-based KV fill)",
+        "config": {
+            "workload": "configs[1]: Llama-2-7B-shaped KV (L32 H32 D128 fp16 B16, "
+                        "Pb=8 MiB) ShareGPT-like 1P1D per pair, PD-Caching-2 P->D with DEDUP",
+            "placement": placement,
+            "pool_blocks_per_instance": n_blocks,
+            "batch_blocks": args.batch_blocks,
+            "copy_kernel": ["auto(vector)", "vector", "bulk"][args.copy_kernel],
+            "blocks_moved_total": int(blocks_all),
+            "l2": "inputs larger than L2 (each step moves GiBs of distinct blocks)",
+        },
+        "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s",
+                "what": "host wall clock around the public Python API calls (inputs: token "
+                        "lists and block addrs from host memory; results: addrs back)",
+                "h2d_bytes_per_step": int(float(tot[2]) / args.steps),
+                "d2h_bytes_per_step": int(float(tot[3]) / args.steps)},
+        "gpu_launches": launches_all,
+        "roofline": roof,
+        "clocks": clocks.summary(),
+    }
+    result.update(extras)
     return result
 
 
-def side_measurements(M, torch, P, D, shape, seed, peak, args):
-    """Standalone pack / unpack (A4/A6, HBM roofline) and swap (A8/A9)."""
+def side_measurements(M, torch, shape, seed, peak, args):
+    """Standalone pack / unpack (A4/A6, HBM roofline) per copy engine, and swap (A8/A9)."""
     out = {}
     Pb = shape.block_bytes
     n = 128   # 2048-token prompt (P:863) = 1 GiB at 7B: 8x the 126 MB L2
     dev = torch.cuda.current_device()
-    del P, D
     for ck, ck_name in ((1, "vector"), (2, "bulk")):
         X = make_pool(M, torch, 200 + ck, dev, shape, 2 * n + 8, copy_kernel=ck)
         a = X.alloc_mem(n)
@@ -311,38 +378,33 @@ def side_measurements(M, torch, P, D, shape, seed, peak, args):
                 "avg_kernel_ms": round(kms, 4)}
         X.close()
         del stg, X
-    # swap sweep point: a separate small pool with pinned DRAM
     if not args.no_swap:
         try:
-            out["swap"] = swap_point(M, torch, shape, seed, args)
+            out["swap"] = swap_point(M, torch, shape, seed)
         except Exception as e:  # report, never hide
             out["swap"] = {"error": str(e)}
     return out
 
 
-def swap_point(M, torch, shape, seed, args):
+def swap_point(M, torch, shape, seed):
+    """HBM <-> pinned DRAM (configs[4] shape): swap_out(n) then swap_in of the moved."""
     B, Pb = shape.block_tokens, shape.block_bytes
     nblk = 512
     dev = torch.cuda.current_device()
     S = make_pool(M, torch, 100, dev, shape, nblk, dram_blocks=nblk)
     rng = np.random.default_rng(seed)
-    seqs = []
     for i in range(8):
         t = rng.integers(3, 32000, size=48 * B, dtype=np.int32)
         a = S.alloc_mem(48)
         S.debug_fill(a, seed)
         S.insert(t, a)
-        seqs.append(t)
     res = {}
     for n in (64, 256):
-        S.stats_reset()
-        S.profile(True)
         t0 = time.perf_counter()
         old, new = S.swap_out(n)
         t1 = time.perf_counter()
         back = S.swap_in(new)
         t2 = time.perf_counter()
-        S.profile(False)
         res[f"n{n}"] = {"swap_out_GBps": round(len(old) * Pb / (t1 - t0) / 1e9, 2),
                         "swap_in_GBps": round(len(back) * Pb / (t2 - t1) / 1e9, 2),
                         "path": "zero-copy SM loads/stores to mapped pinned DRAM"}
@@ -351,56 +413,93 @@ def swap_point(M, torch, shape, seed, args):
 
 
 # ------------------------------------------------------------ cpu baseline
-def run_oracle(seconds_budget, steps=1):
-    """The CPU oracle as it stands (materialised numpy byte path), same
-    workload shape, on a bounded sample: a 7B-shaped pool of 160 blocks per
-    instance and as many whole requests as fit the time budget."""
-    import oracle as O
-    try:
-        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
-        cores = 1
-    except Exception:
-        cores = os.cpu_count()
-    shape = LLAMA2_7B
-    B, Pb = shape.block_tokens, shape.block_bytes
-    nb = 160
-    seed = seed_for(1)
-    mk = lambda inst: O.OraclePool(inst, shape.layers, shape.kv_heads, shape.head_dim, B, nb,
-                                   seed=seed, materialize=True)
-    P, D = mk(0), mk(1)
-    reqs = build_requests(shape, seed, nb, int(nb * 0.8))
-    srcs = []
-    for sid, prompt in reqs:
-        mt, matched = P.match(prompt)
-        new = P.alloc_mem(-(-len(prompt) // B) - len(matched), O.HBM)
-        P.fill(new)
-        full = matched + new
-        P.insert(prompt, full[: len(prompt) // B])
-        srcs.append(full[len(prompt) // B:])
-    moved = 0
-    t_total = 0.0
-    n_req = 0
-    for _ in range(steps):
+class OracleArm:
+    """The CPU oracle as it stands (materialised numpy byte path) on the same
+    workload shape, bounded: a 7B-shaped pool of 160 blocks per instance
+    (1.25 GiB each) and as many whole requests per step as fit a time budget."""
+
+    def __init__(self):
+        import oracle as O
+        self.O = O
+        try:
+            os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+            self.cores = 1
+        except Exception:
+            self.cores = os.cpu_count()
+        shape = LLAMA2_7B
+        self.B, self.Pb = shape.block_tokens, shape.block_bytes
+        self.nb = 160
+        seed = seed_for(1)
+        mk = lambda inst: O.OraclePool(inst, shape.layers, shape.kv_heads, shape.head_dim,
+                                       self.B, self.nb, seed=seed, materialize=True)
+        self.P, self.D = mk(0), mk(1)
+        self.reqs = build_requests(shape, seed, int(self.nb * 0.8))
+        self.srcs = []
+        for sid, prompt in self.reqs:
+            mt, matched = self.P.match(prompt)
+            new = self.P.alloc_mem(-(-len(prompt) // self.B) - len(matched), O.HBM)
+            self.P.fill(new)
+            full = matched + new
+            self.P.insert(prompt, full[: len(prompt) // self.B])
+            self.srcs.append(full[len(prompt) // self.B:])
+        self.next = 0
+
+    def step(self, budget_s):
+        O, B = self.O, self.B
         t0 = time.perf_counter()
-        done = []
-        for (sid, prompt), partial in zip(reqs, srcs):
-            _, matched = P.match(prompt)
-            final, nm, _ = O.transfer_with_insert(P, D, prompt, matched + partial,
+        done, moved, n_req = [], 0, 0
+        while time.perf_counter() - t0 < budget_s and n_req < len(self.reqs):
+            (sid, prompt), partial = self.reqs[self.next], self.srcs[self.next]
+            self.next = (self.next + 1) % len(self.reqs)
+            _, matched = self.P.match(prompt)
+            final, nm, _ = O.transfer_with_insert(self.P, self.D, prompt, matched + partial,
                                                   flags=O.FLAG_DEDUP)
             moved += nm
             n_req += 1
             done.append((prompt, final[len(prompt) // B:]))
-            if time.perf_counter() - t0 > seconds_budget:
-                break
         for prompt, part in done:
-            D.free_mem(part)
-            D.delete(prompt)
-        t_total += time.perf_counter() - t0
-    return {"value": round(moved * Pb / t_total / 1e9, 4), "unit": "GB/s", "cores": cores,
-            "kind": "oracle",
-            "sample": f"{n_req} ShareGPT-like requests x {steps} step(s), 7B shape, "
-                      f"{nb}-block pools, DEDUP P->D transfer_with_insert, numpy byte path",
-            "blocks_moved": moved, "seconds": round(t_total, 3)}
+            self.D.free_mem(part)
+            self.D.delete(prompt)
+        return moved, n_req, time.perf_counter() - t0
+
+    def sample(self, n_req, steps):
+        return (f"{n_req} ShareGPT-like requests over {steps} step(s), 7B shape, "
+                f"{self.nb}-block pools, DEDUP P->D transfer_with_insert, numpy byte path")
+
+
+def cpu_baseline(seconds):
+    arm = OracleArm()
+    moved, n_req, t = arm.step(seconds)
+    return {"value": round(moved * arm.Pb / t / 1e9, 4), "unit": "GB/s", "cores": arm.cores,
+            "kind": "oracle", "sample": arm.sample(n_req, 1)}
+
+
+def run_reference(args, world):
+    """--impl reference: the CPU oracle is this tier's reference arm."""
+    arm = OracleArm()
+    per_step = max(0.2, min(5.0, args.cpu_seconds / max(args.steps, 1)))
+    for _ in range(args.warmup):
+        arm.step(min(per_step, 1.0))
+    moved = n_req = 0
+    secs = 0.0
+    for _ in range(args.steps):
+        m, r, t = arm.step(per_step)
+        moved, n_req, secs = moved + m, n_req + r, secs + t
+    val = moved * arm.Pb / secs / 1e9
+    print(json.dumps({
+        "impl": "reference",
+        "metric": METRIC, "value": round(val, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs * 1e3 / max(args.steps, 1), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DTYPE, "data": "synthetic",
+        "config": {"workload": "configs[1]: Llama-2-7B-shaped KV ShareGPT-like 1P1D "
+                               "(bounded sample per step, CPU oracle)"},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": arm.cores,
+                         "kind": "oracle", "sample": arm.sample(n_req, args.steps)},
+        "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
 
 
 def main():
@@ -417,56 +516,32 @@ def main():
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    # testing the multi-process path on a 1-GPU box: every rank on --device,
+    # gloo for the bootstrap / reductions (NCCL refuses two ranks on one GPU)
+    ap.add_argument("--device", type=int, default=-1, help=argparse.SUPPRESS)
+    ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
 
     if args.impl == "reference":
-        # The reference arm is the CPU oracle (no upstream code exists); rank 0 only.
-        if rank != 0:
-            return
-        steps = []
-        r = None
-        for _ in range(args.warmup):
-            run_oracle(min(2.0, args.cpu_seconds))
-        for _ in range(args.steps):
-            r = run_oracle(max(1.0, args.cpu_seconds / max(args.steps, 1)))
-            steps.append(r)
-        tot_b = sum(x["blocks_moved"] for x in steps)
-        tot_s = sum(x["seconds"] for x in steps)
-        val = tot_b * LLAMA2_7B.block_bytes / tot_s / 1e9
-        print(json.dumps({
-            "impl": "reference",
-            "metric": "KV migration GB/s (P->D transfer_with_insert payload)",
-            "value": round(val, 4), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(tot_s * 1e3 / max(args.steps, 1), 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u16 (fp16 KV copied as opaque 16-bit words)", "data": "synthetic",
-            "config": {"workload": "configs[1]: Llama-2-7B-shaped KV ShareGPT-like 1P1D "
-                                   "(bounded sample per step, CPU oracle)"},
-            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": r["cores"],
-                             "kind": "oracle", "sample": r["sample"]},
-            "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-        }))
+        if rank == 0:        # rank 0 alone runs it; the other ranks exit 0
+            run_reference(args, world)
         return
 
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist_mod
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist_mod.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) if args.device < 0
+                              else args.device)
+        dist_mod.init_process_group(args.dist_backend)
         dist = dist_mod
     res = run_ours(args, rank, world, dist)
     if rank == 0:
         if not args.no_cpu_baseline:
-            cb = run_oracle(args.cpu_seconds)
-            cb.pop("blocks_moved", None)
-            cb.pop("seconds", None)
-            res["cpu_baseline"] = cb
+            res["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
         print(json.dumps(res))
     if dist is not None:
         dist.barrier()

@@ -230,6 +230,40 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_instance, const mp_t
 mp_status mp_recv_poll(mp_pool* dst, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,
                        mp_addr* addrs, int64_t addr_cap);
 
+/* ------------------- multi-process (one process per GPU) ----------------- */
+/* Serialize what a pool in ANOTHER process needs to reach this one: CUDA-IPC
+ * handles of the slab allocations (slabs must come from cudaMalloc, e.g. the
+ * torch caching allocator) and of the id arena, an interprocess event, the
+ * shape and a random pool uid (mailbox names).  len receives the size; call
+ * with buf = NULL to query it.  The blob is plain bytes (exchange it with
+ * torch.distributed / any transport). */
+mp_status mp_export_handle(mp_pool* pool, void* buf, int64_t cap, int64_t* len);
+/* Map a peer's exported pool: its slabs and arena are opened with
+ * cudaIpcOpenMemHandle (peer access over NVLink when on another GPU), its
+ * event with cudaIpcOpenEventHandle, and the two shared-memory mailboxes of
+ * the pair are created / opened.  Both sides import each other.  Afterwards
+ * mp_transfer / mp_transfer_with_insert accept the peer's instance id as
+ * dst_instance: the caller's process sends the request, the peer's process
+ * executes the receiver's half of the workflow (allocation, insertion;
+ * P:361-365) inside mp_serve -- or inside any of its own blocking transfer
+ * calls -- and the caller's fused kernel stores the blocks one-sided into
+ * the peer's IPC-mapped slabs (FUSED path only).  Shapes must match. */
+mp_status mp_import_peer(mp_pool* pool, const void* buf, int64_t len);
+/* Receiver loop: serve requests of imported peers until an end-of-batch
+ * mark arrives (until_mark != 0) or timeout_ms elapses (< 0: no timeout;
+ * 0 with until_mark == 0: one non-blocking pass).  served (nullable): requests
+ * served; mark (nullable): the mark's tag, or -1 if none arrived. */
+mp_status mp_serve(mp_pool* pool, int64_t timeout_ms, int32_t until_mark, int64_t* served,
+                   int32_t* mark);
+/* Send an end-of-batch mark (tag) to an imported peer; returns once the
+ * peer's mp_serve has taken it. */
+mp_status mp_send_mark(mp_pool* src, int32_t dst_instance, int32_t tag);
+/* Test hook, no GPU needed: two processes exchange n_msgs messages of up to
+ * payload bytes through one shared-memory mailbox `name` (role 0 sends and
+ * verifies the echo, role 1 echoes). */
+mp_status mp_debug_channel_selftest(const char* name, int32_t role, int64_t n_msgs,
+                                    int64_t payload);
+
 /* ---------------- building blocks (A4 pack / A6 unpack) ------------------ */
 /* Gather layers [l0, l1) of n HBM blocks into device buffer `staging`
  * (aggregated layout [n][l1-l0][2][c]); unpack is the inverse scatter into

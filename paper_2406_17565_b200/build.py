@@ -16,7 +16,8 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libmempool.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["pool.cpp", "api_memory_index.cpp", "api_transfer.cpp", "api_swap.cpp", "kernels.cu"]
+SOURCES = ["pool.cpp", "api_memory_index.cpp", "api_transfer.cpp", "api_swap.cpp",
+           "remote.cpp", "kernels.cu"]
 HEADERS = ["kernels.cuh", "index.hpp", "pool.hpp"]
 
 NVCC_FLAGS = [
@@ -24,7 +25,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-Wall,-Wno-unused-function",
     "-Xptxas", "-v",
-    "-shared",
+    "-shared", "-lrt",
 ]
 
 

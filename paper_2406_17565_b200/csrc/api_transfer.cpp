@@ -10,6 +10,9 @@
 //          contiguous copy per slot, unpack; a ring of slots overlaps the three;
 //   CE     one copy-engine memcpy per (block, layer, K/V) chunk: the paper's
 //          discrete per-block transfer, kept as a library baseline.
+// The receiver's half (allocation, insertion) is dst_prepare_* / dst_commit,
+// called directly for an in-process peer and from the mailbox server
+// (remote.cpp) for a peer in another process.
 // Readings R3, R4, R12, R13.
 #include <algorithm>
 #include <cstring>
@@ -63,11 +66,16 @@ mp_pool* peer_of(mp_pool* src, int32_t inst) {
   return it == src->peers.end() ? nullptr : it->second;
 }
 
-// The transmission step.  Copies chunks [j0, j0+nj) of source blocks `sids`
-// into destination blocks `dids`; d_dst is the destination allocator's device
-// table of the same ids (on dst's device) or nullptr.  Enqueued after all
-// earlier work of both pools and before their later work; STAGED completes
-// before returning, the others are stream-ordered.
+RemotePeer* remote_of(mp_pool* src, int32_t inst) {
+  auto it = src->remotes.find(inst);
+  return it == src->remotes.end() ? nullptr : it->second;
+}
+
+// The transmission step (in-process peers).  Copies chunks [j0, j0+nj) of
+// source blocks `sids` into destination blocks `dids`; d_dst is the
+// destination allocator's device table of the same ids (on dst's device) or
+// nullptr.  Enqueued after all earlier work of both pools and before their
+// later work; STAGED completes before returning, the others are stream-ordered.
 mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
                    const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj,
                    uint32_t path) {
@@ -191,7 +199,110 @@ mp_status finish(mp_pool* src, mp_pool* dst, uint32_t flags) {
   return sync(src);
 }
 
+void stash_priv(DstPrep* st, const void* priv, int64_t priv_len) {
+  st->priv.clear();
+  if (priv_len > 0) st->priv.assign((const uint8_t*)priv, (const uint8_t*)priv + priv_len);
+}
+
 }  // namespace
+
+// ------------------------------------------------- receiver: allocation step
+mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t flags,
+                           const mp_addr* given, const void* priv, int64_t priv_len,
+                           DstPrep* st) {
+  *st = DstPrep{};
+  st->kind = 0;
+  st->src_inst = src_inst;
+  st->flags = flags;
+  st->nm = n;
+  const bool dst_given = (flags & MP_XFER_DST_GIVEN) != 0;
+  if (dst_given) TRY(validate_dst_given(dst, given, n, &st->dids));
+  const std::vector<mpi::Node*> none;
+  if (!dst_given && !can_make_room(dst, n, MP_HBM, none)) return MP_ERR_DST_OOM;
+  stash_priv(st, priv, priv_len);
+  if (!dst_given) {
+    DevGuard g(dst->dev);
+    if (dst->nfree[MP_HBM] < n) evict_internal(dst, n - dst->nfree[MP_HBM], MP_HBM, nullptr);
+    TRY(alloc_hbm(dst, n, src_inst, &st->dids, &st->d_dst));
+    if (st->d_dst) st->d_dst_off = st->d_dst - dst->ar.d;
+  }
+  return MP_OK;
+}
+
+mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, int64_t n_tok,
+                          int64_t m, uint32_t flags, const mp_addr* given, const void* priv,
+                          int64_t priv_len, DstPrep* st) {
+  *st = DstPrep{};
+  st->kind = 1;
+  st->src_inst = src_inst;
+  st->flags = flags;
+  const bool dst_given = (flags & MP_XFER_DST_GIVEN) != 0;
+  const bool dedup = (flags & MP_XFER_DEDUP) != 0;
+  const int64_t B = dst->B;
+  st->n_tok = n_tok;
+  st->ceil_b = (n_tok + B - 1) / B;
+  st->floor_b = n_tok / B;
+  std::vector<int32_t> given_ids;
+  if (dst_given) TRY(validate_dst_given(dst, given, m, &given_ids));
+  st->q = st->ceil_b - m;
+  const bool need_match = dedup || st->q > 0;
+  std::vector<mpi::Node*> peek;
+  if (need_match) peek = dst->index->path(toks, st->floor_b);
+  const int64_t k_match = (int64_t)peek.size();
+  if (k_match < st->q) return MP_ERR_PREFIX_MISSING;
+  st->skip = dedup ? k_match - st->q : 0;
+  st->nm = m - st->skip;
+  if (flags & MP_INS_ERR_ON_CONFLICT) {
+    const int64_t k_exist = need_match ? k_match : dst->index->peek(toks, n_tok);
+    if (k_exist > st->q + st->skip) return MP_ERR_CONFLICT;
+  }
+  if (!dst_given && !can_make_room(dst, st->nm, MP_HBM, peek)) return MP_ERR_DST_OOM;
+  // ---- mutations start here ----
+  st->toks.assign(toks, toks + n_tok);
+  stash_priv(st, priv, priv_len);
+  // receiver-side match, pinned while the receiver allocates (R3, R12)
+  if (need_match) st->matched = dst->index->match(toks, n_tok, /*pin=*/true);
+  if (dst_given) {
+    st->dids = given_ids;
+  } else {
+    DevGuard g(dst->dev);
+    if (dst->nfree[MP_HBM] < st->nm)
+      evict_internal(dst, st->nm - dst->nfree[MP_HBM], MP_HBM, nullptr);
+    TRY(alloc_hbm(dst, st->nm, src_inst, &st->dids, &st->d_dst));
+    if (st->d_dst) st->d_dst_off = st->d_dst - dst->ar.d;
+  }
+  return MP_OK;
+}
+
+// ------------------------------------------------- receiver: insertion step
+mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out) {
+  Msg msg{st.kind, st.src_inst, {}, {}};
+  msg.priv.swap(st.priv);
+  if (st.kind == 0) {
+    for (int64_t i = 0; i < st.nm; ++i) final_out[i] = enc(dst, MP_HBM, st.dids[(size_t)i]);
+    msg.addrs.assign(final_out, final_out + st.nm);
+    dst->inbox.push_back(std::move(msg));
+    return MP_OK;
+  }
+  std::vector<mp_addr> full;
+  full.reserve((size_t)st.ceil_b);
+  for (int64_t i = 0; i < st.q + st.skip; ++i)
+    full.push_back(enc(dst, st.matched[(size_t)i]->medium, st.matched[(size_t)i]->idx));
+  for (int64_t i = 0; i < st.nm; ++i) full.push_back(enc(dst, MP_HBM, st.dids[(size_t)i]));
+  int64_t dup = 0;
+  TRY(insert_internal(dst, st.toks.data(), st.n_tok, full.data(), (int64_t)full.size(),
+                      st.flags & MP_INS_ERR_ON_CONFLICT, &dup));
+  unpin_nodes(dst, st.matched);
+  st.matched.clear();
+  std::vector<mpi::Node*> fin = dst->index->path(st.toks.data(), st.floor_b);
+  for (int64_t i = 0; i < st.floor_b; ++i)
+    final_out[i] = enc(dst, fin[(size_t)i]->medium, fin[(size_t)i]->idx);
+  if (st.ceil_b > st.floor_b) final_out[st.floor_b] = full[(size_t)st.floor_b];
+  msg.addrs.assign(final_out, final_out + st.ceil_b);
+  dst->inbox.push_back(std::move(msg));
+  return MP_OK;
+}
+
 }  // namespace mp
 
 using namespace mp;
@@ -203,32 +314,24 @@ mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t
   if (!src || n < 0 || (n > 0 && (!sa || !da)) || priv_len < 0 || (priv_len > 0 && !priv))
     return MP_ERR_CONFIG;
   mp_pool* dst = peer_of(src, dst_inst);
-  if (!dst) return MP_ERR_DST_UNREACHABLE;
-  TRY(check_compatible(src, dst));
+  RemotePeer* rp = dst ? nullptr : remote_of(src, dst_inst);
+  if (!dst && !rp) return MP_ERR_DST_UNREACHABLE;
+  if (dst) TRY(check_compatible(src, dst));
   if (!(0 <= l0 && l0 < l1 && l1 <= src->L) || (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
-  std::vector<int32_t> sids, dids;
+  std::vector<int32_t> sids;
   TRY(validate_src(src, sa, n, &sids));
-  const bool dst_given = (flags & MP_XFER_DST_GIVEN) != 0;
-  if (dst_given) TRY(validate_dst_given(dst, da, n, &dids));
-  const std::vector<mpi::Node*> none;
-  if (!dst_given && !can_make_room(dst, n, MP_HBM, none)) return MP_ERR_DST_OOM;
+  if (rp)
+    return remote_transfer(src, rp, 0, nullptr, 0, sids, sa, n, da, flags, l0, l1, priv,
+                           priv_len, nullptr);
   // ---- (1) allocation at the receiver ----
-  int* d_dst = nullptr;
-  if (!dst_given) {
-    DevGuard g(dst->dev);
-    if (dst->nfree[MP_HBM] < n) evict_internal(dst, n - dst->nfree[MP_HBM], MP_HBM, nullptr);
-    TRY(alloc_hbm(dst, n, src->inst, &dids, &d_dst));
-  }
+  DstPrep st;
+  TRY(dst_prepare_xfer(dst, src->inst, n, flags, da, priv, priv_len, &st));
   // ---- (2) transmission ----
-  TRY(transmit(src, dst, sids, dids, d_dst, 2 * l0, 2 * (l1 - l0), flags & MP_XFER_PATH_MASK));
-  TRY(finish(src, dst, flags));
-  if (!dst_given)
-    for (int64_t i = 0; i < n; ++i) da[i] = enc(dst, MP_HBM, dids[(size_t)i]);
-  Msg msg{0, src->inst, {}, {}};
-  if (priv_len) msg.priv.assign((const uint8_t*)priv, (const uint8_t*)priv + priv_len);
-  msg.addrs.assign(da, da + n);
-  dst->inbox.push_back(std::move(msg));
-  return MP_OK;
+  TRY(transmit(src, dst, sids, st.dids, st.d_dst, 2 * l0, 2 * (l1 - l0),
+               flags & MP_XFER_PATH_MASK));
+  // ---- (3) completion ----
+  TRY(dst_commit(dst, st, da));
+  return finish(src, dst, flags);
 }
 
 mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token* toks,
@@ -239,68 +342,27 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
       priv_len < 0 || (priv_len > 0 && !priv))
     return MP_ERR_CONFIG;
   mp_pool* dst = peer_of(src, dst_inst);
-  if (!dst) return MP_ERR_DST_UNREACHABLE;
-  TRY(check_compatible(src, dst));
-  const bool dst_given = (flags & MP_XFER_DST_GIVEN) != 0;
-  const bool dedup = (flags & MP_XFER_DEDUP) != 0;
-  if (dst_given && dedup) return MP_ERR_CONFIG;
-  const int64_t B = dst->B, ceil_b = (n_tok + B - 1) / B, floor_b = n_tok / B;
+  RemotePeer* rp = dst ? nullptr : remote_of(src, dst_inst);
+  if (!dst && !rp) return MP_ERR_DST_UNREACHABLE;
+  if (dst) TRY(check_compatible(src, dst));
+  if ((flags & MP_XFER_DST_GIVEN) && (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
+  const int64_t B = src->B, ceil_b = (n_tok + B - 1) / B;
   if (m > ceil_b) return MP_ERR_ADDR_COUNT;
-  std::vector<int32_t> sids, given;
+  std::vector<int32_t> sids;
   TRY(validate_src(src, sa, m, &sids));
-  if (dst_given) TRY(validate_dst_given(dst, da, m, &given));
-  const int64_t q = ceil_b - m;
-  const bool need_match = dedup || q > 0;
-  std::vector<mpi::Node*> peek;
-  if (need_match) peek = dst->index->path(toks, floor_b);
-  const int64_t k_match = (int64_t)peek.size();
-  if (k_match < q) return MP_ERR_PREFIX_MISSING;
-  const int64_t skip = dedup ? k_match - q : 0;
-  const int64_t nm = m - skip;
-  if (flags & MP_INS_ERR_ON_CONFLICT) {
-    const int64_t k_exist = need_match ? k_match : dst->index->peek(toks, n_tok);
-    if (k_exist > q + skip) return MP_ERR_CONFLICT;
-  }
-  if (!dst_given && !can_make_room(dst, nm, MP_HBM, peek)) return MP_ERR_DST_OOM;
-  // ---- mutations start here ----
-  // receiver-side match, pinned while the receiver allocates (R3, R12)
-  std::vector<mpi::Node*> matched;
-  if (need_match) matched = dst->index->match(toks, n_tok, /*pin=*/true);
-  // ---- (1) allocation at the receiver ----
-  std::vector<int32_t> dids;
-  int* d_dst = nullptr;
-  if (dst_given) {
-    dids = given;
-  } else {
-    DevGuard g(dst->dev);
-    if (dst->nfree[MP_HBM] < nm) evict_internal(dst, nm - dst->nfree[MP_HBM], MP_HBM, nullptr);
-    TRY(alloc_hbm(dst, nm, src->inst, &dids, &d_dst));
-  }
+  if (rp)
+    return remote_transfer(src, rp, 1, toks, n_tok, sids, sa, m, da, flags, 0, src->L, priv,
+                           priv_len, n_moved);
+  // ---- (1) allocation at the receiver, with its DEDUP match ----
+  DstPrep st;
+  TRY(dst_prepare_twi(dst, src->inst, toks, n_tok, m, flags, da, priv, priv_len, &st));
   // ---- (2) transmission of all layers ----
-  std::vector<int32_t> moved_src(sids.begin() + skip, sids.end());
-  TRY(transmit(src, dst, moved_src, dids, d_dst, 0, src->nch, flags & MP_XFER_PATH_MASK));
-  // ---- (3) insertion at the receiver ----
-  std::vector<mp_addr> full;
-  full.reserve((size_t)ceil_b);
-  for (int64_t i = 0; i < q + skip; ++i)
-    full.push_back(enc(dst, matched[(size_t)i]->medium, matched[(size_t)i]->idx));
-  for (int64_t i = 0; i < nm; ++i) full.push_back(enc(dst, MP_HBM, dids[(size_t)i]));
-  int64_t dup = 0;
-  TRY(insert_internal(dst, toks, n_tok, full.data(), (int64_t)full.size(),
-                      flags & MP_INS_ERR_ON_CONFLICT, &dup));
-  unpin_nodes(dst, matched);
-  TRY(finish(src, dst, flags));
-  // ---- ok: the receiver's final address of every block ----
-  std::vector<mpi::Node*> fin = dst->index->path(toks, floor_b);
-  for (int64_t i = 0; i < floor_b; ++i)
-    da[i] = enc(dst, fin[(size_t)i]->medium, fin[(size_t)i]->idx);
-  if (ceil_b > floor_b) da[floor_b] = full[(size_t)floor_b];
-  if (n_moved) *n_moved = nm;
-  Msg msg{1, src->inst, {}, {}};
-  if (priv_len) msg.priv.assign((const uint8_t*)priv, (const uint8_t*)priv + priv_len);
-  msg.addrs.assign(da, da + ceil_b);
-  dst->inbox.push_back(std::move(msg));
-  return MP_OK;
+  std::vector<int32_t> moved_src(sids.begin() + st.skip, sids.end());
+  TRY(transmit(src, dst, moved_src, st.dids, st.d_dst, 0, src->nch, flags & MP_XFER_PATH_MASK));
+  // ---- (3) insertion at the receiver, ok ----
+  TRY(dst_commit(dst, st, da));
+  if (n_moved) *n_moved = st.nm;
+  return finish(src, dst, flags);
 }
 
 mp_status mp_recv_poll(mp_pool* p, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,

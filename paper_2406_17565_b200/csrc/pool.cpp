@@ -262,6 +262,7 @@ const char* mp_last_error(void) { return get_err().c_str(); }
 
 void mp_pool_destroy(mp_pool* p) {
   if (!p) return;
+  remote_close_all(p);
   {
     DevGuard g(p->dev);
     if (p->meta) cudaStreamSynchronize(p->meta);
@@ -289,6 +290,7 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->staging) cudaFree(p->staging);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
     if (p->ev_meta) cudaEventDestroy(p->ev_meta);
+    if (p->ev_ipc) cudaEventDestroy(p->ev_ipc);
     for (auto e : p->slot_ev) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -372,6 +374,8 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   CKC(cudaStreamCreateWithFlags(&p->meta, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_meta, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&p->ev_ipc, cudaEventDisableTiming | cudaEventInterprocess));
+  p->uid = new_uid();
   p->slot_ev.resize((size_t)p->staging_slots);
   for (auto& e : p->slot_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   p->tev.resize(2 * (size_t)kTimedPairs);

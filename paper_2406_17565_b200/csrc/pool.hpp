@@ -87,6 +87,41 @@ struct PendingVerify {
   std::vector<int32_t> want;
 };
 
+// Receiver-side state of one transfer between its allocation step and its
+// insertion step.  Built by dst_prepare_*, consumed by dst_commit.
+struct DstPrep {
+  int kind = 0;  // 0 transfer, 1 transfer_with_insert
+  int32_t src_inst = -1;
+  uint32_t flags = 0;
+  std::vector<int32_t> toks;
+  int64_t n_tok = 0, ceil_b = 0, floor_b = 0, q = 0, skip = 0, nm = 0;
+  std::vector<mpi::Node*> matched;  // pinned receiver prefix (R3, R12)
+  std::vector<int32_t> dids;        // receiver block ids of the moved blocks
+  int* d_dst = nullptr;             // allocator output on the receiver's device
+  int64_t d_dst_off = -1;           // its offset in the receiver's id arena
+  std::vector<uint8_t> priv;
+};
+
+struct Channel;  // shared-memory mailbox (remote.cpp)
+
+// A pool living in another process (one process per GPU), imported with
+// mp_import_peer: its slabs and id arena are CUDA-IPC mapped into this
+// process, its interprocess event orders the two processes' streams, and two
+// mailboxes carry the control messages of the workflow.
+struct RemotePeer {
+  int32_t inst = -1, dev = -1;
+  uint64_t uid = 0;
+  bool same_device = false;
+  std::vector<void*> mapped;      // IPC-opened allocation bases
+  char** d_slabs = nullptr;       // the peer's slab pointers, valid on my device
+  int* arena = nullptr;           // the peer's id arena (device), mapped
+  cudaEvent_t ev = nullptr;       // the peer's interprocess event
+  Channel* out = nullptr;         // me -> peer requests
+  Channel* in = nullptr;          // peer -> me requests
+  bool has_pending = false;       // peer's transfer between prepare and commit
+  DstPrep pending;
+};
+
 }  // namespace mp
 
 struct mp_pool {
@@ -140,6 +175,11 @@ struct mp_pool {
   std::map<int32_t, mp_pool*> peers;
   std::map<int32_t, char**> peer_tables;   // peer's slab table, on this device
   std::deque<mp::Msg> inbox;
+  // multi-process
+  uint64_t uid = 0;                        // random identity (mailbox names)
+  cudaEvent_t ev_ipc = nullptr;            // interprocess event of this pool
+  std::map<int32_t, mp::RemotePeer*> remotes;
+  std::vector<int32_t> marks;              // end-of-batch marks received (mp_serve)
 };
 
 namespace mp {
@@ -176,5 +216,28 @@ inline mpk::Endpoint agg_ep(char* base, long long stride, const int* ids) {
 mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const mp_addr* addrs,
                           int64_t n_addr, uint32_t flags, int64_t* n_dup);
 void unpin_nodes(mp_pool* p, const std::vector<mpi::Node*>& nodes);
+
+// ---- the receiver's half of the workflow (shared by in-process and remote)
+// (1) allocation: validates everything first (no state change on error),
+// then matches / pins / allocates.  `given`: caller-given destination addrs
+// (MP_XFER_DST_GIVEN) or nullptr.
+mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t flags,
+                           const mp_addr* given, const void* priv, int64_t priv_len,
+                           DstPrep* st);
+mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, int64_t n_tok,
+                          int64_t m, uint32_t flags, const mp_addr* given, const void* priv,
+                          int64_t priv_len, DstPrep* st);
+// (3) insertion + completion: insert (twi), unpin, final addrs, `private`
+// delivery.  final_out: st.ceil_b entries (twi) or st.nm entries (transfer).
+mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out);
+
+// remote.cpp
+uint64_t new_uid();
+mp_status remote_serve_once(mp_pool* p, int64_t* served);
+void remote_close_all(mp_pool* p);
+mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,
+                          int64_t n_tok, const std::vector<int32_t>& sids, const mp_addr* sa,
+                          int64_t n, mp_addr* da, uint32_t flags, int32_t l0, int32_t l1,
+                          const void* priv, int64_t priv_len, int64_t* n_moved);
 
 }  // namespace mp

@@ -136,6 +136,11 @@ SIGNATURES = {
     "mp_transfer_with_insert": (_I32, [_P, _I32, _PI32, _I64, _PU64, _I64, _PU64, _U32, _P,
                                        _I64, _PI64]),
     "mp_recv_poll": (_I32, [_P, C.POINTER(RecvMsg), _P, _I64, _PU64, _I64]),
+    "mp_export_handle": (_I32, [_P, _P, _I64, _PI64]),
+    "mp_import_peer": (_I32, [_P, _P, _I64]),
+    "mp_serve": (_I32, [_P, _I64, _I32, _PI64, _PI32]),
+    "mp_send_mark": (_I32, [_P, _I32, _I32]),
+    "mp_debug_channel_selftest": (_I32, [C.c_char_p, _I32, _I64, _I64]),
     "mp_pack": (_I32, [_P, _PU64, _I64, _I32, _I32, _P]),
     "mp_unpack": (_I32, [_P, _P, _PU64, _I64, _I32, _I32]),
     "mp_profile": (_I32, [_P, _I32]),
@@ -340,6 +345,29 @@ class Pool:
                "recv_poll")
         return m.kind, m.src_instance, pb.raw[: m.priv_len], ad[: m.n_addrs]
 
+    # ------------------------------------------- multi-process (one per GPU)
+    def export_handle(self) -> bytes:
+        n = C.c_int64(0)
+        _lib.mp_export_handle(self._h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value)
+        _check(_lib.mp_export_handle(self._h, buf, n.value, C.byref(n)), "export_handle")
+        return buf.raw[: n.value]
+
+    def import_peer(self, blob: bytes):
+        b = C.create_string_buffer(bytes(blob), len(blob))
+        _check(_lib.mp_import_peer(self._h, b, len(blob)), "import_peer")
+
+    def serve(self, timeout_ms: int = -1, until_mark: bool = True):
+        """Run the receiver's half of remote transfers; returns (served, mark)."""
+        served = C.c_int64(0)
+        mark = C.c_int32(-1)
+        _check(_lib.mp_serve(self._h, timeout_ms, int(until_mark), C.byref(served),
+                             C.byref(mark)), "serve")
+        return served.value, (None if mark.value < 0 else mark.value)
+
+    def send_mark(self, dst_instance: int, tag: int):
+        _check(_lib.mp_send_mark(self._h, dst_instance, tag), "send_mark")
+
     # ----------------------------------------------------- building blocks
     def pack(self, addrs, layer_begin: int, layer_end: int, staging_ptr: int):
         a = _u64(addrs)
@@ -403,3 +431,19 @@ class Pool:
 
 def connect(a: Pool, b: Pool):
     _check(_lib.mp_connect(a.handle, b.handle), "connect")
+
+
+def channel_selftest(name: str, role: int, n_msgs: int, payload: int):
+    """Mailbox self-test (no GPU): run role 0 and role 1 in two processes."""
+    _check(_lib.mp_debug_channel_selftest(name.encode(), role, n_msgs, payload),
+           "channel_selftest")
+
+
+def exchange_handles(pool: Pool, group=None) -> dict:
+    """Bootstrap over torch.distributed: every rank exports its pool and
+    gathers everyone's blob (plumbing only; returns {rank: blob})."""
+    import torch.distributed as dist
+    blob = pool.export_handle()
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, (pool.inst, blob), group=group)
+    return {r: v for r, v in enumerate(out)}

@@ -1,0 +1,131 @@
+"""Cross-process MemPool on the GPU: P and D pools in two processes (both on
+cuda:0 here -- the only GPU a test box has; on an 8-GPU box the same code maps
+the peer's slabs over NVLink), bootstrapped with torch.distributed (gloo),
+CUDA-IPC-mapped slabs/arena, shared-memory mailbox for the allocation /
+insertion round trips.  The receiver's final state (index dump,
+block states, every byte of every written block) must equal the oracle's
+after the golden worked example (with and without DEDUP) plus plain
+transfers with `private` payloads."""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rank, port, dedup, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import TINY
+        from workloads.traces import golden_prompts
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        s = TINY
+        pool = M.Pool(rank, 0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64,
+                      verify=True)
+        blobs = M.exchange_handles(pool)
+        pool.import_peer(blobs[1 - rank][1])
+        dist.barrier()
+        out = {}
+        if rank == 0:
+            _, p1, p2, p3 = golden_prompts()
+            finals = []
+            for i, p in enumerate((p1, p2, p3)):
+                mt, matched = pool.match(p)
+                new = pool.alloc_mem(-(-len(p) // 16) - len(matched))
+                pool.debug_fill(new, 17565)
+                full = np.concatenate([matched, new])
+                pool.insert(p, full[: len(p) // 16])
+                fl = M.XFER_DEDUP if dedup else 0
+                if i == 2:
+                    fl |= M.XFER_ASYNC
+                final, moved = pool.transfer_with_insert(1, p, full, flags=fl,
+                                                         priv=bytes(p.astype(np.int32)))
+                finals.append((M.addr_indices(final).tolist(), moved))
+            extra = pool.alloc_mem(3)
+            pool.debug_fill(extra, 17565)
+            d = pool.transfer(1, extra, priv=b"plain")
+            finals.append((M.addr_indices(d).tolist(), 3))
+            pool.send_mark(1, 7)
+            out["finals"] = finals
+        else:
+            served, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+            assert mark == 7, (served, mark)
+            msgs = []
+            while True:
+                m = pool.recv_poll()
+                if m is None:
+                    break
+                msgs.append((m[0], m[1], m[2], M.addr_indices(m[3]).tolist()))
+            out["msgs"] = msgs
+        pool.sync()
+        out["dump"] = pool.dump_index()
+        out["states"] = pool.block_states().tolist()
+        out["bytes"] = {i: pool.debug_read_block(M.make_addr(rank, 0, i))
+                        for i, st in enumerate(out["states"]) if st != 0}
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:  # report to the parent
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+@pytest.mark.parametrize("dedup", [False, True])
+def test_two_process_golden(dedup):
+    import oracle as O
+    from workloads.configs import TINY
+    from workloads.traces import golden_prompts
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + (os.getpid() % 200) + int(dedup)
+    ps = [ctx.Process(target=_run, args=(r, port, dedup, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in ps:
+        r, out = q.get(timeout=300)
+        res[r] = out
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in res[r], res[r].get("error")
+    # oracle of the same sequence
+    s = TINY
+    oP = O.OraclePool(0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64, seed=17565)
+    oD = O.OraclePool(1, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64, seed=17565)
+    _, p1, p2, p3 = golden_prompts()
+    finals = []
+    for p in (p1, p2, p3):
+        _, matched = oP.match(p)
+        new = oP.alloc_mem(-(-len(p) // 16) - len(matched), O.HBM)
+        oP.fill(new)
+        full = matched + new
+        oP.insert(p, full[: len(p) // 16])
+        f, moved, _ = O.transfer_with_insert(oP, oD, p, full,
+                                             flags=O.FLAG_DEDUP if dedup else 0,
+                                             priv=bytes(p.astype(np.int32)))
+        finals.append(([a[2] for a in f], moved))
+    extra = oP.alloc_mem(3, O.HBM)
+    oP.fill(extra)
+    d = O.transfer(oP, oD, extra, priv=b"plain")
+    finals.append(([a[2] for a in d], 3))
+    assert res[0]["finals"] == finals
+    for pool_o, r in ((oP, 0), (oD, 1)):
+        assert res[r]["dump"] == pool_o.dump_index()
+        smap = {O.FREE: 0, O.ACTIVE: 1, O.INDEXED: 2, O.ORPHAN: 3}
+        assert res[r]["states"] == [smap[x] for x in pool_o.state[O.HBM]]
+        for i, got in res[r]["bytes"].items():
+            if all(t is not None for t in pool_o.tags[O.HBM][i]):
+                assert np.array_equal(got, pool_o.block_bytes((r, O.HBM, i))), (r, i)
+    # `private` delivered byte-exact at the receiver, with the final addrs
+    want_msgs = [(1 if k == "transfer_with_insert" else 0, src, priv, [a[2] for a in addrs])
+                 for (k, src, priv, addrs) in oD.inbox]
+    assert res[1]["msgs"] == want_msgs
