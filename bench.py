@@ -183,16 +183,25 @@ def run_ours(args, rank, world, dist):
         reqs, partials = populate_prefill(P, shape, seed, n_blocks)
         batches = make_batches(reqs, partials, args.batch_blocks, B)
 
+    host_t = {"match": 0.0, "twi": 0.0, "n": 0}
+
     def p_step(bi, io=None):
         """Prefill side of one step."""
         moved = 0
         sent = []
         for prompt, partial in batches[bi % len(batches)]:
+            t0 = time.perf_counter()
             mt, matched = P.match(prompt)
             src = np.concatenate([matched, partial])
             priv = prompt.tobytes() if role.kind == "P" else b""
+            t1 = time.perf_counter()
             final, nm = P.transfer_with_insert(role.d_inst, prompt, src,
                                                flags=M.XFER_DEDUP | M.XFER_ASYNC, priv=priv)
+            t2 = time.perf_counter()
+            if io is not None:
+                host_t["match"] += t1 - t0
+                host_t["twi"] += t2 - t1
+                host_t["n"] += 1
             moved += nm
             sent.append((prompt, final))
             if io is not None:
@@ -301,7 +310,8 @@ def run_ours(args, rank, world, dist):
         "frac": round(achieved / roof["peak"], 4) if achieved else None,
         "traffic": None, "bytes_per_launch_algorithmic": alg,
         "avg_launch_ms": round(kernel_ms, 5), "launches": int(st["timed_launches"]),
-        "share_of_step": round(st["kernel_ms"] / ms, 4) if ms > 0 else None})
+        "share_of_step": round(st["kernel_ms"] / ms, 4) if ms > 0 else None,
+        "idle_between_launches_share": round(st["gap_ms"] / ms, 4) if ms > 0 else None})
     extras = {}
     if rank == 0 and not args.no_extras:
         extras = side_measurements(M, torch, shape, seed, peak, args)
@@ -340,6 +350,8 @@ def run_ours(args, rank, world, dist):
                 "h2d_bytes_per_step": int(float(tot[2]) / args.steps),
                 "d2h_bytes_per_step": int(float(tot[3]) / args.steps)},
         "gpu_launches": launches_all,
+        "host_us_per_request": {k: round(v / max(host_t["n"], 1) * 1e6, 2)
+                                for k, v in host_t.items() if k != "n"},
         "roofline": roof,
         "clocks": clocks.summary(),
     }

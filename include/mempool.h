@@ -119,7 +119,10 @@ typedef struct {
   int32_t staging_slots; /* ring depth (0: 4) */
   int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = one full wave) */
   int32_t copy_kernel;   /* device<->device copy engine: 0 auto, 1 vector LD/ST, 2 bulk (TMA) */
-  int32_t reserved0;
+  int32_t coalesce_mib;  /* launch coalescing of same-device fused transfers into this pool:
+                            one launch per batch, flushed when the data stream is idle, at
+                            this many MiB, or when anything else touches either pool;
+                            0: 1024 MiB, < 0: off (one launch per transfer) */
 } mp_pool_config;
 
 typedef struct {
@@ -139,6 +142,8 @@ typedef struct {
   uint64_t timed_launches;    /* launches included in kernel_ms */
   uint64_t timed_bytes;       /* payload bytes of those launches */
   uint64_t aux_launches;      /* allocator / free / fill kernels launched */
+  double gap_ms;              /* data-stream idle time between consecutive timed launches
+                                 issued between two syncs (profiling on) */
 } mp_stats;
 
 typedef struct {

@@ -19,6 +19,7 @@ mp_status mp_swap_out(mp_pool* p, int64_t n, uint32_t flags, mp_addr* out_old, m
   (void)flags;
   if (!p || n < 0 || (n > 0 && (!out_old || !out_new))) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
+  TRY(flush_involving(p));  // victims may still be the target of a coalesced copy
   std::vector<std::pair<int32_t, int32_t>> pairs;
   bool no_dram = false;
   while ((int64_t)pairs.size() < n) {
@@ -85,6 +86,7 @@ mp_status mp_swap_in(mp_pool* p, const mp_addr* a, int64_t n, uint32_t flags, mp
   const std::vector<mpi::Node*> none;
   if (!can_make_room(p, n, MP_HBM, none)) return MP_ERR_OOM;
   DevGuard g(p->dev);
+  TRY(flush_involving(p));
   if (p->nfree[MP_HBM] < n) evict_internal(p, n - p->nfree[MP_HBM], MP_HBM, nullptr);
   std::vector<int32_t> hids;
   int *dh = nullptr, *dd = nullptr;
@@ -122,6 +124,7 @@ static mp_status pack_unpack(mp_pool* p, const mp_addr* a, int64_t n, int32_t l0
     ids[(size_t)i] = idx;
   }
   DevGuard g(p->dev);
+  TRY(flush_involving(p));
   int* d = nullptr;
   TRY(upload_ids(p, ids, &d));
   const int nj = 2 * (l1 - l0);
@@ -158,6 +161,7 @@ mp_status mp_debug_fill(mp_pool* p, const mp_addr* a, int64_t n, uint64_t seed) 
     ids[(size_t)i] = idx;
   }
   DevGuard g(p->dev);
+  TRY(flush_involving(p));  // a pending coalesced copy must read / write the old content
   ++p->epoch;
   int* d = nullptr;
   TRY(upload_ids(p, ids, &d));

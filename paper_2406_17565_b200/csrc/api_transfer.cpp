@@ -83,6 +83,14 @@ mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
   if (n == 0) return MP_OK;
   if (path == MP_XFER_PATH_AUTO) path = MP_XFER_PATH_FUSED;
   const bool same_dev = src->dev == dst->dev;
+  if (path == MP_XFER_PATH_FUSED && same_dev && dst->coalesce) {
+    DevGuard g(dst->dev);
+    return batch_append(src, dst, sids, dids, d_dst, j0, nj);
+  }
+  // every other path launches now: pending coalesced copies touching either
+  // pool go first
+  TRY(flush_involving(src));
+  TRY(flush_involving(dst));
   if (path == MP_XFER_PATH_FUSED && same_dev) {
     TRY(link(src, dst));
     DevGuard g(dst->dev);

@@ -381,7 +381,9 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
 cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,
                          int* err, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  alloc_kernel<<<1, 1024, 0, stream>>>(bitmap, nwords, n, out_dev, out_host, err);
+  // 256 threads: <= 8 bitmap words each up to 65536 blocks; small enough to
+  // slot in beside retiring migration CTAs
+  alloc_kernel<<<1, 256, 0, stream>>>(bitmap, nwords, n, out_dev, out_host, err);
   return cudaGetLastError();
 }
 

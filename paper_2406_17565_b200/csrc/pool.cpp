@@ -3,6 +3,7 @@
 #include "pool.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace mp {
@@ -58,12 +59,19 @@ mp_status flush_frees(mp_pool* p) {
 mp_status drain(mp_pool* p) {
   CK(cudaStreamSynchronize(p->meta));
   CK(cudaStreamSynchronize(p->stream));
-  for (const TimedLaunch& t : p->timed) {
+  for (size_t i = 0; i < p->timed.size(); ++i) {
+    const TimedLaunch& t = p->timed[i];
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, p->tev[2 * (size_t)t.pair], p->tev[2 * (size_t)t.pair + 1]));
     p->stats.kernel_ms += ms;
     p->stats.timed_launches += 1;
     p->stats.timed_bytes += t.bytes;
+    if (i > 0) {  // idle time of the data stream between consecutive migrations
+      float gap = 0.f;
+      CK(cudaEventElapsedTime(&gap, p->tev[2 * (size_t)p->timed[i - 1].pair + 1],
+                              p->tev[2 * (size_t)t.pair]));
+      p->stats.gap_ms += gap;
+    }
   }
   p->timed.clear();
   if (!p->pending_verify.empty()) {
@@ -86,8 +94,99 @@ mp_status drain(mp_pool* p) {
 }
 
 mp_status sync(mp_pool* p) {
+  TRY(flush_involving(p));
   TRY(flush_frees(p));
   return drain(p);
+}
+
+// --------------------------------------------------------- coalescing
+mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                       const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj) {
+  const int64_t n = (int64_t)sids.size();
+  auto& b = dst->batch;
+  if (b.count > 0 && (b.src != src || b.j0 != j0 || b.nj != nj || b.count + n > dst->batch_cap))
+    TRY(flush_batch(dst));
+  // Everything else pending on the two pools goes first: a batch that writes
+  // src's blocks or reads dst's blocks must not be overtaken by this one.
+  for (auto& kv : src->peers)
+    if (kv.second != dst && kv.second->batch.src == src && kv.second->batch.count)
+      TRY(flush_batch(kv.second));
+  if (src->batch.count) TRY(flush_batch(src));
+  for (auto& kv : dst->peers)
+    if (kv.second->batch.src == dst && kv.second->batch.count) TRY(flush_batch(kv.second));
+  if (b.count == 0) {
+    b.src = src;
+    b.j0 = j0;
+    b.nj = nj;
+    b.bytes = 0;
+    b.sids.clear();
+    b.dids.clear();
+  }
+  // id tables: source ids from the host, destination ids from the device
+  // allocator's output (or the caller's ids)
+  int* h = nullptr;
+  if (!arena_take(dst, n, &h)) {
+    set_err("id arena exhausted");
+    return MP_ERR_INTERNAL;
+  }
+  std::memcpy(h, sids.data(), (size_t)n * sizeof(int32_t));
+  CK(cudaMemcpyAsync(dst->bsrc + b.count, h, (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                     dst->meta));
+  if (d_dst) {
+    CK(cudaMemcpyAsync(dst->bdst + b.count, d_dst, (size_t)n * sizeof(int32_t),
+                       cudaMemcpyDeviceToDevice, dst->meta));
+  } else {
+    int* h2 = nullptr;
+    if (!arena_take(dst, n, &h2)) {
+      set_err("id arena exhausted");
+      return MP_ERR_INTERNAL;
+    }
+    std::memcpy(h2, dids.data(), (size_t)n * sizeof(int32_t));
+    CK(cudaMemcpyAsync(dst->bdst + b.count, h2, (size_t)n * sizeof(int32_t),
+                       cudaMemcpyHostToDevice, dst->meta));
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    src->pend_r[(size_t)sids[(size_t)i]] = 1;
+    dst->pend_w[(size_t)dids[(size_t)i]] = 1;
+  }
+  b.sids.insert(b.sids.end(), sids.begin(), sids.end());
+  b.dids.insert(b.dids.end(), dids.begin(), dids.end());
+  b.count += n;
+  b.bytes += (uint64_t)n * (uint64_t)nj * (uint64_t)dst->chunk;
+  dst->stats.blocks_moved += (uint64_t)n;
+  // keep the device busy: go now if its data stream has run dry
+  if (b.bytes >= dst->batch_limit ||
+      (dst->idle_flush && cudaStreamQuery(dst->stream) == cudaSuccess))
+    TRY(flush_batch(dst));
+  return MP_OK;
+}
+
+mp_status flush_batch(mp_pool* dst) {
+  auto& b = dst->batch;
+  if (b.count == 0) return MP_OK;
+  mp_pool* src = b.src;
+  const int64_t n = b.count;
+  b.count = 0;  // reentrancy guard: link / launch below do not flush
+  TRY(link(src, dst));
+  {
+    DevGuard g(dst->dev);
+    TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, dst->bsrc),
+                             pool_ep(dst->d_slabs, dst->bdst), n, b.j0, b.nj));
+  }
+  TRY(link(dst, src));
+  for (int32_t id : b.sids) src->pend_r[(size_t)id] = 0;
+  for (int32_t id : b.dids) dst->pend_w[(size_t)id] = 0;
+  b.sids.clear();
+  b.dids.clear();
+  b.bytes = 0;
+  return MP_OK;
+}
+
+mp_status flush_involving(mp_pool* p) {
+  if (p->batch.count) TRY(flush_batch(p));
+  for (auto& kv : p->peers)
+    if (kv.second->batch.src == p && kv.second->batch.count) TRY(flush_batch(kv.second));
+  return MP_OK;
 }
 
 mp_status link(mp_pool* signal, mp_pool* waiter) {
@@ -173,6 +272,11 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
     }
   }
   p->nfree[MP_HBM] -= n;
+  // a reused block may still be read or written by a coalesced copy that has
+  // not been launched yet: launch those first (stream order does the rest)
+  bool hazard = false;
+  for (int32_t id : *ids) hazard = hazard || p->pend_w[(size_t)id] || p->pend_r[(size_t)id];
+  if (hazard) TRY(flush_involving(p));
   TRY(flush_frees(p));  // the device bitmap must see every earlier free first
   int* h = nullptr;
   int* d = arena_take(p, n, &h);
@@ -262,6 +366,7 @@ const char* mp_last_error(void) { return get_err().c_str(); }
 
 void mp_pool_destroy(mp_pool* p) {
   if (!p) return;
+  if (p->stream) flush_involving(p);
   remote_close_all(p);
   {
     DevGuard g(p->dev);
@@ -285,6 +390,8 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->d_bitmap) cudaFree(p->d_bitmap);
     if (p->d_err) cudaFree(p->d_err);
     if (p->ar.d) cudaFree(p->ar.d);
+    if (p->bsrc) cudaFree(p->bsrc);
+    if (p->bdst) cudaFree(p->bdst);
     if (p->ar.h) cudaFreeHost(p->ar.h);
     if (p->own_dram && p->dram) cudaFreeHost(p->dram);
     if (p->staging) cudaFree(p->staging);
@@ -371,7 +478,15 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   DevGuard g(p->dev);
   CKC(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
-  CKC(cudaStreamCreateWithFlags(&p->meta, cudaStreamNonBlocking));
+  // The allocator's one-CTA kernel for the next transfer is issued while the
+  // current migration kernel fills every SM; at the highest priority its CTA
+  // is placed as soon as migration CTAs start retiring, so the next
+  // migration does not wait behind it.
+  {
+    int lo = 0, hi = 0;
+    CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CKC(cudaStreamCreateWithPriority(&p->meta, cudaStreamNonBlocking, hi));
+  }
   CKC(cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_meta, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_ipc, cudaEventDisableTiming | cudaEventInterprocess));
@@ -406,6 +521,17 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   CKC(cudaMemset(p->d_err, 0, sizeof(int)));
   p->ar.cap = 16 * std::max<int64_t>(std::max(p->n_hbm, p->n_dram), 4096);
   CKC(cudaMalloc(&p->ar.d, sizeof(int) * p->ar.cap));
+  p->coalesce = cfg->coalesce_mib >= 0;
+  {  // test knob: batch by size only, so tests exercise multi-transfer launches
+    const char* e = getenv("MP_COALESCE_NO_IDLE_FLUSH");
+    p->idle_flush = !(e && e[0] == '1');
+  }
+  p->batch_limit = (uint64_t)(cfg->coalesce_mib > 0 ? cfg->coalesce_mib : 1024) << 20;
+  p->batch_cap = p->n_hbm;
+  p->pend_w.assign((size_t)p->n_hbm, 0);
+  p->pend_r.assign((size_t)p->n_hbm, 0);
+  CKC(cudaMalloc(&p->bsrc, sizeof(int) * (size_t)p->batch_cap));
+  CKC(cudaMalloc(&p->bdst, sizeof(int) * (size_t)p->batch_cap));
   CKC(cudaHostAlloc(&p->ar.h, sizeof(int) * p->ar.cap, cudaHostAllocMapped | cudaHostAllocPortable));
   if (p->n_dram > 0) {
     if (cfg->dram_base) {

@@ -175,6 +175,26 @@ struct mp_pool {
   std::map<int32_t, mp_pool*> peers;
   std::map<int32_t, char**> peer_tables;   // peer's slab table, on this device
   std::deque<mp::Msg> inbox;
+  // launch coalescing of in-process fused transfers INTO this pool: consecutive
+  // transfers from the same source pool and layer range append their id
+  // lists to bsrc / bdst and go out as one migration launch when the data
+  // stream is idle, the batch reaches batch_limit bytes, or anything else
+  // touches either pool's blocks (flush_involving).
+  struct {
+    mp_pool* src = nullptr;
+    int j0 = 0, nj = 0;
+    int64_t count = 0;
+    uint64_t bytes = 0;
+    std::vector<int32_t> sids, dids;  // host copies (to clear the pending marks)
+  } batch;
+  int* bsrc = nullptr;
+  int* bdst = nullptr;
+  int64_t batch_cap = 0;
+  uint64_t batch_limit = 0;
+  std::vector<uint8_t> pend_w;  // block written by a pending batch (this pool is dst)
+  std::vector<uint8_t> pend_r;  // block read by a pending batch (this pool is src)
+  bool coalesce = true;
+  bool idle_flush = true;
   // multi-process
   uint64_t uid = 0;                        // random identity (mailbox names)
   cudaEvent_t ev_ipc = nullptr;            // interprocess event of this pool
@@ -208,6 +228,12 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
 
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
                                const mpk::Endpoint& b, int64_t n, int j0, int nj);
+
+// Launch coalescing (same-device fused transfers).
+mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                       const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj);
+mp_status flush_batch(mp_pool* dst);
+mp_status flush_involving(mp_pool* p);  // every pending batch reading or writing p's blocks
 inline mpk::Endpoint pool_ep(char** slabs, const int* ids) { return {slabs, nullptr, 0, ids}; }
 inline mpk::Endpoint agg_ep(char* base, long long stride, const int* ids) {
   return {nullptr, base, stride, ids};

@@ -209,10 +209,12 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       if (flags & MP_XFER_DST_GIVEN) given = (const mp_addr*)rd.bytes(m * (int64_t)sizeof(mp_addr));
       const int64_t plen = rd.get<int64_t>();
       const void* priv = rd.bytes(plen);
-      mp_status s = MP_OK;
-      if (!rd.ok) s = MP_ERR_CONFIG;
-      else if (r->has_pending) s = MP_ERR_PRECONDITION;
-      else if (q->type == REQ_TWI)
+      mp_status s = flush_involving(p);
+      if (s == MP_OK && !rd.ok) s = MP_ERR_CONFIG;
+      if (s == MP_OK && r->has_pending) s = MP_ERR_PRECONDITION;
+      if (s != MP_OK) {
+        // nothing prepared
+      } else if (q->type == REQ_TWI)
         s = dst_prepare_twi(p, r->inst, toks, n_tok, m, flags, given, priv, plen, &r->pending);
       else
         s = dst_prepare_xfer(p, r->inst, m, flags, given, priv, plen, &r->pending);
@@ -387,7 +389,8 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     std::vector<int32_t> moved(sids.begin() + skip, sids.end());
     int* ds = nullptr;
     const int* dd = nullptr;
-    if (cudaStreamWaitEvent(src->stream, r->ev, 0) != cudaSuccess) xs = MP_ERR_CUDA;
+    xs = flush_involving(src);
+    if (xs == MP_OK && cudaStreamWaitEvent(src->stream, r->ev, 0) != cudaSuccess) xs = MP_ERR_CUDA;
     if (xs == MP_OK && nm > 0) xs = upload_ids(src, moved, &ds);
     if (xs == MP_OK && nm > 0) {
       if (off >= 0) {

@@ -77,7 +77,7 @@ class PoolConfig(C.Structure):
         ("hbm_blocks", C.c_int64), ("dram_blocks", C.c_int64),
         ("slabs", C.POINTER(C.c_void_p)), ("dram_base", C.c_void_p),
         ("staging_bytes", C.c_int64), ("staging_slots", C.c_int32), ("max_ctas", C.c_int32),
-        ("copy_kernel", C.c_int32), ("reserved0", C.c_int32),
+        ("copy_kernel", C.c_int32), ("coalesce_mib", C.c_int32),
     ]
 
 
@@ -96,7 +96,7 @@ class Stats(C.Structure):
         ("kernel_launches", C.c_uint64), ("bytes_moved", C.c_uint64),
         ("blocks_moved", C.c_uint64), ("kernel_ms", C.c_double),
         ("timed_launches", C.c_uint64), ("timed_bytes", C.c_uint64),
-        ("aux_launches", C.c_uint64),
+        ("aux_launches", C.c_uint64), ("gap_ms", C.c_double),
     ]
 
 
@@ -199,14 +199,15 @@ class Pool:
                  head_dim: int, block_tokens: int, hbm_blocks: int, dram_blocks: int = 0,
                  elem_bytes: int = 2, slabs=None, dram_base=None, staging_bytes: int = 0,
                  staging_slots: int = 0, max_ctas: int = 0, verify: bool = False,
-                 copy_kernel: int = 0):
+                 copy_kernel: int = 0, coalesce_mib: int = 0):
         self.inst = instance_id
         self.B = block_tokens
         self.L = layers
         self._slab_arr = None
         cfg = PoolConfig(instance_id, device, layers, kv_heads, head_dim, elem_bytes,
                          block_tokens, int(verify), hbm_blocks, dram_blocks, None,
-                         dram_base, staging_bytes, staging_slots, max_ctas, copy_kernel, 0)
+                         dram_base, staging_bytes, staging_slots, max_ctas, copy_kernel,
+                         coalesce_mib)
         if slabs is not None:
             assert len(slabs) == 2 * layers
             self._slab_arr = (C.c_void_p * len(slabs))(*[int(s) for s in slabs])

@@ -92,10 +92,10 @@ def test_private_and_transfer_layers():
     assert [M.addr_index(a) for a in kinds[-1][3]] == [x[2] for x in out]
 
 
-def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0):
+def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coalesce_mib=0):
     rng = np.random.default_rng(seed)
-    P = Twin(0, shape, n_hbm, n_dram, copy_kernel=copy_kernel)
-    D = Twin(1, shape, n_hbm, n_dram, copy_kernel=copy_kernel)
+    P = Twin(0, shape, n_hbm, n_dram, copy_kernel=copy_kernel, coalesce_mib=coalesce_mib)
+    D = Twin(1, shape, n_hbm, n_dram, copy_kernel=copy_kernel, coalesce_mib=coalesce_mib)
     connect(P, D)
     B = shape.block_tokens
     pools = {0: P, 1: D}
@@ -181,6 +181,21 @@ def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0):
 def test_random_ops_tiny(path):
     for seed in range(3):
         random_ops(seed, TINY, 300, path)
+
+
+@pytest.mark.parametrize("path", [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_FUSED])
+def test_random_ops_coalesced_launches(path, monkeypatch):
+    """Launch coalescing batched by size only (no idle flush): many transfers
+    per launch, interleaved with fills, frees, swaps, deletes and transfers in
+    the other direction -- every hazard must flush in the right order."""
+    monkeypatch.setenv("MP_COALESCE_NO_IDLE_FLUSH", "1")
+    for seed in range(3):
+        random_ops(200 + seed, TINY, 400, path, coalesce_mib=1)
+
+
+def test_random_ops_no_coalescing():
+    for seed in range(2):
+        random_ops(300 + seed, TINY, 300, M.PATH_FUSED | M.XFER_ASYNC, coalesce_mib=-1)
 
 
 @pytest.mark.parametrize("path", [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_STAGED])
