@@ -340,7 +340,8 @@ def run_ours(args, rank, world, dist):
             "placement": placement,
             "pool_blocks_per_instance": n_blocks,
             "batch_blocks": args.batch_blocks,
-            "copy_kernel": ["auto(vector)", "vector", "bulk"][args.copy_kernel],
+            "copy_kernel": ["auto (bulk cp.async ring in HBM)", "vector LD/ST",
+                            "bulk cp.async ring"][args.copy_kernel],
             "blocks_moved_total": int(blocks_all),
             "l2": "inputs larger than L2 (each step moves GiBs of distinct blocks)",
         },

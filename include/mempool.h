@@ -118,7 +118,8 @@ typedef struct {
   int64_t staging_bytes; /* device staging for the STAGED path (0: 256 MiB) */
   int32_t staging_slots; /* ring depth (0: 4) */
   int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = one full wave) */
-  int32_t copy_kernel;   /* device<->device copy engine: 0 auto, 1 vector LD/ST, 2 bulk (TMA) */
+  int32_t copy_kernel;   /* copy engine: 0 auto (bulk cp.async ring within this GPU's HBM,
+                            vector LD/ST for pinned DRAM and peer memory), 1 vector, 2 bulk */
   int32_t coalesce_mib;  /* launch coalescing of same-device fused transfers into this pool:
                             one launch per batch, flushed when the data stream is idle, at
                             this many MiB, or when anything else touches either pool;

@@ -118,7 +118,7 @@ mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
     TRY(upload_ids(src, sids, &ds));
     TRY(upload_ids(src, dids, &dd));
     TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
-                             pool_ep(it->second, dd), n, j0, nj));
+                             pool_ep(it->second, dd), n, j0, nj, /*peer=*/true));
     src->stats.blocks_moved += (uint64_t)n;
     return link(src, dst);
   }

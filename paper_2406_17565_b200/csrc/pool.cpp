@@ -307,7 +307,7 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester) {
 
 // ------------------------------------------------------------ migration
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
-                               const mpk::Endpoint& b, int64_t n, int j0, int nj) {
+                               const mpk::Endpoint& b, int64_t n, int j0, int nj, bool peer) {
   if (n <= 0) return MP_OK;
   const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)p->chunk;
   const bool timed = p->profiling && s == p->stream;
@@ -319,11 +319,13 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
     p->tev_next = (p->tev_next + 1) % kTimedPairs;
     CK(cudaEventRecord(p->tev[2 * (size_t)pair], s));
   }
-  // The bulk (TMA) engine only for device <-> device copies; mapped pinned
-  // DRAM (swap) stays on the vector path.
+  // Copy engine: auto = the bulk (TMA) ring for copies within this GPU's HBM
+  // (measured ~1% ahead of the vector kernel, with a third of the issued
+  // instructions); mapped pinned DRAM (swap) and peer memory (NVLink / IPC)
+  // stay on the vector LD/ST path.
   const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
-  int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyVector : p->copy_kernel;
-  if (host_side) variant = mpk::kCopyVector;
+  int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyBulk : p->copy_kernel;
+  if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
   CK(mpk::launch_migrate(a, b, (int)n, j0, nj, p->chunk, p->max_ctas, s, variant));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));

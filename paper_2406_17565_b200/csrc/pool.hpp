@@ -226,8 +226,11 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
                     int** d_ids);
 std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
 
+// peer: one endpoint is another GPU's / process's memory (P2P or IPC mapped);
+// the copy engine choice then stays on the vector path.
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
-                               const mpk::Endpoint& b, int64_t n, int j0, int nj);
+                               const mpk::Endpoint& b, int64_t n, int j0, int nj,
+                               bool peer = false);
 
 // Launch coalescing (same-device fused transfers).
 mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,

@@ -405,7 +405,7 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     const int nj = kind == 1 ? src->nch : 2 * (l1 - l0);
     if (xs == MP_OK && nm > 0)
       xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
-                                pool_ep(r->d_slabs, dd), nm, j0, nj);
+                                pool_ep(r->d_slabs, dd), nm, j0, nj, /*peer=*/true);
     if (xs == MP_OK && cudaEventRecord(src->ev_ipc, src->stream) != cudaSuccess) xs = MP_ERR_CUDA;
     if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);
     src->stats.blocks_moved += (uint64_t)nm;
