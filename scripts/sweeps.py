@@ -1,0 +1,151 @@
+#!/usr/bin/env python
+"""Size sweeps on one B200:
+
+  transfer  configs[1]'s fixed sweep: raw P->D transfer of n scattered 7B
+            blocks, n in {1, 2, 4, ..., 256} (named point n = 128 = a 2048-token
+            prompt), for each transport (fused vector / fused bulk /
+            staged / copy-engine per chunk = the paper's discrete per-block
+            transfer).  Loopback on one GPU: HBM-bound.
+  swap      configs[4]: swap_out(n) then swap_in of the moved blocks,
+            n in {1, 2, 4, ..., 4096}, 7B pool of 8192 HBM blocks (64 GiB) and
+            4096 pinned DRAM blocks (32 GiB), plus the pinned-memcpy peak.
+
+Usage: python scripts/sweeps.py {transfer|swap} > out.json
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2406_17565_b200 import mempool as M  # noqa: E402
+from workloads.configs import LLAMA2_7B, seed_for  # noqa: E402
+
+SHAPE = LLAMA2_7B
+Pb = SHAPE.block_bytes
+
+
+def pool(inst, n, **kw):
+    return M.Pool(inst, 0, SHAPE.layers, SHAPE.kv_heads, SHAPE.head_dim, SHAPE.block_tokens,
+                  n, **kw)
+
+
+def transfer_sweep():
+    out = {"workload": "raw transfer of n scattered Llama-2-7B blocks (Pb = 8 MiB), "
+                       "loopback on one B200; payload GB/s; each repetition uses a fresh "
+                       "random source subset (working set >> L2 for n >= 16)",
+           "results": []}
+    seed = seed_for(1)
+    engines = [("fused_vector", M.PATH_FUSED, 1), ("fused_bulk", M.PATH_FUSED, 2),
+               ("staged_bulk", M.PATH_STAGED, 2), ("ce_per_chunk", M.PATH_CE, 1)]
+    for name, path, ck in engines:
+        P = pool(0, 2048, copy_kernel=ck, coalesce_mib=-1, staging_bytes=1 << 30)
+        D = pool(1, 1024, copy_kernel=ck, coalesce_mib=-1, staging_bytes=1 << 30)
+        M.connect(P, D)
+        src = P.alloc_mem(2048)
+        for k in range(0, 2048, 256):
+            P.debug_fill(src[k:k + 256], seed)
+        rng = np.random.default_rng(seed)
+        for n in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+            reps = 3 if path == M.PATH_CE and n >= 64 else 10
+            for _ in range(2):   # warm-up
+                d = P.transfer(1, src[rng.permutation(2048)[:n]], flags=path)
+                D.free_mem(d)
+            P.stats_reset()
+            D.stats_reset()
+            P.profile(True)
+            D.profile(True)
+            t = 0.0
+            for _ in range(reps):
+                sel = src[rng.permutation(2048)[:n]]
+                t0 = time.perf_counter()
+                d = P.transfer(1, sel, flags=path)
+                t += time.perf_counter() - t0
+                D.free_mem(d)
+            P.profile(False)
+            D.profile(False)
+            st = [x.stats() for x in (P, D)]
+            kms = sum(s["kernel_ms"] for s in st)
+            kl = sum(s["timed_launches"] for s in st)
+            row = {"engine": name, "n_blocks": n, "bytes": n * Pb,
+                   "call_GBps": round(n * Pb * reps / t / 1e9, 2),
+                   "call_us": round(t / reps * 1e6, 1),
+                   "blocks_per_s": round(n * reps / t, 1)}
+            if kl:
+                row["kernel_ms_per_call"] = round(kms / reps, 4)
+                row["kernels_per_call"] = kl / reps
+            out["results"].append(row)
+            print(json.dumps(row), file=sys.stderr)
+        P.close()
+        D.close()
+    return out
+
+
+def swap_sweep():
+    seed = seed_for(4)
+    B = SHAPE.block_tokens
+    n_hbm, n_dram = 8192, 4096
+    t0 = time.perf_counter()
+    S = pool(0, n_hbm, dram_blocks=n_dram)
+    pin_s = time.perf_counter() - t0
+    rng = np.random.default_rng(seed)
+    base = [rng.integers(3, 32000, size=40 * B, dtype=np.int32) for _ in range(8)]
+    seqs = []
+    for i in range(96):   # 96 historical sequences of 48-80 blocks, shared prefixes
+        pre = base[i % 8][: int(rng.integers(0, 41)) * B]
+        tail = rng.integers(3, 32000, size=int(rng.integers(48, 81)) * B - len(pre),
+                            dtype=np.int32)
+        t = np.concatenate([pre, tail]).astype(np.int32)
+        _, matched = S.match(t)
+        new = S.alloc_mem(len(t) // B - len(matched))
+        S.debug_fill(new, seed)
+        S.insert(t, np.concatenate([matched, new]))
+        seqs.append(t)
+    info = S.info()
+    # pinned-memcpy peak (torch), the host-link reference
+    a = torch.empty(1 << 30, dtype=torch.uint8, device="cuda:0")
+    h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    for _ in range(2):
+        h.copy_(a)
+        a.copy_(h)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    h.copy_(a, non_blocking=True)
+    ev[1].record()
+    a.copy_(h, non_blocking=True)
+    ev[2].record()
+    torch.cuda.synchronize()
+    d2h = (1 << 30) / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
+    h2d = (1 << 30) / (ev[1].elapsed_time(ev[2]) * 1e-3) / 1e9
+    del a, h
+    out = {"workload": "configs[4]: Llama-2-7B pool, 8192 HBM + 4096 pinned DRAM blocks, "
+                       f"96 historical sequences ({info.index_blocks} indexed blocks)",
+           "pinned_alloc_s": round(pin_s, 2),
+           "pcie_memcpy_GBps": {"d2h": round(d2h, 2), "h2d": round(h2d, 2)},
+           "results": []}
+    for n in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
+        t0 = time.perf_counter()
+        old, new = S.swap_out(n)
+        t1 = time.perf_counter()
+        back = S.swap_in(new)
+        t2 = time.perf_counter()
+        row = {"n": n, "moved": len(old), "bytes": len(old) * Pb,
+               "swap_out_GBps": round(len(old) * Pb / (t1 - t0) / 1e9, 2),
+               "swap_in_GBps": round(len(back) * Pb / (t2 - t1) / 1e9, 2),
+               "swap_out_ms": round((t1 - t0) * 1e3, 3), "swap_in_ms": round((t2 - t1) * 1e3, 3)}
+        out["results"].append(row)
+        print(json.dumps(row), file=sys.stderr)
+    S.close()
+    return out
+
+
+if __name__ == "__main__":
+    fn = {"transfer": transfer_sweep, "swap": swap_sweep}[sys.argv[1]]
+    print(json.dumps(fn(), indent=1))
