@@ -480,12 +480,13 @@ class OraclePool:
 
 # ---------------------------------------------------------------- distributed
 def _validate_src(src, src_addrs):
+    """R13 (memory asymmetry: "historical KV cache has been swapped
+    out to DRAM"): a source block may live in HBM or in the source's DRAM;
+    it must be allocated (caller-owned or index-owned) and listed once."""
     seen = set()
     for a in src_addrs:
         src._check_addr(a)
-        if a[1] != HBM:                      # R13: DRAM sources are NEXT (f1)
-            raise MPError("PRECONDITION")
-        if src.state[HBM][a[2]] not in (ACTIVE, INDEXED) or a in seen:
+        if src.state[a[1]][a[2]] not in (ACTIVE, INDEXED) or a in seen:
             raise MPError("PRECONDITION")
         seen.add(a)
 
@@ -525,7 +526,7 @@ def transfer(src, dst, src_addrs, dst_addrs=None, flags=0, layer_begin=0,
             raise MPError("DST_OOM")
         out = dst.alloc_mem(n, HBM, requester=src.inst)
     for s, d in zip(src_addrs, out):
-        dst._copy_chunks(src, HBM, s[2], HBM, d[2], 2 * layer_begin, 2 * layer_end)
+        dst._copy_chunks(src, s[1], s[2], HBM, d[2], 2 * layer_begin, 2 * layer_end)
     dst.inbox.append(("transfer", src.inst, bytes(priv), list(out)))
     return out
 
@@ -584,7 +585,7 @@ def transfer_with_insert(src, dst, tokens, src_addrs, dst_addrs=None, flags=0,
             raise MPError("DST_OOM")
         new = dst.alloc_mem(nm, HBM, requester=src.inst)
     for s, d in zip(src_addrs[skip:], new):
-        dst._copy_chunks(src, HBM, s[2], HBM, d[2], 0, dst.nch)
+        dst._copy_chunks(src, s[1], s[2], HBM, d[2], 0, dst.nch)
     full = list(matched[: q + skip]) + list(new)
     dup = dst.insert(tokens, full, flags & FLAG_INS_ERR_ON_CONFLICT)
     if matched:

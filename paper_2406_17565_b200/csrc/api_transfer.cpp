@@ -22,18 +22,23 @@
 namespace mp {
 namespace {
 
-mp_status validate_src(mp_pool* src, const mp_addr* a, int64_t n, std::vector<int32_t>* ids) {
+// R13 (memory asymmetry): a source block may be in HBM or, swapped
+// out, in the source's pinned DRAM; allocated, listed once.
+mp_status validate_src(mp_pool* src, const mp_addr* a, int64_t n, std::vector<int32_t>* ids,
+                       std::vector<uint8_t>* meds) {
   ids->resize((size_t)n);
-  std::vector<uint8_t> mark((size_t)src->n_hbm, 0);
+  meds->resize((size_t)n);
+  std::vector<uint8_t> mark[2] = {std::vector<uint8_t>((size_t)src->n_hbm, 0),
+                                  std::vector<uint8_t>((size_t)src->n_dram, 0)};
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
     int32_t idx = 0;
     if (!decode(src, a[i], &m, &idx)) return MP_ERR_INVALID_ADDR;
-    if (m != MP_HBM) return MP_ERR_PRECONDITION;  // R13
-    const uint8_t s = src->st[MP_HBM][(size_t)idx];
-    if (!(s == ST_ACTIVE || s == ST_INDEXED) || mark[(size_t)idx]) return MP_ERR_PRECONDITION;
-    mark[(size_t)idx] = 1;
+    const uint8_t s = src->st[m][(size_t)idx];
+    if (!(s == ST_ACTIVE || s == ST_INDEXED) || mark[m][(size_t)idx]) return MP_ERR_PRECONDITION;
+    mark[m][(size_t)idx] = 1;
     (*ids)[(size_t)i] = idx;
+    (*meds)[(size_t)i] = (uint8_t)m;
   }
   return MP_OK;
 }
@@ -71,14 +76,15 @@ RemotePeer* remote_of(mp_pool* src, int32_t inst) {
   return it == src->remotes.end() ? nullptr : it->second;
 }
 
-// The transmission step (in-process peers).  Copies chunks [j0, j0+nj) of
-// source blocks `sids` into destination blocks `dids`; d_dst is the
-// destination allocator's device table of the same ids (on dst's device) or
-// nullptr.  Enqueued after all earlier work of both pools and before their
-// later work; STAGED completes before returning, the others are stream-ordered.
-mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
-                   const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj,
-                   uint32_t path) {
+// The transmission step for HBM-resident sources (in-process peers).  Copies
+// chunks [j0, j0+nj) of source blocks `sids` into destination blocks `dids`;
+// d_dst is the destination allocator's device table of the same ids (on
+// dst's device) or nullptr.  Enqueued after all earlier work of both pools and
+// before their later work; STAGED completes before returning, the others are
+// stream-ordered.
+mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                       const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj,
+                       uint32_t path) {
   const int64_t n = (int64_t)sids.size();
   if (n == 0) return MP_OK;
   if (path == MP_XFER_PATH_AUTO) path = MP_XFER_PATH_FUSED;
@@ -195,6 +201,63 @@ mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
   }
   set_err("unknown transfer path");
   return MP_ERR_CONFIG;
+}
+
+// Sources swapped out to the source's pinned DRAM (memory asymmetry,
+// "the fastest link with the least data copies"): the DRAM block
+// is already aggregated, so one kernel reads it over PCIe and
+// scatters its chunks straight into the destination blocks -- no bounce
+// through the source's HBM.  Runs on the destination's GPU when both pools
+// share it, else on the source's GPU storing over NVLink.
+mp_status transmit_dram(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                        const std::vector<int32_t>& dids, int j0, int nj) {
+  const int64_t n = (int64_t)sids.size();
+  if (n == 0) return MP_OK;
+  TRY(flush_involving(src));
+  TRY(flush_involving(dst));
+  // aggregated block layout [2L][c]: shift the base to chunk j0
+  char* base = src->dram_dev + (int64_t)j0 * src->chunk;
+  const bool same_dev = src->dev == dst->dev;
+  mp_pool* ex = same_dev ? dst : src;
+  if (same_dev)
+    TRY(link(src, dst));
+  else
+    TRY(link(dst, src));
+  {
+    DevGuard g(ex->dev);
+    int *ds = nullptr, *dd = nullptr;
+    TRY(upload_ids(ex, sids, &ds));
+    TRY(upload_ids(ex, dids, &dd));
+    char** dslabs = dst->d_slabs;
+    if (!same_dev) {
+      auto it = src->peer_tables.find(dst->inst);
+      if (it == src->peer_tables.end()) return MP_ERR_DST_UNREACHABLE;
+      dslabs = it->second;
+    }
+    TRY(launch_migrate_timed(ex, ex->stream, agg_ep(base, src->Pb, ds), pool_ep(dslabs, dd), n,
+                             j0, nj, /*peer=*/!same_dev));
+    ex->stats.blocks_moved += (uint64_t)n;
+  }
+  return same_dev ? link(dst, src) : link(src, dst);
+}
+
+// The transmission step: HBM-resident sources take the requested transport,
+// DRAM-resident ones the direct DRAM -> destination kernel.
+mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                   const std::vector<uint8_t>& smeds, const std::vector<int32_t>& dids,
+                   const int* d_dst, int j0, int nj, uint32_t path) {
+  bool any_dram = false;
+  for (uint8_t m : smeds) any_dram = any_dram || m == MP_DRAM;
+  if (!any_dram) return transmit_hbm(src, dst, sids, dids, d_dst, j0, nj, path);
+  std::vector<int32_t> hs, hd, ds, dd;
+  for (size_t i = 0; i < sids.size(); ++i) {
+    (smeds[i] == MP_DRAM ? ds : hs).push_back(sids[i]);
+    (smeds[i] == MP_DRAM ? dd : hd).push_back(dids[i]);
+  }
+  // a mixed list no longer matches the allocator's device table order: the
+  // two parts upload their destination ids
+  if (!hs.empty()) TRY(transmit_hbm(src, dst, hs, hd, nullptr, j0, nj, path));
+  return transmit_dram(src, dst, ds, dd, j0, nj);
 }
 
 mp_status finish(mp_pool* src, mp_pool* dst, uint32_t flags) {
@@ -327,15 +390,16 @@ mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t
   if (dst) TRY(check_compatible(src, dst));
   if (!(0 <= l0 && l0 < l1 && l1 <= src->L) || (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
   std::vector<int32_t> sids;
-  TRY(validate_src(src, sa, n, &sids));
+  std::vector<uint8_t> smeds;
+  TRY(validate_src(src, sa, n, &sids, &smeds));
   if (rp)
-    return remote_transfer(src, rp, 0, nullptr, 0, sids, sa, n, da, flags, l0, l1, priv,
+    return remote_transfer(src, rp, 0, nullptr, 0, sids, smeds, n, da, flags, l0, l1, priv,
                            priv_len, nullptr);
   // ---- (1) allocation at the receiver ----
   DstPrep st;
   TRY(dst_prepare_xfer(dst, src->inst, n, flags, da, priv, priv_len, &st));
   // ---- (2) transmission ----
-  TRY(transmit(src, dst, sids, st.dids, st.d_dst, 2 * l0, 2 * (l1 - l0),
+  TRY(transmit(src, dst, sids, smeds, st.dids, st.d_dst, 2 * l0, 2 * (l1 - l0),
                flags & MP_XFER_PATH_MASK));
   // ---- (3) completion ----
   TRY(dst_commit(dst, st, da));
@@ -357,16 +421,19 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
   const int64_t B = src->B, ceil_b = (n_tok + B - 1) / B;
   if (m > ceil_b) return MP_ERR_ADDR_COUNT;
   std::vector<int32_t> sids;
-  TRY(validate_src(src, sa, m, &sids));
+  std::vector<uint8_t> smeds;
+  TRY(validate_src(src, sa, m, &sids, &smeds));
   if (rp)
-    return remote_transfer(src, rp, 1, toks, n_tok, sids, sa, m, da, flags, 0, src->L, priv,
+    return remote_transfer(src, rp, 1, toks, n_tok, sids, smeds, m, da, flags, 0, src->L, priv,
                            priv_len, n_moved);
   // ---- (1) allocation at the receiver, with its DEDUP match ----
   DstPrep st;
   TRY(dst_prepare_twi(dst, src->inst, toks, n_tok, m, flags, da, priv, priv_len, &st));
   // ---- (2) transmission of all layers ----
   std::vector<int32_t> moved_src(sids.begin() + st.skip, sids.end());
-  TRY(transmit(src, dst, moved_src, st.dids, st.d_dst, 0, src->nch, flags & MP_XFER_PATH_MASK));
+  std::vector<uint8_t> moved_med(smeds.begin() + st.skip, smeds.end());
+  TRY(transmit(src, dst, moved_src, moved_med, st.dids, st.d_dst, 0, src->nch,
+               flags & MP_XFER_PATH_MASK));
   // ---- (3) insertion at the receiver, ok ----
   TRY(dst_commit(dst, st, da));
   if (n_moved) *n_moved = st.nm;

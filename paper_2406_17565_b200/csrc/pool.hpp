@@ -265,8 +265,9 @@ uint64_t new_uid();
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
 void remote_close_all(mp_pool* p);
 mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,
-                          int64_t n_tok, const std::vector<int32_t>& sids, const mp_addr* sa,
-                          int64_t n, mp_addr* da, uint32_t flags, int32_t l0, int32_t l1,
-                          const void* priv, int64_t priv_len, int64_t* n_moved);
+                          int64_t n_tok, const std::vector<int32_t>& sids,
+                          const std::vector<uint8_t>& smeds, int64_t n, mp_addr* da,
+                          uint32_t flags, int32_t l0, int32_t l1, const void* priv,
+                          int64_t priv_len, int64_t* n_moved);
 
 }  // namespace mp

@@ -324,10 +324,10 @@ mp_status remote_serve_once(mp_pool* p, int64_t* served) {
 
 // ------------------------------------------------------------ sender side
 mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,
-                          int64_t n_tok, const std::vector<int32_t>& sids, const mp_addr* sa,
-                          int64_t n, mp_addr* da, uint32_t flags, int32_t l0, int32_t l1,
-                          const void* priv, int64_t priv_len, int64_t* n_moved) {
-  (void)sa;
+                          int64_t n_tok, const std::vector<int32_t>& sids,
+                          const std::vector<uint8_t>& smeds, int64_t n, mp_addr* da,
+                          uint32_t flags, int32_t l0, int32_t l1, const void* priv,
+                          int64_t priv_len, int64_t* n_moved) {
   const uint32_t path = flags & MP_XFER_PATH_MASK;
   if (path != MP_XFER_PATH_AUTO && path != MP_XFER_PATH_FUSED) {
     set_err("cross-process transfers use the fused one-sided path");
@@ -352,8 +352,8 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   // Pin our indexed source blocks while we wait: serving the peer's own
   // requests meanwhile must not evict them.
   std::vector<mpi::Node*> pinned;
-  for (int32_t id : sids) {
-    mpi::Node* nd = src->index->owner(MP_HBM, id);
+  for (size_t i = 0; i < sids.size(); ++i) {
+    mpi::Node* nd = src->index->owner(smeds[i], sids[i]);
     if (nd) {
       src->index->set_ref(nd, nd->ref + 1);
       pinned.push_back(nd);
@@ -386,26 +386,48 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   mp_status xs = MP_OK;
   {
     DevGuard g(src->dev);
-    std::vector<int32_t> moved(sids.begin() + skip, sids.end());
-    int* ds = nullptr;
-    const int* dd = nullptr;
-    xs = flush_involving(src);
-    if (xs == MP_OK && cudaStreamWaitEvent(src->stream, r->ev, 0) != cudaSuccess) xs = MP_ERR_CUDA;
-    if (xs == MP_OK && nm > 0) xs = upload_ids(src, moved, &ds);
-    if (xs == MP_OK && nm > 0) {
-      if (off >= 0) {
-        dd = r->arena + off;  // the receiver's device allocator output, IPC mapped
-      } else {
-        int* t = nullptr;
-        xs = upload_ids(src, std::vector<int32_t>(dids, dids + nm), &t);
-        dd = t;
-      }
+    // HBM-resident sources and (memory asymmetry) sources swapped
+    // out to our pinned DRAM, each with its destination ids
+    std::vector<int32_t> hs, hd, ds_, dd_;
+    bool mixed = false;
+    for (int64_t i = skip; i < n; ++i) {
+      const bool dram = smeds[(size_t)i] == MP_DRAM;
+      mixed = mixed || dram;
+      (dram ? ds_ : hs).push_back(sids[(size_t)i]);
+      (dram ? dd_ : hd).push_back(dids[i - skip]);
     }
     const int j0 = kind == 1 ? 0 : 2 * l0;
     const int nj = kind == 1 ? src->nch : 2 * (l1 - l0);
-    if (xs == MP_OK && nm > 0)
-      xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
-                                pool_ep(r->d_slabs, dd), nm, j0, nj, /*peer=*/true);
+    xs = flush_involving(src);
+    if (xs == MP_OK && cudaStreamWaitEvent(src->stream, r->ev, 0) != cudaSuccess) xs = MP_ERR_CUDA;
+    if (xs == MP_OK && !hs.empty()) {
+      int* d_s = nullptr;
+      const int* d_d = nullptr;
+      xs = upload_ids(src, hs, &d_s);
+      if (xs == MP_OK) {
+        if (off >= 0 && !mixed) {
+          d_d = r->arena + off;  // the receiver's device allocator output, IPC mapped
+        } else {
+          int* t = nullptr;
+          xs = upload_ids(src, hd, &t);
+          d_d = t;
+        }
+      }
+      if (xs == MP_OK)
+        xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
+                                  pool_ep(r->d_slabs, d_d), (int64_t)hs.size(), j0, nj,
+                                  /*peer=*/true);
+    }
+    if (xs == MP_OK && !ds_.empty()) {
+      int *d_s = nullptr, *d_d = nullptr;
+      xs = upload_ids(src, ds_, &d_s);
+      if (xs == MP_OK) xs = upload_ids(src, dd_, &d_d);
+      if (xs == MP_OK)
+        xs = launch_migrate_timed(src, src->stream,
+                                  agg_ep(src->dram_dev + (int64_t)j0 * src->chunk, src->Pb, d_s),
+                                  pool_ep(r->d_slabs, d_d), (int64_t)ds_.size(), j0, nj,
+                                  /*peer=*/true);
+    }
     if (xs == MP_OK && cudaEventRecord(src->ev_ipc, src->stream) != cudaSuccess) xs = MP_ERR_CUDA;
     if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);
     src->stats.blocks_moved += (uint64_t)nm;

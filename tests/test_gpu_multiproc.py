@@ -28,7 +28,7 @@ def _run(rank, port, dedup, q):
         torch.cuda.set_device(0)
         s = TINY
         pool = M.Pool(rank, 0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64,
-                      verify=True)
+                      dram_blocks=16 if rank == 0 else 0, verify=True)
         blobs = M.exchange_handles(pool)
         pool.import_peer(blobs[1 - rank][1])
         dist.barrier()
@@ -52,6 +52,11 @@ def _run(rank, port, dedup, q):
             pool.debug_fill(extra, 17565)
             d = pool.transfer(1, extra, priv=b"plain")
             finals.append((M.addr_indices(d).tolist(), 3))
+            # memory asymmetry: historical KV swapped out to this
+            # process's pinned DRAM goes straight into the peer's HBM
+            _old, dram = pool.swap_out(2)
+            d = pool.transfer(1, dram, priv=b"from-dram")
+            finals.append((M.addr_indices(d).tolist(), 2))
             pool.send_mark(1, 7)
             out["finals"] = finals
         else:
@@ -99,7 +104,8 @@ def test_two_process_golden(dedup):
         assert "error" not in res[r], res[r].get("error")
     # oracle of the same sequence
     s = TINY
-    oP = O.OraclePool(0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64, seed=17565)
+    oP = O.OraclePool(0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64, n_dram=16,
+                      seed=17565)
     oD = O.OraclePool(1, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64, seed=17565)
     _, p1, p2, p3 = golden_prompts()
     finals = []
@@ -117,6 +123,9 @@ def test_two_process_golden(dedup):
     oP.fill(extra)
     d = O.transfer(oP, oD, extra, priv=b"plain")
     finals.append(([a[2] for a in d], 3))
+    moved = oP.swap_out(2)
+    d = O.transfer(oP, oD, [new for _o, new in moved], priv=b"from-dram")
+    finals.append(([a[2] for a in d], 2))
     assert res[0]["finals"] == finals
     for pool_o, r in ((oP, 0), (oD, 1)):
         assert res[r]["dump"] == pool_o.dump_index()

@@ -92,6 +92,32 @@ def test_private_and_transfer_layers():
     assert [M.addr_index(a) for a in kinds[-1][3]] == [x[2] for x in out]
 
 
+@pytest.mark.parametrize("path", [M.PATH_FUSED, M.PATH_FUSED | M.XFER_ASYNC, M.PATH_STAGED,
+                                  M.PATH_CE])
+def test_dram_source_memory_asymmetry(path):
+    """historical KV swapped out to DRAM goes straight from the
+    source's pinned DRAM to the receiver's HBM (mixed-media source lists,
+    whole blocks and a by-layer range)."""
+    P = Twin(0, TINY, 32, 16)
+    D = Twin(1, TINY, 32, 16)
+    connect(P, D)
+    S, p1, p2, p3 = golden_prompts()
+    for p in (p1, p2):
+        _, matched = P.match(p)
+        new = P.alloc(-(-len(p) // 16) - len(matched))
+        P.fill(new)
+        P.insert(p, (matched + new)[: len(p) // 16])
+    P.swap_out(3)
+    _, src = P.match(p2)
+    assert {a[1] for a in src} == {O.HBM, O.DRAM}
+    transfer_with_insert(P, D, p2[: len(src) * 16], src, path=path)
+    x = D.alloc(2)
+    D.fill(x)
+    transfer(P, D, src[-2:], x, oflags=O.FLAG_DST_GIVEN, l0=1, l1=2, path=path)
+    P.check_state()
+    D.check_state()
+
+
 def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coalesce_mib=0):
     rng = np.random.default_rng(seed)
     P = Twin(0, shape, n_hbm, n_dram, copy_kernel=copy_kernel, coalesce_mib=coalesce_mib)

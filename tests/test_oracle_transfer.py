@@ -61,7 +61,7 @@ def test_transfer_errors_no_state_change():
     assert e.value.name == "DST_OOM"
     assert (D.dump_index(), list(D.state[HBM])) == snap
     with pytest.raises(MPError) as e:
-        transfer(P, D, [(0, DRAM, 0)])       # R13: DRAM sources are NEXT (f1)
+        transfer(P, D, [(0, DRAM, 0)])       # R13: a FREE DRAM block is no source
     assert e.value.name in ("PRECONDITION",)
     with pytest.raises(MPError) as e:
         transfer(P, None, src)
@@ -99,6 +99,30 @@ def test_suffix_and_prefix_missing():
         transfer_with_insert(D, X, full, dsrc[3:])
     assert e.value.name == "PREFIX_MISSING"
     assert (X.clock, X.dump_index()) == snap
+
+
+def test_dram_source_memory_asymmetry():
+    """historical KV swapped out to DRAM is transferred straight
+    from DRAM.  After swap_out, the matched prefix mixes HBM and DRAM addrs;
+    the receiver's bytes must equal the ORIGINAL (pre-swap) content."""
+    P, D = mk(0), mk(1)
+    p = T(0, 48)
+    a = P.alloc_mem(6, HBM)
+    P.fill(a)
+    P.insert(p, a)
+    want = {x[2]: P.hbm_bytes[:, x[2]].copy() for x in a}
+    moved = P.swap_out(2)                    # the two deepest blocks go to DRAM
+    assert [o[2] for o, _ in moved] == [5, 4]
+    _, matched = P.match(p)
+    assert [x[1] for x in matched] == [HBM] * 4 + [DRAM] * 2
+    final, nm, _ = transfer_with_insert(P, D, p, matched)
+    assert nm == 6
+    for i, d in enumerate(final):
+        np.testing.assert_array_equal(D.hbm_bytes[:, d[2]], want[a[i][2]])
+    # by-layer from a DRAM block into a caller-given block
+    x = D.alloc_mem(1, HBM)
+    transfer(P, D, [matched[5]], x, flags=FLAG_DST_GIVEN, layer_begin=1, layer_end=3)
+    np.testing.assert_array_equal(D.hbm_bytes[2:6, x[0][2]], want[a[5][2]][2:6])
 
 
 def test_dedup_conflict_flag():
