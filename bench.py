@@ -44,6 +44,23 @@ METRIC = "KV migration GB/s (P->D transfer_with_insert payload)"
 DTYPE = "u16 (fp16 KV copied as opaque 16-bit words)"
 
 
+def ncu_traffic_ratio(engine):
+    """DRAM traffic / algorithmic bytes of the migration kernel from the latest
+    committed `ncu --set full` capture (profiles/ncu_traffic_r*.json; the
+    longest captured launch).  None when no capture exists."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_traffic_r*.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        cap = json.load(f)
+    launches = cap.get(engine) or []
+    if not launches:
+        return None, None
+    big = max(launches, key=lambda l: l["duration_us"])
+    return big["traffic_over_algorithmic"], os.path.relpath(files[-1], ROOT)
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -305,10 +322,16 @@ def run_ours(args, rank, world, dist):
                 "peak_source": "B200_PROFILING.md measured peer copy per direction "
                                f"(nominal {NVLINK_GBS} GB/s)"}
     achieved = alg / (kernel_ms * 1e-3) / 1e9 if kernel_ms > 0 else None
+    ratio, ratio_src = (ncu_traffic_ratio("vector" if args.copy_kernel == 1 else "bulk")
+                        if role.kind == "PD" else (None, None))
     roof.update({
         "achieved": round(achieved, 1) if achieved else None, "unit": "GB/s",
         "frac": round(achieved / roof["peak"], 4) if achieved else None,
-        "traffic": None, "bytes_per_launch_algorithmic": alg,
+        "traffic": round(ratio * alg) if ratio else None,
+        "traffic_note": (f"dram read+write per launch = {ratio} x algorithmic, from the ncu "
+                         f"capture {ratio_src} (writes still in L2 at kernel end are not "
+                         "counted; no re-reads)") if ratio else None,
+        "bytes_per_launch_algorithmic": alg,
         "avg_launch_ms": round(kernel_ms, 5), "launches": int(st["timed_launches"]),
         "share_of_step": round(st["kernel_ms"] / ms, 4) if ms > 0 else None,
         "idle_between_launches_share": round(st["gap_ms"] / ms, 4) if ms > 0 else None})

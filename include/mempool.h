@@ -238,6 +238,33 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_instance, const mp_t
 mp_status mp_recv_poll(mp_pool* dst, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,
                        mp_addr* addrs, int64_t addr_cap);
 
+/* ------------- asymmetric parallelism ------------- */
+/* Layout reading R16: inside a chunk the KV is head-major ([H][B][D], vLLM's
+ * paged cache puts the head dimension before the in-block token dimension),
+ * so heads [h0, h0+k) of a chunk are one contiguous range of k*B*D*elem bytes.
+ * A tensor-parallel instance of TP degree t is t pools (one per GPU), rank r
+ * holding heads [r*H/t, (r+1)*H/t) of every layer ("the KV head
+ * dimension is split evenly by tp ratio").
+ *
+ * mp_transfer_heads: copy heads [src_head0, src_head0+n_heads) of layers
+ * [layer_begin, layer_end) of n HBM source blocks into heads [dst_head0, ...)
+ * of n caller-given (active) destination blocks of an in-process peer whose
+ * kv_heads may differ (same L, B, D, elem).  The destination is an input
+ * (MP_XFER_DST_GIVEN implied); MP_XFER_ASYNC allowed; DEDUP / path flags are
+ * CONFIG.  One fused sub-chunk gather->store kernel (peer stores over NVLink
+ * when the pools are on different GPUs). */
+mp_status mp_transfer_heads(mp_pool* src, int32_t dst_instance, const mp_addr* src_addrs,
+                            int64_t n, const mp_addr* dst_addrs, uint32_t flags,
+                            int32_t src_head0, int32_t dst_head0, int32_t n_heads,
+                            int32_t layer_begin, int32_t layer_end);
+/* The repartition plan TP=p -> TP=q for H heads: every overlapping
+ * (src rank, dst rank) pair as 5 ints (src_rank, dst_rank, src_head0 within
+ * the source shard, dst_head0 within the destination shard, n_heads); the
+ * pieces cover each head exactly once.  H must be divisible by p and q
+ * (else CONFIG).  out may be NULL to query n_pieces; cap counts pieces. */
+mp_status mp_tp_plan(int32_t H, int32_t p, int32_t q, int32_t* out, int64_t cap,
+                     int64_t* n_pieces);
+
 /* ------------------- multi-process (one process per GPU) ----------------- */
 /* Serialize what a pool in ANOTHER process needs to reach this one: CUDA-IPC
  * handles of the slab allocations (slabs must come from cudaMalloc, e.g. the

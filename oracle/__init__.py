@@ -23,5 +23,5 @@ delete's terminal rule (R6), suffix/DEDUP semantics of transfer_with_insert
 from .mempool_oracle import (  # noqa: F401
     HBM, DRAM, MIXED, FREE, ACTIVE, INDEXED, ORPHAN,
     FLAG_DST_GIVEN, FLAG_DEDUP, FLAG_INS_ERR_ON_CONFLICT, FLAG_MATCH_PIN,
-    MPError, OraclePool, transfer, transfer_with_insert,
+    MPError, OraclePool, transfer, transfer_with_insert, transfer_heads, tp_plan,
 )

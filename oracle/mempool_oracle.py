@@ -531,6 +531,53 @@ def transfer(src, dst, src_addrs, dst_addrs=None, flags=0, layer_begin=0,
     return out
 
 
+def tp_plan(H, p, q):
+    """Asymmetric parallelism: rank r of a TP=t instance holds
+    heads [r*H/t, (r+1)*H/t) ("split evenly by tp ratio").  The
+    pieces of a TP=p -> TP=q move: for every overlapping (src rank, dst rank),
+    (r, s, first head within the source shard, first head within the
+    destination shard, head count).  Brute force over heads: each head h goes
+    from rank h // (H/p) to rank h // (H/q); consecutive heads with the same
+    (r, s) form one piece."""
+    if H < 1 or p < 1 or q < 1 or H % p or H % q:
+        raise MPError("CONFIG")
+    hs, hd = H // p, H // q
+    pieces = []
+    for h in range(H):
+        r, s = h // hs, h // hd
+        if pieces and pieces[-1][0] == r and pieces[-1][1] == s:
+            r_, s_, a, b, k = pieces[-1]
+            pieces[-1] = (r_, s_, a, b, k + 1)
+        else:
+            pieces.append((r, s, h - r * hs, h - s * hd, 1))
+    return sorted(pieces)
+
+
+def transfer_heads(src, dst, src_addrs, dst_addrs, src_head0, dst_head0, n_heads,
+                   layer_begin=0, layer_end=None, kv_heads=None):
+    """Copy heads [src_head0, +n_heads) of layers [layer_begin, layer_end) of
+    each source block into heads [dst_head0, ...) of the given destination
+    blocks.  Reading R16: a chunk is head-major [H][B][D], so a head is a
+    contiguous slice of B*D*elem bytes.  Materialised pools only (the tag
+    model is per chunk: touched chunks lose their tag)."""
+    layer_end = src.L if layer_end is None else layer_end
+    sH, dH = kv_heads
+    if (not (0 <= layer_begin < layer_end <= src.L) or n_heads < 1 or src_head0 < 0
+            or dst_head0 < 0 or src_head0 + n_heads > sH or dst_head0 + n_heads > dH):
+        raise MPError("CONFIG")
+    _validate_src(src, src_addrs)
+    if any(a[1] != HBM for a in src_addrs):
+        raise MPError("PRECONDITION")
+    _validate_dst_given(dst, dst_addrs, len(src_addrs))
+    hw = src.W // sH                      # uint64 words per head per chunk
+    assert dst.W // dH == hw
+    for s, d in zip(src_addrs, dst_addrs):
+        for j in range(2 * layer_begin, 2 * layer_end):
+            dst.hbm_bytes[j, d[2], dst_head0 * hw:(dst_head0 + n_heads) * hw] = \
+                src.hbm_bytes[j, s[2], src_head0 * hw:(src_head0 + n_heads) * hw]
+            dst.tags[HBM][d[2]][j] = None
+
+
 def transfer_with_insert(src, dst, tokens, src_addrs, dst_addrs=None, flags=0,
                          priv=b""):
     """transfer_with_insert(id, tokenList, srcAddrList, dstAddrList, flags,

@@ -440,6 +440,83 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
   return finish(src, dst, flags);
 }
 
+// ---------------------------------------------------------------------------
+// Asymmetric parallelism.  Chunks are head-major (R16),
+// so heads [h0, h0+k) of a chunk are one contiguous byte range of k*B*D*elem
+// bytes; a tensor-parallel repartition is a set of such sub-chunk copies
+// between the shards of two instances, planned by mp_tp_plan.
+mp_status mp_transfer_heads(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t n,
+                            const mp_addr* da, uint32_t flags, int32_t src_head0,
+                            int32_t dst_head0, int32_t n_heads, int32_t l0, int32_t l1) {
+  if (!src || n < 0 || (n > 0 && (!sa || !da))) return MP_ERR_CONFIG;
+  mp_pool* dst = peer_of(src, dst_inst);
+  if (!dst) return remote_of(src, dst_inst) ? MP_ERR_CONFIG : MP_ERR_DST_UNREACHABLE;
+  if (src->L != dst->L || src->B != dst->B || src->D != dst->D || src->elem != dst->elem ||
+      !(0 <= l0 && l0 < l1 && l1 <= src->L) || n_heads < 1 || src_head0 < 0 ||
+      dst_head0 < 0 || src_head0 + n_heads > src->H || dst_head0 + n_heads > dst->H ||
+      (flags & (MP_XFER_DEDUP | MP_XFER_PATH_MASK)))
+    return MP_ERR_CONFIG;
+  const int64_t head_bytes = (int64_t)src->B * src->D * src->elem;
+  if (head_bytes % 16) {
+    set_err("a head's bytes per chunk must be a multiple of 16");
+    return MP_ERR_CONFIG;
+  }
+  std::vector<int32_t> sids, dids;
+  std::vector<uint8_t> smeds;
+  TRY(validate_src(src, sa, n, &sids, &smeds));
+  for (uint8_t m : smeds)
+    if (m != MP_HBM) return MP_ERR_PRECONDITION;
+  TRY(validate_dst_given(dst, da, n, &dids));
+  if (n == 0) return MP_OK;
+  TRY(flush_involving(src));
+  TRY(flush_involving(dst));
+  const bool same_dev = src->dev == dst->dev;
+  mp_pool* ex = same_dev ? dst : src;
+  char** dslabs = dst->d_slabs;
+  if (!same_dev) {
+    auto it = src->peer_tables.find(dst->inst);
+    if (it == src->peer_tables.end()) return MP_ERR_DST_UNREACHABLE;
+    dslabs = it->second;
+  }
+  TRY(same_dev ? link(src, dst) : link(dst, src));
+  {
+    DevGuard g(ex->dev);
+    int *ds = nullptr, *dd = nullptr;
+    TRY(upload_ids(ex, sids, &ds));
+    TRY(upload_ids(ex, dids, &dd));
+    TRY(launch_migrate_timed(ex, ex->stream,
+                             pool_ep(src->d_slabs, ds, src->chunk, src_head0 * head_bytes),
+                             pool_ep(dslabs, dd, dst->chunk, dst_head0 * head_bytes), n, 2 * l0,
+                             2 * (l1 - l0), /*peer=*/!same_dev, n_heads * head_bytes));
+    ex->stats.blocks_moved += (uint64_t)n;
+  }
+  TRY(same_dev ? link(dst, src) : link(src, dst));
+  return finish(src, dst, flags);
+}
+
+mp_status mp_tp_plan(int32_t H, int32_t p, int32_t q, int32_t* out, int64_t cap,
+                     int64_t* n_pieces) {
+  if (H < 1 || p < 1 || q < 1 || H % p || H % q) return MP_ERR_CONFIG;
+  const int32_t hs = H / p, hd = H / q;
+  int64_t k = 0;
+  for (int32_t r = 0; r < p; ++r)
+    for (int32_t s = 0; s < q; ++s) {
+      const int32_t lo = std::max(r * hs, s * hd), hi = std::min((r + 1) * hs, (s + 1) * hd);
+      if (lo >= hi) continue;
+      if (out && k < cap) {
+        int32_t* o = out + 5 * k;
+        o[0] = r;
+        o[1] = s;
+        o[2] = lo - r * hs;
+        o[3] = lo - s * hd;
+        o[4] = hi - lo;
+      }
+      ++k;
+    }
+  if (n_pieces) *n_pieces = k;
+  return (out && k > cap) ? MP_ERR_BUFFER_TOO_SMALL : MP_OK;
+}
+
 mp_status mp_recv_poll(mp_pool* p, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,
                        mp_addr* addrs, int64_t addr_cap) {
   if (!p || !out) return MP_ERR_CONFIG;

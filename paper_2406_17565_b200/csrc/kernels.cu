@@ -34,15 +34,25 @@ __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
                : "memory");
 }
 
+// Start of the copied range of chunk (block id, slab j = j0 + jr) on one side.
+template <bool kPool>
+__device__ __forceinline__ char* chunk_ptr(const Endpoint& e, unsigned j, unsigned jr,
+                                           long long id) {
+  return kPool ? (char*)__ldg((const unsigned long long*)(e.slabs + j)) + id * e.cstride + e.off
+               : e.base + id * e.stride + (long long)jr * e.cstride + e.off;
+}
+
+// Copies `len` bytes per chunk (the whole chunk, or a head range of it).
 template <bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endpoint dst, int j0,
-                                                           int nj, long long chunk,
+                                                           int nj, long long len,
                                                            unsigned units_per_chunk,
                                                            unsigned total_units) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned warp = (blockIdx.x * (unsigned)kThreads + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * (unsigned)kThreads) >> 5;
-  const bool full_units = (chunk % kUnitBytes) == 0;
+  const bool full_units = (len % kUnitBytes) == 0;
+  const long long chunk = len;
   for (unsigned u = warp; u < total_units; u += nwarps) {
     const unsigned ch = u / units_per_chunk;
     const unsigned part = u - ch * units_per_chunk;
@@ -50,10 +60,8 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
     const unsigned jr = ch - i * (unsigned)nj;
     const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
     const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
-    const char* sp = kSrcPool ? (const char*)__ldg((const unsigned long long*)(src.slabs + j0 + jr)) + sid * chunk
-                              : src.base + sid * src.stride + (long long)jr * chunk;
-    char* dp = kDstPool ? (char*)__ldg((const unsigned long long*)(dst.slabs + j0 + jr)) + did * chunk
-                        : dst.base + did * dst.stride + (long long)jr * chunk;
+    const char* sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid);
+    char* dp = chunk_ptr<kDstPool>(dst, j0 + jr, jr, did);
     const long long off = (long long)part * kUnitBytes + lane * 16;
     uint4 v[kVec];
     if (full_units) {
@@ -147,13 +155,9 @@ __device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& d
   const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
   const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
   const long long off = (long long)part * kPiece;
-  *sp = (kSrcPool ? (const char*)__ldg((const unsigned long long*)(src.slabs + j0 + jr)) + sid * chunk
-                  : src.base + sid * src.stride + (long long)jr * chunk) +
-        off;
-  *dp = (kDstPool ? (char*)__ldg((const unsigned long long*)(dst.slabs + j0 + jr)) + did * chunk
-                  : dst.base + did * dst.stride + (long long)jr * chunk) +
-        off;
-  const long long rest = chunk - off;
+  *sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid) + off;
+  *dp = chunk_ptr<kDstPool>(dst, j0 + jr, jr, did) + off;
+  const long long rest = chunk - off;  // chunk == bytes copied per chunk
   *bytes = (uint32_t)(rest < kPiece ? rest : kPiece);
 }
 

@@ -10,27 +10,33 @@
 namespace mpk {
 
 // One side of a block copy.
-//   POOL side: chunk j of block b lives at slabs[j] + b * chunk   (per-layer
+//   POOL side: chunk j of block b lives at slabs[j] + b * cstride   (per-layer
 //              paged layout, "two blocks per LLM layer").
 //   AGG side : chunk jr (relative to the copied layer range) of block b lives
-//              at base + b * stride + jr * chunk  (aggregated layout).
+//              at base + b * stride + jr * cstride  (aggregated layout).
+// The copied range of every chunk starts `off` bytes into it (0 for whole
+// chunks; a head offset for tensor-parallel repartition).
 // ids == nullptr means the identity (block i of the copy is id i).
 struct Endpoint {
   char* const* slabs;  // device array of 2L slab pointers (POOL), else nullptr
   char* base;          // AGG base (device or mapped pinned host), else nullptr
   long long stride;    // AGG bytes per block
   const int* ids;      // device array of n ids or nullptr
+  long long cstride;   // bytes per chunk on this side
+  long long off;       // byte offset of the copied range inside each chunk
 };
 
 // Copy engines of the migration kernel.
 enum CopyVariant { kCopyAuto = 0, kCopyVector = 1, kCopyBulk = 2 };
 
-// dst.chunk(ids_d[i], j) = src.chunk(ids_s[i], j) for i < n, j in [j0, j0+nj).
+// dst.chunk(ids_d[i], j)[0:len] = src.chunk(ids_s[i], j)[0:len] (each side
+// from its own `off`) for i < n, j in [j0, j0+nj); len, offsets and strides
+// multiples of 16 bytes.
 // variant kCopyVector: 16-byte vector loads/stores by every lane;
 // kCopyBulk: cp.async.bulk (TMA engine) ring through shared memory.
 // max_ctas <= 0: one full wave (occupancy x SMs).
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
-                           long long chunk, int max_ctas, cudaStream_t stream, int variant);
+                           long long len, int max_ctas, cudaStream_t stream, int variant);
 
 // Lowest-first allocation of n blocks from a bitmap (bit = 1: free).  Writes
 // the ids ascending into out_dev (device) and out_host (mapped pinned host,

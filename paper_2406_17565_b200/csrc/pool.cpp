@@ -306,10 +306,15 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester) {
 }
 
 // ------------------------------------------------------------ migration
-mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
-                               const mpk::Endpoint& b, int64_t n, int j0, int nj, bool peer) {
+mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a0,
+                               const mpk::Endpoint& b0, int64_t n, int j0, int nj, bool peer,
+                               int64_t len) {
   if (n <= 0) return MP_OK;
-  const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)p->chunk;
+  if (len <= 0) len = p->chunk;
+  mpk::Endpoint a = a0, b = b0;
+  if (!a.cstride) a.cstride = p->chunk;
+  if (!b.cstride) b.cstride = p->chunk;
+  const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)len;
   const bool timed = p->profiling && s == p->stream;
   if (s == p->stream) TRY(meta_fence(p));  // ids uploaded / allocated on meta
   int pair = -1;
@@ -326,7 +331,7 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
   int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyBulk : p->copy_kernel;
   if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
-  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, p->chunk, p->max_ctas, s, variant));
+  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});
@@ -559,7 +564,9 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
 
 mp_status mp_connect(mp_pool* a, mp_pool* b) {
   if (!a || !b || a == b || a->inst == b->inst) return MP_ERR_CONFIG;
-  if (a->L != b->L || a->chunk != b->chunk || a->B != b->B) {
+  // kv_heads may differ: tensor-parallel shards of one model (mp_transfer_heads);
+  // whole-block transfers additionally require equal chunk sizes
+  if (a->L != b->L || a->B != b->B || a->D != b->D || a->elem != b->elem) {
     set_err("pools have different KV shapes");
     return MP_ERR_CONFIG;
   }

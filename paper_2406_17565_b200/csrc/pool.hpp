@@ -228,18 +228,24 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
 
 // peer: one endpoint is another GPU's / process's memory (P2P or IPC mapped);
 // the copy engine choice then stays on the vector path.
+// len: bytes copied per chunk (0: the whole chunk, p->chunk); an endpoint
+// with cstride == 0 uses p->chunk as its chunk stride.
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
                                const mpk::Endpoint& b, int64_t n, int j0, int nj,
-                               bool peer = false);
+                               bool peer = false, int64_t len = 0);
 
 // Launch coalescing (same-device fused transfers).
 mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
                        const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj);
 mp_status flush_batch(mp_pool* dst);
 mp_status flush_involving(mp_pool* p);  // every pending batch reading or writing p's blocks
-inline mpk::Endpoint pool_ep(char** slabs, const int* ids) { return {slabs, nullptr, 0, ids}; }
-inline mpk::Endpoint agg_ep(char* base, long long stride, const int* ids) {
-  return {nullptr, base, stride, ids};
+inline mpk::Endpoint pool_ep(char** slabs, const int* ids, long long cstride = 0,
+                             long long off = 0) {
+  return {slabs, nullptr, 0, ids, cstride, off};
+}
+inline mpk::Endpoint agg_ep(char* base, long long stride, const int* ids, long long cstride = 0,
+                            long long off = 0) {
+  return {nullptr, base, stride, ids, cstride, off};
 }
 
 mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const mp_addr* addrs,

@@ -136,6 +136,9 @@ SIGNATURES = {
     "mp_transfer_with_insert": (_I32, [_P, _I32, _PI32, _I64, _PU64, _I64, _PU64, _U32, _P,
                                        _I64, _PI64]),
     "mp_recv_poll": (_I32, [_P, C.POINTER(RecvMsg), _P, _I64, _PU64, _I64]),
+    "mp_transfer_heads": (_I32, [_P, _I32, _PU64, _I64, _PU64, _U32, _I32, _I32, _I32, _I32,
+                                 _I32]),
+    "mp_tp_plan": (_I32, [_I32, _I32, _I32, _PI32, _I64, _PI64]),
     "mp_export_handle": (_I32, [_P, _P, _I64, _PI64]),
     "mp_import_peer": (_I32, [_P, _P, _I64]),
     "mp_serve": (_I32, [_P, _I64, _I32, _PI64, _PI32]),
@@ -346,6 +349,16 @@ class Pool:
                "recv_poll")
         return m.kind, m.src_instance, pb.raw[: m.priv_len], ad[: m.n_addrs]
 
+    def transfer_heads(self, dst_instance: int, src_addrs, dst_addrs, src_head0: int,
+                       dst_head0: int, n_heads: int, layer_begin: int = 0,
+                       layer_end: int = None, flags: int = 0):
+        """Head-range copy between tensor-parallel shards."""
+        s, d = _u64(src_addrs), _u64(dst_addrs)
+        le = self.L if layer_end is None else layer_end
+        _check(_lib.mp_transfer_heads(self._h, dst_instance, _pu64(s), len(s), _pu64(d), flags,
+                                      src_head0, dst_head0, n_heads, layer_begin, le),
+               "transfer_heads")
+
     # ------------------------------------------- multi-process (one per GPU)
     def export_handle(self) -> bytes:
         n = C.c_int64(0)
@@ -432,6 +445,28 @@ class Pool:
 
 def connect(a: Pool, b: Pool):
     _check(_lib.mp_connect(a.handle, b.handle), "connect")
+
+
+def tp_plan(H: int, p: int, q: int):
+    """Pieces (src_rank, dst_rank, src_head0, dst_head0, n_heads) of a TP=p ->
+    TP=q repartition of H KV heads (mp_tp_plan)."""
+    k = C.c_int64(0)
+    _check(_lib.mp_tp_plan(H, p, q, None, 0, C.byref(k)), "tp_plan")
+    out = np.zeros(5 * max(k.value, 1), np.int32)
+    _check(_lib.mp_tp_plan(H, p, q, out.ctypes.data_as(_PI32), k.value, C.byref(k)), "tp_plan")
+    return [tuple(int(x) for x in out[5 * i: 5 * i + 5]) for i in range(k.value)]
+
+
+def repartition(src_shards, dst_shards, src_addrs_per_shard, dst_addrs_per_shard, H: int,
+                layer_begin: int = 0, layer_end: int = None, flags: int = 0):
+    """TP=p -> TP=q move of the same blocks ("the sender partitions its
+    local cache and invokes the appropriate network primitives"): one
+    transfer_heads per plan piece.  Block ids are per shard (each shard's own
+    allocation); addrs lists are aligned block by block."""
+    for r, s, h0, g0, k in tp_plan(H, len(src_shards), len(dst_shards)):
+        src_shards[r].transfer_heads(dst_shards[s].inst, src_addrs_per_shard[r],
+                                     dst_addrs_per_shard[s], h0, g0, k, layer_begin,
+                                     layer_end, flags)
 
 
 def channel_selftest(name: str, role: int, n_msgs: int, payload: int):
