@@ -166,6 +166,17 @@ mp_status mp_pool_info_get(const mp_pool* pool, mp_pool_info* out);
  * MP_XFER_ASYNC transfers that execute on its stream).  In verify mode also
  * checks every device allocation against the host shadow (MP_ERR_INTERNAL). */
 mp_status mp_sync(mp_pool* pool);
+/* Stream-ordered integration with an inference engine's own CUDA streams
+ * (e.g. torch's current stream), without host synchronisation:
+ * mp_wait_event: every later device operation of this pool (and of the
+ * transfers it takes part in) waits for `cuda_event` (a cudaEvent_t the
+ * caller recorded after writing the KV it is about to move -- the per-layer
+ * dependency of layer-by-layer transmission);
+ * mp_record_event: records `cuda_event` after all work issued so far on this
+ * pool (including MP_XFER_ASYNC transfers into it), so a consumer stream can
+ * wait for the landed blocks.  The event must belong to the pool's device. */
+mp_status mp_wait_event(mp_pool* pool, void* cuda_event);
+mp_status mp_record_event(mp_pool* pool, void* cuda_event);
 const char* mp_status_str(mp_status s);
 const char* mp_last_error(void); /* thread-local detail of the last failure */
 

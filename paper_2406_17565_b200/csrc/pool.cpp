@@ -628,6 +628,25 @@ mp_status mp_sync(mp_pool* p) {
   return sync(p);
 }
 
+mp_status mp_wait_event(mp_pool* p, void* ev) {
+  if (!p || !ev) return MP_ERR_CONFIG;
+  DevGuard g(p->dev);
+  // a pending coalesced copy was issued before the dependency existed: it
+  // must not be delayed behind it, nor run before the producer's data below
+  TRY(flush_involving(p));
+  CK(cudaStreamWaitEvent(p->stream, (cudaEvent_t)ev, 0));
+  return MP_OK;
+}
+
+mp_status mp_record_event(mp_pool* p, void* ev) {
+  if (!p || !ev) return MP_ERR_CONFIG;
+  DevGuard g(p->dev);
+  TRY(flush_involving(p));
+  TRY(meta_fence(p));
+  CK(cudaEventRecord((cudaEvent_t)ev, p->stream));
+  return MP_OK;
+}
+
 mp_status mp_profile(mp_pool* p, int32_t enable) {
   if (!p) return MP_ERR_CONFIG;
   DevGuard g(p->dev);

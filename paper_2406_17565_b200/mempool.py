@@ -121,6 +121,8 @@ SIGNATURES = {
     "mp_connect": (_I32, [_P, _P]),
     "mp_pool_info_get": (_I32, [_P, C.POINTER(PoolInfo)]),
     "mp_sync": (_I32, [_P]),
+    "mp_wait_event": (_I32, [_P, _P]),
+    "mp_record_event": (_I32, [_P, _P]),
     "mp_status_str": (C.c_char_p, [_I32]),
     "mp_last_error": (C.c_char_p, []),
     "mp_alloc_mem": (_I32, [_P, _I64, _I32, _I32, _PU64]),
@@ -195,6 +197,15 @@ def _pi32(a: np.ndarray):
     return a.ctypes.data_as(_PI32)
 
 
+def _event_handle(event) -> int:
+    """cudaEvent_t of a torch.cuda.Event (created on first record) or an int."""
+    if isinstance(event, int):
+        return event
+    if not getattr(event, "cuda_event", 0):
+        event.record()      # torch creates the CUDA event lazily, on first record
+    return int(event.cuda_event)
+
+
 class Pool:
     """One serving instance's MemPool."""
 
@@ -242,6 +253,15 @@ class Pool:
     def sync(self):
         """Wait for all device work issued on this pool (mp_sync)."""
         _check(_lib.mp_sync(self._h), "sync")
+
+    def wait_event(self, event):
+        """Later device work of this pool waits for a CUDA event (e.g. a
+        torch.cuda.Event recorded after the engine wrote the KV)."""
+        _check(_lib.mp_wait_event(self._h, C.c_void_p(_event_handle(event))), "wait_event")
+
+    def record_event(self, event):
+        """Record a CUDA event after all work issued on this pool so far."""
+        _check(_lib.mp_record_event(self._h, C.c_void_p(_event_handle(event))), "record_event")
 
     def info(self) -> PoolInfo:
         o = PoolInfo()

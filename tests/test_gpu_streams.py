@@ -1,0 +1,50 @@
+"""Stream-ordered integration with an engine's torch streams (mp_wait_event /
+mp_record_event): the layer-by-layer pattern of P:369 / P:525 -- the engine
+writes layer l's KV on its own stream, records an event, and the transfer of
+layer l (caller-given destination blocks, no allocation step) must copy the
+NEW content even though the host issues it before the write has run."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _pool(M, torch, inst, shape, n):
+    c = shape.chunk_bytes
+    region = torch.zeros(2 * shape.layers * n * c, dtype=torch.uint8, device="cuda:0")
+    slabs = [region.data_ptr() + j * n * c for j in range(2 * shape.layers)]
+    p = M.Pool(inst, 0, shape.layers, shape.kv_heads, shape.head_dim, shape.block_tokens, n,
+               slabs=slabs, verify=True)
+    return p, region.view(2 * shape.layers, n, c)
+
+
+def test_layer_by_layer_waits_for_engine_stream():
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    from workloads.configs import KVShape
+    shape = KVShape("s", 4, 4, 64, 16)
+    P, pr = _pool(M, torch, 0, shape, 16)
+    D, dr = _pool(M, torch, 1, shape, 16)
+    M.connect(P, D)
+    src = P.alloc_mem(3)
+    dst = D.alloc_mem(3)
+    sid = M.addr_indices(src)
+    did = M.addr_indices(dst)
+    engine = torch.cuda.Stream()
+    landed = torch.cuda.Event()
+    for layer in range(shape.layers):
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(engine):
+            torch.cuda._sleep(2_000_000)            # the layer's "compute"
+            for kv in range(2):                      # its KV write
+                pr[2 * layer + kv, torch.as_tensor(sid, device="cuda:0")] = 10 * layer + kv + 1
+            ev.record(engine)
+        P.wait_event(ev)
+        P.transfer(1, src, dst, layer_begin=layer, layer_end=layer + 1, flags=M.XFER_ASYNC)
+    D.record_event(landed)
+    torch.cuda.current_stream().wait_event(landed)
+    got = dr[:, torch.as_tensor(did, device="cuda:0")].cpu().numpy()
+    for j in range(2 * shape.layers):
+        assert (got[j] == 10 * (j // 2) + j % 2 + 1).all(), f"chunk {j} copied stale KV"
+    P.close()
+    D.close()
