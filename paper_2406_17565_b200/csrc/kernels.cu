@@ -10,6 +10,8 @@
 //  * alloc_kernel / free_kernel : the device-resident block allocator
 //    (BASELINE.json north_star item 1) over a bitmap, lowest-first.
 //  * fill_kernel : test/bench-only synthetic KV writer (content model).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace mpk {
@@ -89,8 +91,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
 // flight with a handful of instructions; the copy itself never touches the
 // register file.  Work unit = one kPiece-byte piece of one chunk (the last
 // piece of a chunk may be shorter; chunks are multiples of 16 B).
-constexpr int kPiece = 16384;
-constexpr int kStages = 4;
+// (kPiece, kStages) are template parameters; see bulk_cfg() for the choices.
 constexpr int kBulkThreads = 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -144,7 +145,7 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <bool kSrcPool, bool kDstPool>
+template <int kPieceT, bool kSrcPool, bool kDstPool>
 __device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& dst, int j0, int nj,
                                           long long chunk, unsigned pieces_per_chunk, unsigned u,
                                           const char** sp, char** dp, uint32_t* bytes) {
@@ -154,14 +155,14 @@ __device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& d
   const unsigned jr = ch - i * (unsigned)nj;
   const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
   const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
-  const long long off = (long long)part * kPiece;
+  const long long off = (long long)part * kPieceT;
   *sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid) + off;
   *dp = chunk_ptr<kDstPool>(dst, j0 + jr, jr, did) + off;
   const long long rest = chunk - off;  // chunk == bytes copied per chunk
-  *bytes = (uint32_t)(rest < kPiece ? rest : kPiece);
+  *bytes = (uint32_t)(rest < kPieceT ? rest : kPieceT);
 }
 
-template <bool kSrcPool, bool kDstPool>
+template <int kPiece, int kStages, bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(Endpoint src, Endpoint dst,
                                                                     int j0, int nj,
                                                                     long long chunk,
@@ -181,8 +182,8 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(Endpoint src
   char* dsts[kStages];
   uint32_t lens[kStages];
   for (unsigned k = 0; k < n_mine && k < (unsigned)kStages; ++k) {
-    unit_addr<kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
-                                  blockIdx.x + k * gridDim.x, &sp, &dp, &bytes);
+    unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
+                                          blockIdx.x + k * gridDim.x, &sp, &dp, &bytes);
     dsts[k] = dp;
     lens[k] = bytes;
     mbar_expect_tx(&bars[k], bytes);
@@ -196,9 +197,9 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(Endpoint src
     if (k >= 1 && k - 1 + kStages < n_mine) {
       bulk_wait_read<1>();
       const unsigned r = (k - 1) % kStages;
-      unit_addr<kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
-                                    blockIdx.x + (k - 1 + kStages) * gridDim.x, &sp, &dp,
-                                    &bytes);
+      unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
+                                            blockIdx.x + (k - 1 + kStages) * gridDim.x, &sp,
+                                            &dp, &bytes);
       dsts[r] = dp;
       lens[r] = bytes;
       mbar_expect_tx(&bars[r], bytes);
@@ -304,23 +305,22 @@ int sm_count(int device) {
   return v > 0 ? v : 148;
 }
 
-template <bool kSrcPool, bool kDstPool>
+template <int kPieceT, int kStagesT, bool kSrcPool, bool kDstPool>
 static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                                long long chunk, int max_ctas, cudaStream_t stream) {
-  const unsigned pieces = (unsigned)((chunk + kPiece - 1) / kPiece);
+  auto kern = migrate_bulk_kernel<kPieceT, kStagesT, kSrcPool, kDstPool>;
+  const unsigned pieces = (unsigned)((chunk + kPieceT - 1) / kPieceT);
   const unsigned long long total = (unsigned long long)n * nj * pieces;
   if (total >= (1ull << 32)) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)kStages * kPiece;
+  const size_t smem = (size_t)kStagesT * kPieceT;
   int dev = 0;
   cudaGetDevice(&dev);
   static int cached_cap[64] = {0};  // per device (the smem attribute is per device too)
   int cap = max_ctas;
   if (dev >= 64 || cached_cap[dev] <= 0) {
-    cudaFuncSetAttribute(migrate_bulk_kernel<kSrcPool, kDstPool>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, migrate_bulk_kernel<kSrcPool, kDstPool>, kBulkThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkThreads, smem);
     if (per_sm <= 0) per_sm = 1;
     if (dev < 64) cached_cap[dev] = per_sm * sm_count(dev);
     if (cap <= 0) cap = per_sm * sm_count(dev);
@@ -328,20 +328,54 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
     cap = cached_cap[dev];
   }
   const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
-  migrate_bulk_kernel<kSrcPool, kDstPool><<<grid, kBulkThreads, smem, stream>>>(
-      src, dst, j0, nj, chunk, pieces, (unsigned)total);
+  kern<<<grid, kBulkThreads, smem, stream>>>(src, dst, j0, nj, chunk, pieces, (unsigned)total);
   return cudaGetLastError();
+}
+
+template <int kPieceT, int kStagesT>
+static cudaError_t launch_bulk_any(const Endpoint& src, const Endpoint& dst, int n, int j0,
+                                   int nj, long long chunk, int max_ctas, cudaStream_t stream) {
+  const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
+  if (sp && dp)
+    return launch_bulk<kPieceT, kStagesT, true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+  if (sp)
+    return launch_bulk<kPieceT, kStagesT, true, false>(src, dst, n, j0, nj, chunk, max_ctas,
+                                                       stream);
+  if (dp)
+    return launch_bulk<kPieceT, kStagesT, false, true>(src, dst, n, j0, nj, chunk, max_ctas,
+                                                       stream);
+  return launch_bulk<kPieceT, kStagesT, false, false>(src, dst, n, j0, nj, chunk, max_ctas,
+                                                      stream);
+}
+
+// Ring geometry of the bulk engine; MP_BULK_CFG=<0..5> selects one (tuning
+// knob, read once).  Measured on B200 (profiles/kernel_sweep_r01.jsonl):
+// 2 GiB scattered 7B copies reach 0.942 of the HBM copy peak with
+// 64 KiB x 3 stages (1 CTA / SM, the default), 0.925 with 16 KiB x 4.
+//   0 = 64 KiB x 3 (1 CTA / SM)     1 = 32 KiB x 3 (2 CTAs / SM)
+//   2 = 8 KiB x 6 (4 CTAs / SM)     3 = 16 KiB x 4 (3 CTAs / SM)
+//   4 = 32 KiB x 6 (1 CTA / SM)     5 = 48 KiB x 4 (1 CTA / SM)
+static int bulk_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("MP_BULK_CFG");
+    cfg = (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : 0;
+  }
+  return cfg;
 }
 
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                            long long chunk, int max_ctas, cudaStream_t stream, int variant) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
   if (variant == kCopyBulk) {
-    const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
-    if (sp && dp) return launch_bulk<true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-    if (sp) return launch_bulk<true, false>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-    if (dp) return launch_bulk<false, true>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-    return launch_bulk<false, false>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+    switch (bulk_cfg()) {
+      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+    }
   }
   const unsigned units_per_chunk = (unsigned)((chunk + kUnitBytes - 1) / kUnitBytes);
   const unsigned long long total = (unsigned long long)n * nj * units_per_chunk;
