@@ -8,19 +8,35 @@
 
 namespace mp {
 
+uint32_t next_mark(mp_pool* p) {
+  if (++p->mark_gen == 0) {  // wrapped: clear and restart
+    for (auto& m : p->mark) std::fill(m.begin(), m.end(), 0u);
+    p->mark_gen = 1;
+  }
+  return p->mark_gen;
+}
+
 // R4: keep-existing, free the caller's duplicate, trailing partial addr
 // ignored, terminal marker on prefix_k.  Validates everything first.
+// hint: nodes of prefixes 1..hint->size() walked earlier and still linked
+// (the receiver's pinned match), so only the rest is looked up; out_nodes
+// (nullable) receives the index nodes of prefixes 1..k afterwards.
 mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const mp_addr* addrs,
-                          int64_t n_addr, uint32_t flags, int64_t* n_dup) {
+                          int64_t n_addr, uint32_t flags, int64_t* n_dup,
+                          const std::vector<mpi::Node*>* hint,
+                          std::vector<mpi::Node*>* out_nodes) {
   const int64_t k = n_tok / p->B, c = (n_tok + p->B - 1) / p->B;
   if (n_tok < 0 || (n_addr != k && n_addr != c)) return MP_ERR_ADDR_COUNT;
-  std::vector<mpi::Node*> path = p->index->path(toks, k);
+  std::vector<mpi::Node*> path = hint ? p->index->path_hinted(*hint, hint->size(), toks, k)
+                                      : p->index->path(toks, k);
   std::vector<int> med((size_t)k);
   std::vector<int32_t> idx((size_t)k);
-  std::set<std::pair<int, int32_t>> seen;
+  const uint32_t g = next_mark(p);
   for (int64_t i = 0; i < k; ++i) {
     if (!decode(p, addrs[i], &med[(size_t)i], &idx[(size_t)i])) return MP_ERR_INVALID_ADDR;
-    if (!seen.insert({med[(size_t)i], idx[(size_t)i]}).second) return MP_ERR_PRECONDITION;
+    uint32_t& mk = p->mark[med[(size_t)i]][(size_t)idx[(size_t)i]];
+    if (mk == g) return MP_ERR_PRECONDITION;
+    mk = g;
     mpi::Node* ex = i < (int64_t)path.size() ? path[(size_t)i] : nullptr;
     const uint8_t s = p->st[med[(size_t)i]][(size_t)idx[(size_t)i]];
     const bool same = ex && ex->medium == med[(size_t)i] && ex->idx == idx[(size_t)i];
@@ -31,6 +47,7 @@ mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const
   int64_t dup = 0;
   mpi::Node* parent = nullptr;
   mpi::Node* last = nullptr;
+  if (out_nodes) out_nodes->clear();
   for (int64_t i = 0; i < k; ++i) {
     mpi::Node* ex = i < (int64_t)path.size() ? path[(size_t)i] : nullptr;
     if (ex) {
@@ -44,6 +61,7 @@ mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const
       last = p->index->add(parent, toks + i * p->B, med[(size_t)i], idx[(size_t)i], t);
       p->st[med[(size_t)i]][(size_t)idx[(size_t)i]] = ST_INDEXED;
     }
+    if (out_nodes) out_nodes->push_back(last);
     parent = last;
   }
   if (last) last->terminal = true;
@@ -93,14 +111,16 @@ mp_status mp_alloc_mem(mp_pool* p, int64_t n, int32_t type, int32_t requester, m
 
 mp_status mp_free_mem(mp_pool* p, const mp_addr* a, int64_t n) {
   if (!p || n < 0 || (n > 0 && !a)) return MP_ERR_CONFIG;
-  std::set<std::pair<int, int32_t>> seen;
+  const uint32_t g = next_mark(p);
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
     int32_t idx = 0;
     if (!decode(p, a[i], &m, &idx)) return MP_ERR_INVALID_ADDR;
     const uint8_t s = p->st[m][(size_t)idx];
-    if (s == ST_FREE || !seen.insert({m, idx}).second) return MP_ERR_DOUBLE_FREE;
+    uint32_t& mk = p->mark[m][(size_t)idx];
+    if (s == ST_FREE || mk == g) return MP_ERR_DOUBLE_FREE;
     if (s != ST_ACTIVE) return MP_ERR_PRECONDITION;
+    mk = g;
   }
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;

@@ -28,15 +28,15 @@ mp_status validate_src(mp_pool* src, const mp_addr* a, int64_t n, std::vector<in
                        std::vector<uint8_t>* meds) {
   ids->resize((size_t)n);
   meds->resize((size_t)n);
-  std::vector<uint8_t> mark[2] = {std::vector<uint8_t>((size_t)src->n_hbm, 0),
-                                  std::vector<uint8_t>((size_t)src->n_dram, 0)};
+  const uint32_t g = next_mark(src);
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
     int32_t idx = 0;
     if (!decode(src, a[i], &m, &idx)) return MP_ERR_INVALID_ADDR;
     const uint8_t s = src->st[m][(size_t)idx];
-    if (!(s == ST_ACTIVE || s == ST_INDEXED) || mark[m][(size_t)idx]) return MP_ERR_PRECONDITION;
-    mark[m][(size_t)idx] = 1;
+    uint32_t& mk = src->mark[m][(size_t)idx];
+    if (!(s == ST_ACTIVE || s == ST_INDEXED) || mk == g) return MP_ERR_PRECONDITION;
+    mk = g;
     (*ids)[(size_t)i] = idx;
     (*meds)[(size_t)i] = (uint8_t)m;
   }
@@ -47,14 +47,15 @@ mp_status validate_dst_given(mp_pool* dst, const mp_addr* a, int64_t n,
                              std::vector<int32_t>* ids) {
   if (!a) return MP_ERR_ADDR_COUNT;
   ids->resize((size_t)n);
-  std::vector<uint8_t> mark((size_t)dst->n_hbm, 0);
+  const uint32_t g = next_mark(dst);
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
     int32_t idx = 0;
     if (!decode(dst, a[i], &m, &idx)) return MP_ERR_INVALID_ADDR;
-    if (m != MP_HBM || dst->st[MP_HBM][(size_t)idx] != ST_ACTIVE || mark[(size_t)idx])
+    if (m != MP_HBM || dst->st[MP_HBM][(size_t)idx] != ST_ACTIVE ||
+        dst->mark[MP_HBM][(size_t)idx] == g)
       return MP_ERR_PRECONDITION;
-    mark[(size_t)idx] = 1;
+    dst->mark[MP_HBM][(size_t)idx] = g;
     (*ids)[(size_t)i] = idx;
   }
   return MP_OK;
@@ -331,8 +332,12 @@ mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, 
   // ---- mutations start here ----
   st->toks.assign(toks, toks + n_tok);
   stash_priv(st, priv, priv_len);
-  // receiver-side match, pinned while the receiver allocates (R3, R12)
-  if (need_match) st->matched = dst->index->match(toks, n_tok, /*pin=*/true);
+  // receiver-side match (the path walked above), pinned while the receiver
+  // allocates (R3, R12)
+  if (need_match) {
+    dst->index->touch_path(peek, /*pin=*/true);
+    st->matched = std::move(peek);
+  }
   if (dst_given) {
     st->dids = given_ids;
   } else {
@@ -361,11 +366,11 @@ mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out) {
     full.push_back(enc(dst, st.matched[(size_t)i]->medium, st.matched[(size_t)i]->idx));
   for (int64_t i = 0; i < st.nm; ++i) full.push_back(enc(dst, MP_HBM, st.dids[(size_t)i]));
   int64_t dup = 0;
+  std::vector<mpi::Node*> fin;  // the index nodes of prefixes 1..floor_b afterwards
   TRY(insert_internal(dst, st.toks.data(), st.n_tok, full.data(), (int64_t)full.size(),
-                      st.flags & MP_INS_ERR_ON_CONFLICT, &dup));
+                      st.flags & MP_INS_ERR_ON_CONFLICT, &dup, &st.matched, &fin));
   unpin_nodes(dst, st.matched);
   st.matched.clear();
-  std::vector<mpi::Node*> fin = dst->index->path(st.toks.data(), st.floor_b);
   for (int64_t i = 0; i < st.floor_b; ++i)
     final_out[i] = enc(dst, fin[(size_t)i]->medium, fin[(size_t)i]->idx);
   if (st.ceil_b > st.floor_b) final_out[st.floor_b] = full[(size_t)st.floor_b];

@@ -75,9 +75,36 @@ class Index {
     return out;
   }
 
+  // path() trusting the first h nodes of `hint` (a prefix walked earlier and
+  // still linked, e.g. pinned): only the remaining positions are looked up.
+  std::vector<Node*> path_hinted(const std::vector<Node*>& hint, size_t h, const int32_t* toks,
+                                 int64_t k) const {
+    h = std::min(h, std::min(hint.size(), (size_t)std::max<int64_t>(k, 0)));
+    std::vector<Node*> out(hint.begin(), hint.begin() + (std::ptrdiff_t)h);
+    const Node* p = out.empty() ? &root_ : out.back();
+    for (int64_t i = (int64_t)h; i < k; ++i) {
+      Node* c = find_child(p, toks + i * B_);
+      if (!c) break;
+      out.push_back(c);
+      p = c;
+    }
+    return out;
+  }
+
   // R5 without side effects.
   int64_t peek(const int32_t* toks, int64_t n_tok) const {
     return (int64_t)path(toks, n_tok / B_).size();
+  }
+
+  // The side effects of match (R7 tick + touch, optional R12 pin) on a path
+  // already walked with path().
+  void touch_path(const std::vector<Node*>& nodes, bool pin) {
+    const uint64_t t = tick();
+    for (Node* n : nodes) {
+      n->last_access = t;
+      if (pin) ++n->ref;
+      refresh(n);
+    }
   }
 
   // R5 + R7 (+ R12 when pin): touches matched nodes with a fresh tick.

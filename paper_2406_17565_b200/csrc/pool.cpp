@@ -461,6 +461,8 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
     p->alloc_by[m].assign((size_t)n, -1);
     p->nfree[m] = n;
   }
+  p->mark[0].assign((size_t)p->n_hbm, 0u);
+  p->mark[1].assign((size_t)p->n_dram, 0u);
   p->hfree.assign((size_t)((p->n_hbm + 63) / 64), ~0ull);
   if (p->n_hbm % 64) p->hfree.back() = (1ull << (p->n_hbm % 64)) - 1ull;
   for (int32_t i = 0; i < (int32_t)p->n_dram; ++i) p->dram_free.insert(p->dram_free.end(), i);

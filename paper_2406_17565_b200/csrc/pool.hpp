@@ -169,6 +169,8 @@ struct mp_pool {
   std::set<int32_t> dram_free;             // host-managed pinned DRAM allocator
   std::map<int32_t, int32_t> orphan_ref[2];
   std::vector<int32_t> pending_free;       // HBM ids to set in the device bitmap
+  std::vector<uint32_t> mark[2];           // scratch duplicate marks (next_mark)
+  uint32_t mark_gen = 0;
   std::vector<mp::PendingVerify> pending_verify;
   mpi::Index* index = nullptr;
   uint64_t epoch = 0;
@@ -249,7 +251,12 @@ inline mpk::Endpoint agg_ep(char* base, long long stride, const int* ids, long l
 }
 
 mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const mp_addr* addrs,
-                          int64_t n_addr, uint32_t flags, int64_t* n_dup);
+                          int64_t n_addr, uint32_t flags, int64_t* n_dup,
+                          const std::vector<mpi::Node*>* hint = nullptr,
+                          std::vector<mpi::Node*>* out_nodes = nullptr);
+// Scratch marks for duplicate detection without clearing: a block is marked
+// in the current pass iff p->mark[medium][idx] == the value returned here.
+uint32_t next_mark(mp_pool* p);
 void unpin_nodes(mp_pool* p, const std::vector<mpi::Node*>& nodes);
 
 // ---- the receiver's half of the workflow (shared by in-process and remote)
