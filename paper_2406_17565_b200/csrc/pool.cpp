@@ -57,6 +57,7 @@ mp_status flush_frees(mp_pool* p) {
 }
 
 mp_status drain(mp_pool* p) {
+  TRY(remote_apply_waits(p));  // blocks stored by other processes have landed too
   CK(cudaStreamSynchronize(p->meta));
   CK(cudaStreamSynchronize(p->stream));
   for (size_t i = 0; i < p->timed.size(); ++i) {
@@ -191,6 +192,7 @@ mp_status flush_involving(mp_pool* p) {
 
 mp_status link(mp_pool* signal, mp_pool* waiter) {
   if (signal == waiter) return MP_OK;
+  TRY(remote_apply_waits(signal));
   {
     DevGuard g(signal->dev);
     CK(cudaEventRecord(signal->ev_order, signal->stream));
@@ -316,7 +318,10 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   if (!b.cstride) b.cstride = p->chunk;
   const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)len;
   const bool timed = p->profiling && s == p->stream;
-  if (s == p->stream) TRY(meta_fence(p));  // ids uploaded / allocated on meta
+  if (s == p->stream) {
+    TRY(remote_apply_waits(p));  // blocks other processes stored into p
+    TRY(meta_fence(p));          // ids uploaded / allocated on meta
+  }
   int pair = -1;
   if (timed) {
     if ((int)p->timed.size() >= kTimedPairs) TRY(drain(p));
@@ -644,6 +649,7 @@ mp_status mp_record_event(mp_pool* p, void* ev) {
   if (!p || !ev) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
   TRY(flush_involving(p));
+  TRY(remote_apply_waits(p));
   TRY(meta_fence(p));
   CK(cudaEventRecord((cudaEvent_t)ev, p->stream));
   return MP_OK;

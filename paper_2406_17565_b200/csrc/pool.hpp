@@ -120,6 +120,11 @@ struct RemotePeer {
   Channel* in = nullptr;          // peer -> me requests
   bool has_pending = false;       // peer's transfer between prepare and commit
   DstPrep pending;
+  // the peer has stored into this pool since this pool's data stream last
+  // waited for the peer's event: the wait is applied lazily, before this
+  // pool's next data-stream work (remote_apply_waits), so consecutive inbound
+  // copies are not chained through the two processes' streams
+  bool inbound_pending = false;
 };
 
 }  // namespace mp
@@ -275,6 +280,9 @@ mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out);
 
 // remote.cpp
 uint64_t new_uid();
+// Make p's data stream wait for every peer that stored into p since the last
+// call (see RemotePeer::inbound_pending).  Cheap when nothing is pending.
+mp_status remote_apply_waits(mp_pool* p);
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
 void remote_close_all(mp_pool* p);
 mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,

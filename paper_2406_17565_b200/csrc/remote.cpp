@@ -178,7 +178,38 @@ double now_s() {
 
 constexpr double kTimeout = 300.0;  // seconds without an answer: peer unreachable
 
+// Phase timers of the cross-process workflow (MP_REMOTE_TIMING=1 prints them
+// when the pool is destroyed): [0] request -> allocation reply, [1] launch,
+// [2] done -> completion reply, [3] receiver prepare, [4] receiver commit.
+struct PhaseTimes {
+  double t[5] = {0, 0, 0, 0, 0};
+  uint64_t n[5] = {0, 0, 0, 0, 0};
+  void add(int i, double s) {
+    t[i] += s;
+    ++n[i];
+  }
+};
+thread_local PhaseTimes g_phase;
+bool timing_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MP_REMOTE_TIMING");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 }  // namespace
+
+void remote_report_timing() {
+  if (!timing_on()) return;
+  const char* names[5] = {"req->prep_reply", "launch", "done->final_reply", "serve_prepare",
+                          "serve_commit"};
+  for (int i = 0; i < 5; ++i)
+    if (g_phase.n[i])
+      fprintf(stderr, "[mempool remote] %-18s %8llu calls %10.2f us avg\n", names[i],
+              (unsigned long long)g_phase.n[i], g_phase.t[i] / g_phase.n[i] * 1e6);
+}
 
 // ---------------------------------------------------------- receiver side
 namespace {
@@ -194,6 +225,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
   uint32_t rtype = REP_ACK;
   int32_t rstatus = MP_OK;
   DevGuard g(p->dev);
+  const double t_start = timing_on() ? now_s() : 0.0;
   switch (q->type) {
     case REQ_XFER:
     case REQ_TWI: {
@@ -221,8 +253,16 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       if (s == MP_OK) {
         r->has_pending = true;
         // the sender's copy must follow this allocation and every earlier use
-        // of the blocks on this pool's streams
-        s = meta_fence(p);
+        // of the blocks on this pool's streams, including other peers' copies
+        // into them (a block freed and re-allocated); its own earlier copies
+        // are ordered by its stream already
+        for (auto& kv2 : p->remotes) {
+          RemotePeer* o = kv2.second;
+          if (o == r || !o->inbound_pending) continue;
+          if (cudaStreamWaitEvent(p->stream, o->ev, 0) != cudaSuccess) s = MP_ERR_CUDA;
+          o->inbound_pending = false;
+        }
+        if (s == MP_OK) s = meta_fence(p);
         if (s == MP_OK && cudaEventRecord(p->ev_ipc, p->stream) != cudaSuccess) s = MP_ERR_CUDA;
       }
       rtype = REP_PREP;
@@ -251,11 +291,10 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         rstatus = sender_status;
         break;
       }
-      // later work of this pool must follow the sender's copy
-      if (cudaStreamWaitEvent(p->stream, r->ev, 0) != cudaSuccess) {
-        rstatus = MP_ERR_CUDA;
-        break;
-      }
+      // later data-stream work of this pool must follow the sender's copy:
+      // applied lazily (remote_apply_waits), not chained into the next
+      // allocation the sender waits for
+      r->inbound_pending = true;
       const int64_t nfin = r->pending.kind == 1 ? r->pending.ceil_b : r->pending.nm;
       std::vector<mp_addr> fin((size_t)std::max<int64_t>(nfin, 1));
       rstatus = dst_commit(p, r->pending, fin.data());
@@ -282,6 +321,8 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
   }
   if (!wr.ok) rstatus = MP_ERR_BUFFER_TOO_SMALL;
   publish(c->rep(), rtype, rstatus, wr.len, seq);
+  if (timing_on() && (rtype == REP_PREP || rtype == REP_FINAL))
+    g_phase.add(rtype == REP_PREP ? 3 : 4, now_s() - t_start);
   return MP_OK;
 }
 
@@ -309,6 +350,17 @@ mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
 }
 
 }  // namespace
+
+mp_status remote_apply_waits(mp_pool* p) {
+  for (auto& kv : p->remotes) {
+    RemotePeer* r = kv.second;
+    if (!r->inbound_pending) continue;
+    DevGuard g(p->dev);
+    CK(cudaStreamWaitEvent(p->stream, r->ev, 0));
+    r->inbound_pending = false;
+  }
+  return MP_OK;
+}
 
 mp_status remote_serve_once(mp_pool* p, int64_t* served) {
   *served = 0;
@@ -360,9 +412,16 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     }
   }
   auto unpin = [&]() { unpin_nodes(src, pinned); };
+  const bool tm = timing_on();
+  double t0 = tm ? now_s() : 0.0;
   const uint64_t s1 = ++c->next_req;
   publish(c->req(), kind == 1 ? REQ_TWI : REQ_XFER, 0, wr.len, s1);
   mp_status st = wait_reply(src, c, s1);
+  if (tm) {
+    const double t = now_s();
+    g_phase.add(0, t - t0);
+    t0 = t;
+  }
   if (st != MP_OK) {
     unpin();
     return st;
@@ -432,12 +491,18 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);
     src->stats.blocks_moved += (uint64_t)nm;
   }
+  if (tm) {
+    const double t = now_s();
+    g_phase.add(1, t - t0);
+    t0 = t;
+  }
   // ---- notify; the receiver inserts and answers ok ----
   Writer w2{c->req_payload(), kChanCap};
   w2.put<int32_t>((int32_t)xs);
   const uint64_t s2 = ++c->next_req;
   publish(c->req(), REQ_DONE, 0, w2.len, s2);
   st = wait_reply(src, c, s2);
+  if (tm) g_phase.add(2, now_s() - t0);
   unpin();
   if (st != MP_OK) return st;
   if (xs != MP_OK) return xs;
@@ -510,6 +575,7 @@ std::string chan_name(uint64_t from, uint64_t to) {
 }  // namespace
 
 void remote_close_all(mp_pool* p) {
+  if (!p->remotes.empty()) remote_report_timing();
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
     {
