@@ -43,29 +43,13 @@ mp_status insert_internal(mp_pool* p, const mp_token* toks, int64_t n_tok, const
     if (!(s == ST_ACTIVE || (s == ST_INDEXED && same))) return MP_ERR_PRECONDITION;
     if ((flags & MP_INS_ERR_ON_CONFLICT) && ex && !same) return MP_ERR_CONFLICT;
   }
-  const uint64_t t = p->index->tick();
-  int64_t dup = 0;
-  mpi::Node* parent = nullptr;
-  mpi::Node* last = nullptr;
-  if (out_nodes) out_nodes->clear();
-  for (int64_t i = 0; i < k; ++i) {
-    mpi::Node* ex = i < (int64_t)path.size() ? path[(size_t)i] : nullptr;
-    if (ex) {
-      p->index->touch(ex, t);
-      if (!(ex->medium == med[(size_t)i] && ex->idx == idx[(size_t)i])) {
-        free_block(p, med[(size_t)i], idx[(size_t)i]);
-        ++dup;
-      }
-      last = ex;
-    } else {
-      last = p->index->add(parent, toks + i * p->B, med[(size_t)i], idx[(size_t)i], t);
-      p->st[med[(size_t)i]][(size_t)idx[(size_t)i]] = ST_INDEXED;
-    }
-    if (out_nodes) out_nodes->push_back(last);
-    parent = last;
-  }
-  if (last) last->terminal = true;
-  if (n_dup) *n_dup = dup;
+  std::vector<mpi::Index::Placed> dups, added;
+  std::vector<mpi::Node*> nodes =
+      p->index->insert_seq(path, toks, k, med.data(), idx.data(), &dups, &added);
+  for (const auto& a : added) p->st[a.medium][(size_t)a.idx] = ST_INDEXED;
+  for (const auto& d : dups) free_block(p, d.medium, d.idx);
+  if (out_nodes) out_nodes->swap(nodes);
+  if (n_dup) *n_dup = (int64_t)dups.size();
   return MP_OK;
 }
 
@@ -190,22 +174,12 @@ mp_status mp_unpin(mp_pool* p, const mp_addr* a, int64_t n) {
 
 mp_status mp_delete(mp_pool* p, const mp_token* toks, int64_t n_tok) {
   if (!p || n_tok < 0 || (n_tok > 0 && !toks)) return MP_ERR_CONFIG;
-  const int64_t k = n_tok / p->B;
-  if (k == 0) return MP_OK;
-  std::vector<mpi::Node*> path = p->index->path(toks, k);
-  if ((int64_t)path.size() < k || !path.back()->terminal) return MP_OK;
-  path.back()->terminal = false;
-  for (int64_t i = k - 1; i >= 0; --i) {
-    mpi::Node* nd = path[(size_t)i];
-    if (!nd->kids.empty() || nd->terminal) break;
-    const int m = nd->medium;
-    const int32_t idx = nd->idx, ref = nd->ref;
-    p->index->unlink(nd);
-    if (ref == 0) {
-      free_block(p, m, idx);
-    } else {
-      p->st[m][(size_t)idx] = ST_ORPHAN;
-      p->orphan_ref[m][idx] = ref;
+  for (const auto& u : p->index->erase_seq(toks, n_tok)) {
+    if (u.ref == 0) {
+      free_block(p, u.medium, u.idx);
+    } else {  // pinned: freed by the last unpin (R6, R12)
+      p->st[u.medium][(size_t)u.idx] = ST_ORPHAN;
+      p->orphan_ref[u.medium][u.idx] = u.ref;
     }
   }
   return MP_OK;

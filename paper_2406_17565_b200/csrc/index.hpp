@@ -184,6 +184,70 @@ class Index {
     refresh(p);
   }
 
+  struct Placed {
+    int medium;
+    int32_t idx;
+    int32_t ref;
+  };
+
+  // R4 (after the caller validated the blocks): one clock tick; for prefixes
+  // 1..k an existing node is touched (the caller's block, if different, is
+  // reported in `dups`: keep-existing), a missing one gets a new node holding
+  // the caller's block (reported in `added`); prefix_k becomes terminal.
+  // `path` = path(toks, k) as walked before.  Returns the nodes of 1..k.
+  std::vector<Node*> insert_seq(const std::vector<Node*>& path, const int32_t* toks, int64_t k,
+                                const int* med, const int32_t* idx, std::vector<Placed>* dups,
+                                std::vector<Placed>* added) {
+    const uint64_t t = tick();
+    std::vector<Node*> out;
+    out.reserve((size_t)std::max<int64_t>(k, 0));
+    Node* parent = nullptr;
+    for (int64_t i = 0; i < k; ++i) {
+      Node* ex = i < (int64_t)path.size() ? path[(size_t)i] : nullptr;
+      Node* cur = ex;
+      if (ex) {
+        touch(ex, t);
+        if (!(ex->medium == med[i] && ex->idx == idx[i]) && dups)
+          dups->push_back({med[i], idx[i], 0});
+      } else {
+        cur = add(parent, toks + i * B_, med[i], idx[i], t);
+        if (added) added->push_back({med[i], idx[i], 0});
+      }
+      out.push_back(cur);
+      parent = cur;
+    }
+    if (!out.empty()) out.back()->terminal = true;
+    return out;
+  }
+
+  // R6: delete a stored sequence -- no-op unless prefix_k (k = floor(n/B)) is
+  // terminal; clear it, then unlink prefixes k, k-1, ... while childless and
+  // not terminal.  Returns the unlinked blocks with their pin counts.
+  std::vector<Placed> erase_seq(const int32_t* toks, int64_t n_tok) {
+    std::vector<Placed> out;
+    const int64_t k = n_tok / B_;
+    if (k <= 0) return out;
+    std::vector<Node*> p = path(toks, k);
+    if ((int64_t)p.size() < k || !p.back()->terminal) return out;
+    p.back()->terminal = false;
+    for (int64_t i = k - 1; i >= 0; --i) {
+      Node* nd = p[(size_t)i];
+      if (!nd->kids.empty() || nd->terminal) break;
+      out.push_back({nd->medium, nd->idx, nd->ref});
+      unlink(nd);
+    }
+    return out;
+  }
+
+  // R8: unlink the least (last_access, idx) unpinned leaf of `medium`.
+  bool evict_lru_leaf(int medium, int32_t* idx) {
+    Node* v = lru_leaf(medium);
+    if (!v) return false;
+    *idx = v->idx;
+    unlink(v);
+    return true;
+  }
+
   // R8: least (last_access, idx) leaf of `medium` with ref == 0, or nullptr.
   Node* lru_leaf(int medium) const {
     if (leaves_[medium].empty()) return nullptr;

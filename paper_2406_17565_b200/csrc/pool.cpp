@@ -235,10 +235,8 @@ void free_block(mp_pool* p, int med, int32_t idx) {
 // R8: evict up to n LRU leaves of `med`; appends freed ids.
 void evict_internal(mp_pool* p, int64_t n, int med, std::vector<int32_t>* freed) {
   for (int64_t k = 0; k < n; ++k) {
-    mpi::Node* v = p->index->lru_leaf(med);
-    if (!v) break;
-    const int32_t idx = v->idx;
-    p->index->unlink(v);
+    int32_t idx = -1;
+    if (!p->index->evict_lru_leaf(med, &idx)) break;
     free_block(p, med, idx);
     if (freed) freed->push_back(idx);
   }
