@@ -276,6 +276,34 @@ mp_status mp_transfer_heads(mp_pool* src, int32_t dst_instance, const mp_addr* s
 mp_status mp_tp_plan(int32_t H, int32_t p, int32_t q, int32_t* out, int64_t cap,
                      int64_t* n_pieces);
 
+/* ------------- global scheduler: global prompt trees ---------- */
+/* Host-only (no device work).  One block-granular prompt tree per instance
+ * kind (0 prefill-only, 1 decode-only, 2 PD-colocated); each node
+ * records which instances hold that prefix and until when (update time +
+ * ttl).  Readings R17: an instance's cached prefix
+ * for a prompt is the deepest path node it holds unexpired; route() picks,
+ * among registered instances of `kind`, the longest cached prefix,
+ * ties to the least load then the lowest id, and lists every instance (any
+ * kind) holding a longer prefix than the pick -- the "extra historical KV"
+ * holders -- longest first, with their prefix lengths; the
+ * chosen instance can fetch those blocks with a suffix transfer_with_insert
+ * from the holder (R3).  Time is an explicit argument (seconds). */
+typedef struct mp_gs mp_gs;
+mp_status mp_gs_create(int32_t block_tokens, double ttl_seconds, mp_gs** out);
+void mp_gs_destroy(mp_gs* gs);
+mp_status mp_gs_register(mp_gs* gs, int32_t instance, int32_t kind);
+mp_status mp_gs_set_load(mp_gs* gs, int32_t instance, double load);
+/* Update path (a response returned): `instance` holds the prompt's
+ * full blocks as of `now`. */
+mp_status mp_gs_update(mp_gs* gs, int32_t instance, const mp_token* tokens, int64_t n_tok,
+                       double now);
+/* Lookup path.  DST_UNREACHABLE if no instance of `kind` is registered;
+ * extra_inst / extra_tokens may be NULL (then only n_extra is written);
+ * BUFFER_TOO_SMALL if more than cap extra holders. */
+mp_status mp_gs_route(mp_gs* gs, int32_t kind, const mp_token* tokens, int64_t n_tok, double now,
+                      int32_t* instance, int64_t* matched_tokens, int32_t* extra_inst,
+                      int64_t* extra_tokens, int64_t cap, int64_t* n_extra);
+
 /* ------------------- multi-process (one process per GPU) ----------------- */
 /* Serialize what a pool in ANOTHER process needs to reach this one: CUDA-IPC
  * handles of the slab allocations (slabs must come from cudaMalloc, e.g. the

@@ -17,7 +17,7 @@ LIB = os.path.join(LIBDIR, "libmempool.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 SOURCES = ["pool.cpp", "api_memory_index.cpp", "api_transfer.cpp", "api_swap.cpp",
-           "remote.cpp", "kernels.cu"]
+           "remote.cpp", "gs.cpp", "kernels.cu"]
 HEADERS = ["kernels.cuh", "index.hpp", "pool.hpp"]
 
 NVCC_FLAGS = [

@@ -141,6 +141,13 @@ SIGNATURES = {
     "mp_transfer_heads": (_I32, [_P, _I32, _PU64, _I64, _PU64, _U32, _I32, _I32, _I32, _I32,
                                  _I32]),
     "mp_tp_plan": (_I32, [_I32, _I32, _I32, _PI32, _I64, _PI64]),
+    "mp_gs_create": (_I32, [_I32, C.c_double, C.POINTER(_P)]),
+    "mp_gs_destroy": (None, [_P]),
+    "mp_gs_register": (_I32, [_P, _I32, _I32]),
+    "mp_gs_set_load": (_I32, [_P, _I32, C.c_double]),
+    "mp_gs_update": (_I32, [_P, _I32, _PI32, _I64, C.c_double]),
+    "mp_gs_route": (_I32, [_P, _I32, _PI32, _I64, C.c_double, _PI32, _PI64, _PI32, _PI64, _I64,
+                           _PI64]),
     "mp_export_handle": (_I32, [_P, _P, _I64, _PI64]),
     "mp_import_peer": (_I32, [_P, _P, _I64]),
     "mp_serve": (_I32, [_P, _I64, _I32, _PI64, _PI32]),
@@ -465,6 +472,53 @@ class Pool:
 
 def connect(a: Pool, b: Pool):
     _check(_lib.mp_connect(a.handle, b.handle), "connect")
+
+
+class GlobalScheduler:
+    """Global prompt trees + locality-aware routing, mp_gs_*."""
+
+    PREFILL, DECODE, COLOCATED = 0, 1, 2
+
+    def __init__(self, block_tokens: int, ttl_seconds: float):
+        h = C.c_void_p()
+        _check(_lib.mp_gs_create(block_tokens, ttl_seconds, C.byref(h)), "mp_gs_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.mp_gs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def register(self, instance: int, kind: int):
+        _check(_lib.mp_gs_register(self._h, instance, kind), "gs_register")
+
+    def set_load(self, instance: int, load: float):
+        _check(_lib.mp_gs_set_load(self._h, instance, load), "gs_set_load")
+
+    def update(self, instance: int, tokens, now: float):
+        t = _i32(tokens)
+        _check(_lib.mp_gs_update(self._h, instance, _pi32(t), len(t), now), "gs_update")
+
+    def route(self, kind: int, tokens, now: float):
+        """-> (instance, matched_tokens, [(extra_instance, its_prefix_tokens), ...])"""
+        t = _i32(tokens)
+        inst = C.c_int32(-1)
+        mt = C.c_int64(0)
+        n = C.c_int64(0)
+        _check(_lib.mp_gs_route(self._h, kind, _pi32(t), len(t), now, C.byref(inst),
+                                C.byref(mt), None, None, 0, C.byref(n)), "gs_route")
+        ei = np.zeros(max(n.value, 1), np.int32)
+        et = np.zeros(max(n.value, 1), np.int64)
+        _check(_lib.mp_gs_route(self._h, kind, _pi32(t), len(t), now, C.byref(inst),
+                                C.byref(mt), _pi32(ei), et.ctypes.data_as(_PI64), len(ei),
+                                C.byref(n)), "gs_route")
+        return inst.value, mt.value, [(int(ei[i]), int(et[i])) for i in range(n.value)]
 
 
 def tp_plan(H: int, p: int, q: int):
