@@ -146,6 +146,60 @@ def swap_sweep():
     return out
 
 
+def api_latency():
+    """The paper's MemPool API study: memory-API latency vs block
+    count ("~800 ns per block, linear") and index insert / match of a 4K-token
+    prompt ("<= 0.7 ms", flat in the cached ratio).  Host clock, per call."""
+    import time as _t
+    out = {"workload": "Llama-2-7B pool of 8192 blocks on one B200; per-call host time",
+           "alloc_free": [], "index": []}
+    P = pool(0, 8192)
+    for n in (16, 64, 256, 1024, 4096):
+        reps = 20
+        ta = tf = 0.0
+        for _ in range(reps):
+            t0 = _t.perf_counter()
+            a = P.alloc_mem(n)
+            t1 = _t.perf_counter()
+            P.free_mem(a)
+            t2 = _t.perf_counter()
+            ta += t1 - t0
+            tf += t2 - t1
+        out["alloc_free"].append({"blocks": n, "alloc_us": round(ta / reps * 1e6, 2),
+                                  "free_us": round(tf / reps * 1e6, 2),
+                                  "alloc_ns_per_block": round(ta / reps / n * 1e9, 1)})
+    rng = np.random.default_rng(0)
+    B = SHAPE.block_tokens
+    base = rng.integers(3, 32000, size=4096, dtype=np.int32)       # 256 blocks
+    for cached in (0.0, 0.25, 0.5, 0.75, 1.0):
+        k = int(256 * cached)
+        ti = tm = 0.0
+        reps = 10
+        for r in range(reps):
+            prompt = np.concatenate([base[: k * B],
+                                     rng.integers(3, 32000, size=4096 - k * B, dtype=np.int32)])
+            if k:
+                _, m = P.match(base[: k * B])
+                if len(m) < k:
+                    a = P.alloc_mem(k - len(m))
+                    P.insert(base[: k * B], np.concatenate([m, a]))
+            t0 = _t.perf_counter()
+            mt, m = P.match(prompt)
+            t1 = _t.perf_counter()
+            new = P.alloc_mem(256 - len(m))
+            t2 = _t.perf_counter()
+            P.insert(prompt, np.concatenate([m, new]))
+            t3 = _t.perf_counter()
+            tm += t1 - t0
+            ti += t3 - t2
+            P.delete(prompt)
+        out["index"].append({"prompt_tokens": 4096, "cached_ratio": cached,
+                             "match_us": round(tm / reps * 1e6, 1),
+                             "insert_us": round(ti / reps * 1e6, 1)})
+    P.close()
+    return out
+
+
 if __name__ == "__main__":
-    fn = {"transfer": transfer_sweep, "swap": swap_sweep}[sys.argv[1]]
+    fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))
