@@ -93,9 +93,12 @@ typedef enum {
 #define MP_XFER_PATH_FUSED (1u << MP_XFER_PATH_SHIFT)  /* one gather->store kernel, no staging (A6f) */
 #define MP_XFER_PATH_STAGED (2u << MP_XFER_PATH_SHIFT) /* pack -> copy -> unpack (A4, A5, A6) */
 #define MP_XFER_PATH_CE (3u << MP_XFER_PATH_SHIFT)     /* copy engines, one memcpy per chunk (library baseline) */
-/* Swap transport selection (mp_swap_out / mp_swap_in flags argument). */
+#define MP_XFER_PATH_CE_BATCH (4u << MP_XFER_PATH_SHIFT) /* one cudaMemcpyBatchAsync of all chunks (library baseline) */
+/* Swap transport (mp_swap_out / mp_swap_in flags).  Default (0): MP_SWAP_CE
+ * when the pool's staging buffer holds at least one block, else zero-copy. */
 #define MP_SWAP_ZERO_COPY (1u << 0) /* SM loads/stores straight to mapped pinned DRAM */
-#define MP_SWAP_CE (2u << 0)        /* pack into device staging + copy-engine D2H/H2D */
+#define MP_SWAP_CE (2u << 0)        /* pack into device staging + one copy-engine D2H/H2D
+                                       per block (staging_bytes must hold >= 1 block) */
 
 typedef struct {
   int32_t instance_id;  /* < 2^24; encoded in every mp_addr */

@@ -43,7 +43,8 @@ def transfer_sweep():
            "results": []}
     seed = seed_for(1)
     engines = [("fused_vector", M.PATH_FUSED, 1), ("fused_bulk", M.PATH_FUSED, 2),
-               ("staged_bulk", M.PATH_STAGED, 2), ("ce_per_chunk", M.PATH_CE, 1)]
+               ("staged_bulk", M.PATH_STAGED, 2), ("ce_per_chunk", M.PATH_CE, 1),
+               ("ce_batch", M.PATH_CE_BATCH, 1)]
     for name, path, ck in engines:
         P = pool(0, 2048, copy_kernel=ck, coalesce_mib=-1, staging_bytes=1 << 30)
         D = pool(1, 1024, copy_kernel=ck, coalesce_mib=-1, staging_bytes=1 << 30)
@@ -84,6 +85,32 @@ def transfer_sweep():
             print(json.dumps(row), file=sys.stderr)
         P.close()
         D.close()
+    # PyTorch library baseline: the same gather/scatter as advanced indexing on
+    # [2L, N, c] byte tensors (index_select + index_copy kernels)
+    c = SHAPE.chunk_bytes
+    src_t = torch.empty(2 * SHAPE.layers, 2048, c, dtype=torch.uint8, device="cuda:0")
+    dst_t = torch.empty(2 * SHAPE.layers, 1024, c, dtype=torch.uint8, device="cuda:0")
+    rng = np.random.default_rng(seed)
+    for n in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for _ in range(2):
+            dst_t[:, torch.arange(n, device="cuda:0")] = src_t[:, torch.as_tensor(
+                rng.permutation(2048)[:n], device="cuda:0")]
+        torch.cuda.synchronize()
+        reps = 10
+        sels = [torch.as_tensor(rng.permutation(2048)[:n], device="cuda:0") for _ in range(reps)]
+        dsel = [torch.as_tensor(rng.permutation(1024)[:n], device="cuda:0") for _ in range(reps)]
+        ev[0].record()
+        for r in range(reps):
+            dst_t[:, dsel[r]] = src_t[:, sels[r]]
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / reps
+        row = {"engine": "torch_advanced_indexing", "n_blocks": n, "bytes": n * Pb,
+               "call_GBps": round(n * Pb / (ms * 1e-3) / 1e9, 2), "call_us": round(ms * 1e3, 1),
+               "blocks_per_s": round(n / (ms * 1e-3), 1), "kernel_ms_per_call": round(ms, 4)}
+        out["results"].append(row)
+        print(json.dumps(row), file=sys.stderr)
     return out
 
 
@@ -130,18 +157,22 @@ def swap_sweep():
            "pinned_alloc_s": round(pin_s, 2),
            "pcie_memcpy_GBps": {"d2h": round(d2h, 2), "h2d": round(h2d, 2)},
            "results": []}
-    for n in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
-        t0 = time.perf_counter()
-        old, new = S.swap_out(n)
-        t1 = time.perf_counter()
-        back = S.swap_in(new)
-        t2 = time.perf_counter()
-        row = {"n": n, "moved": len(old), "bytes": len(old) * Pb,
-               "swap_out_GBps": round(len(old) * Pb / (t1 - t0) / 1e9, 2),
-               "swap_in_GBps": round(len(back) * Pb / (t2 - t1) / 1e9, 2),
-               "swap_out_ms": round((t1 - t0) * 1e3, 3), "swap_in_ms": round((t2 - t1) * 1e3, 3)}
-        out["results"].append(row)
-        print(json.dumps(row), file=sys.stderr)
+    for mode, flags in (("zero_copy", M.SWAP_ZERO_COPY), ("ce_staged", M.SWAP_CE)):
+        for n in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
+            if mode == "ce_staged" and n not in (1, 16, 256, 4096):
+                continue
+            t0 = time.perf_counter()
+            old, new = S.swap_out(n, flags)
+            t1 = time.perf_counter()
+            back = S.swap_in(new, flags)
+            t2 = time.perf_counter()
+            row = {"mode": mode, "n": n, "moved": len(old), "bytes": len(old) * Pb,
+                   "swap_out_GBps": round(len(old) * Pb / (t1 - t0) / 1e9, 2),
+                   "swap_in_GBps": round(len(back) * Pb / (t2 - t1) / 1e9, 2),
+                   "swap_out_ms": round((t1 - t0) * 1e3, 3),
+                   "swap_in_ms": round((t2 - t1) * 1e3, 3)}
+            out["results"].append(row)
+            print(json.dumps(row), file=sys.stderr)
     S.close()
     return out
 

@@ -118,10 +118,13 @@ def test_dram_source_memory_asymmetry(path):
     D.check_state()
 
 
-def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coalesce_mib=0):
+def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coalesce_mib=0,
+               swap_flags=0, staging_bytes=0):
     rng = np.random.default_rng(seed)
-    P = Twin(0, shape, n_hbm, n_dram, copy_kernel=copy_kernel, coalesce_mib=coalesce_mib)
-    D = Twin(1, shape, n_hbm, n_dram, copy_kernel=copy_kernel, coalesce_mib=coalesce_mib)
+    kw = dict(copy_kernel=copy_kernel, coalesce_mib=coalesce_mib, staging_bytes=staging_bytes)
+    P = Twin(0, shape, n_hbm, n_dram, **kw)
+    D = Twin(1, shape, n_hbm, n_dram, **kw)
+    P.swap_flags = D.swap_flags = swap_flags
     connect(P, D)
     B = shape.block_tokens
     pools = {0: P, 1: D}
@@ -217,6 +220,15 @@ def test_random_ops_coalesced_launches(path, monkeypatch):
     monkeypatch.setenv("MP_COALESCE_NO_IDLE_FLUSH", "1")
     for seed in range(3):
         random_ops(200 + seed, TINY, 400, path, coalesce_mib=1)
+
+
+def test_random_ops_ce_batch_and_swap_ce():
+    """The library baselines: one cudaMemcpyBatchAsync per transfer, and swap
+    through device staging + copy-engine D2H/H2D (small staging: 2 blocks per
+    round so multi-round swaps are exercised)."""
+    for seed in range(2):
+        random_ops(400 + seed, TINY, 300, M.PATH_CE_BATCH, swap_flags=M.SWAP_CE,
+                   staging_bytes=2 * TINY.block_bytes)
 
 
 def test_random_ops_no_coalescing():

@@ -43,6 +43,7 @@ class Twin:
                         verify=verify, **kw)
         self.inst = inst
         self.seed = seed
+        self.swap_flags = 0          # MP_SWAP_* transport for swap_out / swap_in
 
     # Each op returns the oracle result (or raises MPError after checking the
     # GPU raised the same error).
@@ -96,13 +97,15 @@ class Twin:
         assert o == g, (o, g)
         return o
 
-    def swap_out(self, n, flags=0):
+    def swap_out(self, n, flags=None):
+        flags = self.swap_flags if flags is None else flags
         o, g = self.call(self.o.swap_out, lambda k: self.g.swap_out(k, flags), (n,), (n,),
                          lambda r: list(zip(to_o(r[0]), to_o(r[1]))))
         assert o == g, (o, g)
         return o
 
-    def swap_in(self, addrs, flags=0):
+    def swap_in(self, addrs, flags=None):
+        flags = self.swap_flags if flags is None else flags
         o, g = self.call(self.o.swap_in, lambda a: self.g.swap_in(a, flags), (addrs,),
                          (to_c(addrs),), to_o)
         assert o == g, (o, g)
