@@ -232,8 +232,10 @@ def test_random_ops_ce_batch_and_swap_ce():
 
 
 def test_random_ops_no_coalescing():
+    # also the zero-copy swap transport (SM stores / loads on mapped DRAM)
     for seed in range(2):
-        random_ops(300 + seed, TINY, 300, M.PATH_FUSED | M.XFER_ASYNC, coalesce_mib=-1)
+        random_ops(300 + seed, TINY, 300, M.PATH_FUSED | M.XFER_ASYNC, coalesce_mib=-1,
+                   swap_flags=M.SWAP_ZERO_COPY)
 
 
 @pytest.mark.parametrize("path", [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_STAGED])
