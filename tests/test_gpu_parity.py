@@ -187,10 +187,16 @@ def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coa
                 _, addrs = X.match(t, O.FLAG_MATCH_PIN)
                 if addrs and rng.random() < 0.7:
                     X.unpin(addrs)
-            elif op < 0.94:
+            elif op < 0.91:
                 # invalid ops must fail identically and change nothing
                 bad = [(X.inst, O.HBM, int(rng.integers(0, n_hbm)))]
                 X.free(bad)
+            elif op < 0.94:
+                # MIXED allocation (HBM first, then DRAM), DRAM-only, free
+                med = int(rng.choice([O.MIXED, O.DRAM]))
+                a = X.alloc(int(rng.integers(1, 8)), med)
+                if rng.random() < 0.5:
+                    X.free(a)
             else:
                 st = [(X.inst, O.HBM, i) for i, s in enumerate(X.o.state[O.HBM]) if s == O.ACTIVE]
                 if st:
