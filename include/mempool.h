@@ -191,6 +191,14 @@ const char* mp_last_error(void); /* thread-local detail of the last failure */
  * allocating instance.  out: n addrs. */
 mp_status mp_alloc_mem(mp_pool* pool, int64_t n, int32_t type, int32_t requester_id,
                        mp_addr* out);
+/* OR'd into alloc_mem's `type`: return without draining the pool (the
+ * cudaMallocAsync contract).  The blocks may still be read or written by
+ * earlier device work of this pool (an MP_XFER_ASYNC transfer of a block that
+ * was freed since); the caller orders its own writes after that work by
+ * making its stream wait on an event from mp_record_event, and every mp_*
+ * operation on these blocks is stream-ordered after it already.  Which
+ * blocks are returned is unchanged. */
+#define MP_ALLOC_STREAM_ORDERED (1 << 8)
 /* free_mem(addrList): only caller-owned (active) blocks; DOUBLE_FREE for a
  * free block or a repeated addr; PRECONDITION for index-owned blocks. */
 mp_status mp_free_mem(mp_pool* pool, const mp_addr* addrs, int64_t n);

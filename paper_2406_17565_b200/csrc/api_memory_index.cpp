@@ -64,6 +64,8 @@ using namespace mp;
 extern "C" {
 
 mp_status mp_alloc_mem(mp_pool* p, int64_t n, int32_t type, int32_t requester, mp_addr* out) {
+  const bool stream_ordered = (type & MP_ALLOC_STREAM_ORDERED) != 0;
+  type &= ~MP_ALLOC_STREAM_ORDERED;
   if (!p || n < 0 || (n > 0 && !out) || type < MP_HBM || type > MP_MIXED) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
   const std::vector<mpi::Node*> none;
@@ -85,8 +87,9 @@ mp_status mp_alloc_mem(mp_pool* p, int64_t n, int32_t type, int32_t requester, m
   TRY(alloc_hbm(p, nh, requester, &ids, &d));
   // The caller will write these blocks from its own streams: every earlier
   // device op of this pool (e.g. an async copy still reading a block that was
-  // freed since) must be complete first.
-  TRY(sync(p));
+  // freed since) must be complete first -- unless the caller orders its
+  // writes itself (MP_ALLOC_STREAM_ORDERED + mp_record_event).
+  if (!stream_ordered) TRY(sync(p));
   for (int64_t i = 0; i < nh; ++i) out[i] = enc(p, MP_HBM, ids[(size_t)i]);
   std::vector<int32_t> dd = alloc_dram(p, nd, requester);
   for (int64_t i = 0; i < nd; ++i) out[nh + i] = enc(p, MP_DRAM, dd[(size_t)i]);

@@ -6,7 +6,12 @@
 // point to KV cache blocks of 16 tokens").  Here every node is one B-token
 // chunk (block-chunk-keyed radix tree): children are found through a hash of
 // (parent, chunk tokens) with token-by-token equality confirmation, so a walk
-// of k blocks costs k hash probes.
+// of k blocks costs k hash probes.  The child table is one open-addressing
+// array (a probe touches the slot and the node, whose chunk is inline), and
+// the last walked path is memoised: engines match then insert the same
+// prompt, and the next turn's prompt extends it, so a walk
+// re-probes only the blocks past the common prefix while no node has been
+// unlinked since.
 //
 // Policies where the paper is silent: R5 match, R6 delete
 // (terminal markers), R7 logical clock, R8 leaf-LRU evict with (last_access,
@@ -29,7 +34,9 @@ struct Node {
   Node* parent = nullptr;
   std::vector<Node*> kids;       // children (any medium)
   int32_t pos_in_parent = -1;    // index in parent->kids
-  std::vector<int32_t> chunk;    // the B tokens of this block
+  int32_t small[16];             // the B tokens of this block (inline when B <= 16)
+  std::vector<int32_t> big;      //   (heap when B > 16)
+  const int32_t* chunk() const { return big.empty() ? small : big.data(); }
   uint64_t hkey = 0;             // key in the child hash map
   int32_t medium = 0, idx = -1;  // where the KV block lives ("anywhere")
   uint64_t last_access = 0;      // R7
@@ -65,13 +72,25 @@ class Index {
   // Existing nodes of prefixes 1..k (stops at the first missing one).
   std::vector<Node*> path(const int32_t* toks, int64_t k) const {
     std::vector<Node*> out;
-    const Node* p = &root_;
-    for (int64_t i = 0; i < k; ++i) {
+    k = std::max<int64_t>(k, 0);
+    // memo: nodes of the last walked path stay linked until an unlink
+    size_t h = 0;
+    if (memo_unlinks_ == unlinks_ && !memo_nodes_.empty()) {
+      const size_t lim = std::min((size_t)k, memo_nodes_.size()) * (size_t)B_;
+      const int32_t* m = memo_toks_.data();
+      size_t same = (size_t)(std::mismatch(toks, toks + lim, m).first - toks);
+      h = same / (size_t)B_;
+      out.assign(memo_nodes_.begin(), memo_nodes_.begin() + (std::ptrdiff_t)h);
+    }
+    out.reserve((size_t)k);
+    const Node* p = out.empty() ? &root_ : out.back();
+    for (int64_t i = (int64_t)h; i < k; ++i) {
       Node* c = find_child(p, toks + i * B_);
       if (!c) break;
       out.push_back(c);
       p = c;
     }
+    remember(toks, out);
     return out;
   }
 
@@ -133,7 +152,10 @@ class Index {
     Node* p = parent ? parent : &root_;
     Node* n = new Node();
     n->parent = p;
-    n->chunk.assign(toks, toks + B_);
+    if (B_ <= 16)
+      std::memcpy(n->small, toks, sizeof(int32_t) * (size_t)B_);
+    else
+      n->big.assign(toks, toks + B_);
     n->hkey = mix(p->id, hash_chunk(toks));
     n->medium = medium;
     n->idx = idx;
@@ -142,7 +164,7 @@ class Index {
     n->pos_in_parent = (int32_t)p->kids.size();
     p->kids.push_back(n);
     if (medium == 0) ++p->n_hbm_kids;
-    map_.emplace(n->hkey, n);
+    map_.insert(n);
     owner_[medium][(size_t)idx] = n;
     ++size_;
     refresh(p);
@@ -153,12 +175,8 @@ class Index {
   // Unlink a childless node; returns its (medium, idx, ref).
   void unlink(Node* n) {
     Node* p = n->parent;
-    auto range = map_.equal_range(n->hkey);
-    for (auto it = range.first; it != range.second; ++it)
-      if (it->second == n) {
-        map_.erase(it);
-        break;
-      }
+    map_.erase(n);
+    ++unlinks_;
     Node* last = p->kids.back();
     p->kids[(size_t)n->pos_in_parent] = last;
     last->pos_in_parent = n->pos_in_parent;
@@ -217,6 +235,7 @@ class Index {
       parent = cur;
     }
     if (!out.empty()) out.back()->terminal = true;
+    remember(toks, out);
     return out;
   }
 
@@ -295,7 +314,7 @@ class Index {
     while (!stack.empty()) {
       auto [n, pre] = stack.back();
       stack.pop_back();
-      pre.insert(pre.end(), n->chunk.begin(), n->chunk.end());
+      pre.insert(pre.end(), n->chunk(), n->chunk() + B_);
       std::string line = std::to_string(pre.size() / (size_t)B_) + "\t" + std::to_string(n->medium) +
                          "\t" + std::to_string(n->idx) + "\t" + std::to_string(n->last_access) +
                          "\t" + std::to_string(n->ref) + "\t" + (n->terminal ? "1" : "0") + "\t";
@@ -325,6 +344,7 @@ class Index {
     root_.kids.clear();
     root_.n_hbm_kids = 0;
     map_.clear();
+    ++unlinks_;
     leaves_[0].clear();
     leaves_[1].clear();
     front_.clear();
@@ -352,14 +372,76 @@ class Index {
   }
 
   Node* find_child(const Node* p, const int32_t* toks) const {
-    auto range = map_.equal_range(mix(p->id, hash_chunk(toks)));
-    for (auto it = range.first; it != range.second; ++it) {
-      Node* c = it->second;
-      if (c->parent == p && std::memcmp(c->chunk.data(), toks, sizeof(int32_t) * B_) == 0)
-        return c;
-    }
-    return nullptr;
+    return map_.find(mix(p->id, hash_chunk(toks)), p, toks, B_);
   }
+
+  void remember(const int32_t* toks, const std::vector<Node*>& nodes) const {
+    memo_toks_.assign(toks, toks + nodes.size() * (size_t)B_);
+    memo_nodes_ = nodes;
+    memo_unlinks_ = unlinks_;
+  }
+
+  // Open addressing, linear probing, backward-shift deletion; key = hkey.
+  class ChildTable {
+   public:
+    ChildTable() { slots_.assign(1024, Slot{}); }
+    void clear() {
+      slots_.assign(1024, Slot{});
+      used_ = 0;
+    }
+    void insert(Node* n) {
+      if (2 * (used_ + 1) > slots_.size()) grow();
+      put(n);
+      ++used_;
+    }
+    void erase(const Node* n) {
+      const size_t mask = slots_.size() - 1;
+      size_t i = (size_t)n->hkey & mask;
+      while (slots_[i].node != n) i = (i + 1) & mask;
+      // backward shift: pull later entries of the run into the hole
+      size_t hole = i;
+      for (size_t j = (i + 1) & mask; slots_[j].node; j = (j + 1) & mask) {
+        const size_t home = (size_t)slots_[j].key & mask;
+        if (((j - home) & mask) >= ((j - hole) & mask)) {
+          slots_[hole] = slots_[j];
+          hole = j;
+        }
+      }
+      slots_[hole] = Slot{};
+      --used_;
+    }
+    Node* find(uint64_t key, const Node* parent, const int32_t* toks, int B) const {
+      const size_t mask = slots_.size() - 1;
+      for (size_t i = (size_t)key & mask; slots_[i].node; i = (i + 1) & mask) {
+        const Slot& s = slots_[i];
+        if (s.key == key && s.node->parent == parent &&
+            std::memcmp(s.node->chunk(), toks, sizeof(int32_t) * (size_t)B) == 0)
+          return s.node;
+      }
+      return nullptr;
+    }
+
+   private:
+    struct Slot {
+      uint64_t key = 0;
+      Node* node = nullptr;
+    };
+    void put(Node* n) {
+      const size_t mask = slots_.size() - 1;
+      size_t i = (size_t)n->hkey & mask;
+      while (slots_[i].node) i = (i + 1) & mask;
+      slots_[i] = Slot{n->hkey, n};
+    }
+    void grow() {
+      std::vector<Slot> old;
+      old.swap(slots_);
+      slots_.assign(old.size() * 2, Slot{});
+      for (const Slot& s : old)
+        if (s.node) put(s.node);
+    }
+    std::vector<Slot> slots_;
+    size_t used_ = 0;
+  };
 
   void drop_from_sets(Node* n) {
     if (n->in_leaf) {
@@ -390,7 +472,11 @@ class Index {
 
   int B_;
   Node root_;
-  std::unordered_multimap<uint64_t, Node*> map_;
+  ChildTable map_;
+  uint64_t unlinks_ = 0;  // bumps invalidate the memo
+  mutable std::vector<int32_t> memo_toks_;
+  mutable std::vector<Node*> memo_nodes_;
+  mutable uint64_t memo_unlinks_ = ~0ull;
   std::set<Key> leaves_[2];
   std::set<Key> front_;
   std::vector<Node*> owner_[2];

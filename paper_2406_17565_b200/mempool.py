@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libmempool.so")
 
 HBM, DRAM, MIXED = 0, 1, 2
+ALLOC_STREAM_ORDERED = 1 << 8
 
 XFER_DST_GIVEN = 1 << 0
 XFER_DEDUP = 1 << 1
@@ -277,10 +278,14 @@ class Pool:
         return o
 
     # -------------------------------------------------------------- memory API
-    def alloc_mem(self, n: int, medium: int = HBM, requester: int = None) -> np.ndarray:
+    def alloc_mem(self, n: int, medium: int = HBM, requester: int = None,
+                  stream_ordered: bool = False) -> np.ndarray:
+        """stream_ordered: no drain; order the caller's writes after an event
+        from record_event (MP_ALLOC_STREAM_ORDERED, include/mempool.h)."""
         out = np.zeros(max(n, 1), np.uint64)
         req = self.inst if requester is None else requester
-        _check(_lib.mp_alloc_mem(self._h, n, medium, req, _pu64(out)), "alloc_mem")
+        t = medium | (ALLOC_STREAM_ORDERED if stream_ordered else 0)
+        _check(_lib.mp_alloc_mem(self._h, n, t, req, _pu64(out)), "alloc_mem")
         return out[:n]
 
     def free_mem(self, addrs):

@@ -1,0 +1,208 @@
+#!/usr/bin/env python
+"""BASELINE.json configs[2] and configs[3] measured on one B200 (P and D as two
+pools on cuda:0, loopback wire), same conventions as bench.py (CUDA events
+around K sessions, the library's per-launch kernel timing, clocks sampled).
+
+  loogle  configs[2]: Llama-2-13B KV (Pb = 12.5 MiB), LooGLE-like sessions --
+          a 16-32K-token document and 5 questions; PD-Caching-2: every
+          turn P -> D transfer_with_insert with DEDUP, so turn 1 moves the
+          document (1024-2048 blocks, 12.5-25 GiB) and turns 2-5 only their
+          new blocks.
+  react   configs[3]: Llama-2-13B KV, ReAct-like sessions -- a shared 1536-token
+          two-shot prefix, 3-6 steps of long generation;
+          PD-Caching-3: P -> D (DEDUP) of the prompt, D appends the generated
+          blocks, D -> P transfer_with_insert returns them (the suffix from
+          block floor(prompt/B) on, R3).
+
+value = payload bytes moved in both directions / time.  Prefill / decode
+compute is out of scope (no model): blocks are allocated and indexed by the
+stand-in engine steps, their KV bytes are whatever the pool holds.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from bench import Clocks, load_peaks, make_pool  # noqa: E402
+from paper_2406_17565_b200 import mempool as M  # noqa: E402
+from workloads import traces  # noqa: E402
+from workloads.configs import LLAMA2_13B, seed_for  # noqa: E402
+
+S = LLAMA2_13B
+B = S.block_tokens
+FLAGS = M.XFER_DEDUP | M.XFER_ASYNC
+STREAM_ORDERED = True
+
+
+class Timed:
+    """Proxy accumulating host time per pool method (--phase-times)."""
+    acc = {}
+
+    def __init__(self, pool):
+        self._p = pool
+
+    def __getattr__(self, name):
+        f = getattr(self._p, name)
+        if not callable(f):
+            return f
+
+        def w(*a, **k):
+            t0 = time.perf_counter()
+            r = f(*a, **k)
+            d = Timed.acc.setdefault(name, [0, 0.0])
+            d[0] += 1
+            d[1] += time.perf_counter() - t0
+            return r
+        return w
+
+
+_EV = None
+
+
+def prefill(P, prompt):
+    """Engine stand-in: match, allocate the rest (stream-ordered: the engine's
+    stream waits on the pool's event before it would write the KV), retire
+    the full blocks."""
+    _, m = P.match(prompt)
+    new = P.alloc_mem(-(-len(prompt) // B) - len(m), stream_ordered=STREAM_ORDERED)
+    if STREAM_ORDERED:
+        global _EV
+        if _EV is None:
+            _EV = (torch.cuda.Event(), torch.cuda.current_stream())
+        P.record_event(_EV[0])
+        _EV[1].wait_event(_EV[0])
+    full = np.concatenate([m, new])
+    P.insert(prompt, full[: len(prompt) // B])
+    return full
+
+
+def loogle_session(P, D, sess):
+    moved = 0
+    prompts = []
+    for t in sess.turns:
+        src = prefill(P, t.prompt)
+        final, nm = P.transfer_with_insert(D.inst, t.prompt, src, flags=FLAGS)
+        moved += nm
+        prompts.append((t.prompt, src[len(t.prompt) // B:], final[len(t.prompt) // B:]))
+    for prompt, p_part, d_part in prompts:       # the session ends: both sides retire it
+        P.free_mem(p_part)
+        D.free_mem(d_part)
+        P.delete(prompt)
+        D.delete(prompt)
+    return moved
+
+
+def react_session(P, D, sess):
+    moved = 0
+    retire = []
+    for t in sess.turns:
+        src = prefill(P, t.prompt)
+        fin_d, nm = P.transfer_with_insert(D.inst, t.prompt, src, flags=FLAGS)
+        moved += nm
+        whole = np.concatenate([t.prompt, t.gen])
+        k = len(t.prompt) // B
+        D.free_mem(fin_d[k:])                                 # the prompt's partial block
+        d_addrs = prefill(D, whole)                           # decode appends blocks
+        _, nm2 = D.transfer_with_insert(P.inst, whole, d_addrs[k:], flags=M.XFER_ASYNC)
+        moved += nm2
+        D.free_mem(d_addrs[len(whole) // B:])
+        P.free_mem(src[k:])
+        retire.append(whole)
+    for whole in retire:
+        P.delete(whole)
+        D.delete(whole)
+    return moved
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("workload", choices=["loogle", "react"])
+    ap.add_argument("--sessions", type=int, default=0)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--pool-blocks", type=int, default=4096)
+    ap.add_argument("--drain-alloc", action="store_true",
+                    help="engine allocations drain the pool (no MP_ALLOC_STREAM_ORDERED)")
+    ap.add_argument("--phase-times", action="store_true",
+                    help="host time per pool method in the timed loop (stderr)")
+    ap.add_argument("--prof", action="store_true", help="cProfile the timed loop (stderr)")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    global STREAM_ORDERED
+    STREAM_ORDERED = not args.drain_alloc
+    idx = 2 if args.workload == "loogle" else 3
+    seed = seed_for(idx)
+    if args.workload == "loogle":
+        sessions = traces.loogle_like(seed, n_sessions=args.sessions or 8)
+        fn = loogle_session
+    else:
+        sessions = traces.react_like(seed, n_sessions=args.sessions or 32)
+        fn = react_session
+    P = make_pool(M, torch, 0, 0, S, args.pool_blocks)
+    D = make_pool(M, torch, 1, 0, S, args.pool_blocks)
+    M.connect(P, D)
+    clocks = Clocks("/tmp/clocks_wl.csv", 0)
+    with clocks:
+        time.sleep(1.0)
+        for s in sessions[: args.warmup]:
+            fn(P, D, s)
+        for x in (P, D):
+            x.sync()
+            x.stats_reset()
+            x.profile(True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h0 = time.perf_counter()
+        if args.prof:
+            import cProfile
+            import pstats
+            pr = cProfile.Profile()
+            pr.enable()
+        if args.phase_times:
+            moved = sum(fn(Timed(P), Timed(D), s) for s in sessions)
+            for k, (n, t) in sorted(Timed.acc.items(), key=lambda kv: -kv[1][1]):
+                print(f"{k:24s} calls {n:5d}  total {t * 1e3:8.3f} ms  per call {t / n * 1e6:7.1f} us",
+                      file=sys.stderr)
+        else:
+            moved = sum(fn(P, D, s) for s in sessions)
+        if args.prof:
+            pr.disable()
+            pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(15)
+        host_ms = (time.perf_counter() - h0) * 1e3
+        for x in (P, D):
+            x.sync()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    st = [x.stats() for x in (P, D)]
+    kms = sum(s["kernel_ms"] for s in st)
+    kl = sum(s["timed_launches"] for s in st)
+    kb = sum(s["timed_bytes"] for s in st)
+    peak, src = load_peaks()
+    ach = 2 * kb / (kms * 1e-3) / 1e9 if kms else None
+    print(json.dumps({
+        "metric": "KV migration GB/s (payload, both directions)",
+        "workload": f"configs[{idx}] {args.workload}-like, Llama-2-13B KV (Pb = 12.5 MiB), "
+                    f"{len(sessions)} sessions, one B200 (P, D loopback)",
+        "value": round(moved * S.block_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+        "blocks_per_s": round(moved / (ms * 1e-3), 1), "blocks_moved": int(moved),
+        "ms": round(ms, 3),
+        "roofline": {"bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
+                     "peak_source": src, "frac": round(ach / peak, 4) if ach else None,
+                     "launches": kl, "share_of_time": round(kms / ms, 4),
+                     "idle_between_launches_share": round(sum(s["gap_ms"] for s in st) / ms, 4),
+                     "host_ms": round(host_ms, 3)},
+        "engine_alloc": "drain" if args.drain_alloc else "stream_ordered",
+        "clocks": clocks.summary()}))
+
+
+if __name__ == "__main__":
+    main()

@@ -148,7 +148,8 @@ def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coa
                 # engine-style prefill: match, alloc the rest, fill, insert
                 t = gen()
                 mt, matched = X.match(t)
-                new = X.alloc(-(-len(t) // B) - len(matched))
+                new = X.alloc(-(-len(t) // B) - len(matched),
+                              stream_ordered=bool(path & M.XFER_ASYNC) and rng.random() < 0.5)
                 X.fill(new)
                 X.insert(t, (matched + new)[: len(t) // B])
                 seqs.append(t)

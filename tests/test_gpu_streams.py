@@ -48,3 +48,46 @@ def test_layer_by_layer_waits_for_engine_stream():
         assert (got[j] == 10 * (j // 2) + j % 2 + 1).all(), f"chunk {j} copied stale KV"
     P.close()
     D.close()
+
+
+def test_stream_ordered_alloc_reuses_block_still_being_read():
+    """MP_ALLOC_STREAM_ORDERED: a block freed while an ASYNC transfer still
+    reads it comes straight back (lowest-first, same ids as a draining alloc);
+    the engine's write, ordered after mp_record_event, must not reach the
+    receiver's copy."""
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    from workloads.configs import KVShape
+    shape = KVShape("s", 4, 4, 64, 16)
+    P, pr = _pool(M, torch, 0, shape, 16)
+    D, dr = _pool(M, torch, 1, shape, 16)
+    M.connect(P, D)
+    src = P.alloc_mem(3)
+    sid = torch.as_tensor(M.addr_indices(src), device="cuda:0")
+    pr[:, sid] = 7
+    torch.cuda.synchronize()
+    gate = torch.cuda.Event()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)               # hold the copy back on the device
+        gate.record(side)
+    P.wait_event(gate)
+    dst = P.transfer(1, src, flags=M.XFER_ASYNC)
+    P.free_mem(src)
+    again = P.alloc_mem(3, stream_ordered=True)
+    assert list(M.addr_indices(again)) == list(M.addr_indices(src))
+    ready = torch.cuda.Event()
+    P.record_event(ready)
+    engine = torch.cuda.Stream()
+    engine.wait_event(ready)
+    with torch.cuda.stream(engine):
+        pr[:, sid] = 99                              # the new owner's KV write
+    landed = torch.cuda.Event()
+    D.record_event(landed)
+    torch.cuda.current_stream().wait_event(landed)
+    torch.cuda.current_stream().wait_stream(engine)
+    did = torch.as_tensor(M.addr_indices(dst), device="cuda:0")
+    assert (dr[:, did] == 7).all(), "receiver copied the new owner's bytes"
+    assert (pr[:, sid] == 99).all()
+    P.close()
+    D.close()

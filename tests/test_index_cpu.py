@@ -160,7 +160,14 @@ def run(L, seed, B, n_ops):
         L.ix_free(h)
 
 
-@pytest.mark.parametrize("B", [8, 16])
+@pytest.mark.parametrize("B", [8, 16, 32])
 def test_index_vs_oracle(lib, B):
     for seed in range(25):
         run(lib, 1000 * B + seed, B, 60)
+
+
+def test_index_long_runs(lib):
+    """Long op sequences: the child table grows past its initial size and the
+    path memo is invalidated by many deletes / evictions in between."""
+    for seed in range(2):
+        run(lib, 77 + seed, 8, 250)

@@ -62,9 +62,12 @@ class Twin:
             raise O.MPError(oerr)
         return ores, conv(gres)
 
-    def alloc(self, n, medium=O.HBM, requester=None):
-        o, g = self.call(self.o.alloc_mem, self.g.alloc_mem, (n, medium, requester),
-                         (n, medium, requester), to_o)
+    def alloc(self, n, medium=O.HBM, requester=None, stream_ordered=False):
+        """stream_ordered (MP_ALLOC_STREAM_ORDERED) changes no result, only
+        whether the GPU pool drains first; fills are pool-stream ordered."""
+        o, g = self.call(self.o.alloc_mem,
+                         lambda *a: self.g.alloc_mem(*a, stream_ordered=stream_ordered),
+                         (n, medium, requester), (n, medium, requester), to_o)
         assert o == g, (o, g)
         return o
 
