@@ -38,6 +38,8 @@ from workloads import traces  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback
+NOMINAL_HBM_GBS = 7700.0    # B200_PROFILING.md: HBM3e 7.7 TB/s (HGX figure); the measured
+                            # peak above is torch's contiguous copy_, which the ring beats
 NVLINK_GBS = 900.0          # nominal per direction per GPU (BJ:5)
 NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction
 METRIC = "KV migration GB/s (P->D transfer_with_insert payload)"
@@ -331,6 +333,9 @@ def run_ours(args, rank, world, dist):
     roof.update({
         "achieved": round(achieved, 1) if achieved else None, "unit": "GB/s",
         "frac": round(achieved / roof["peak"], 4) if achieved else None,
+        "nominal_peak": NOMINAL_HBM_GBS if role.kind == "PD" else NVLINK_GBS,
+        "frac_of_nominal": (round(achieved / (NOMINAL_HBM_GBS if role.kind == "PD" else NVLINK_GBS), 4)
+                            if achieved else None),
         "traffic": round(ratio * alg) if ratio else None,
         "traffic_note": (f"dram read+write per launch = {ratio} x algorithmic, from the ncu "
                          f"capture {ratio_src} (writes still in L2 at kernel end are not "

@@ -162,48 +162,77 @@ __device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& d
   *bytes = (uint32_t)(rest < kPieceT ? rest : kPieceT);
 }
 
+// Work distribution: static round-robin (unit u_k = blockIdx.x + k*gridDim.x)
+// or, with a device counter, dynamic -- each CTA claims its next unit with
+// one atomicAdd issued a full ring turn before the unit is needed, so SMs
+// that see slower HBM (the far die) simply take fewer units and the launch
+// ends when the LAST unit lands, not when the slowest static share does.  The
+// counter is never reset: the launch is given its start value (`base`), and
+// every CTA makes exactly one failing claim, so the host advances base by
+// total + grid per launch (launches on one stream are serialised).
+struct UnitSource {
+  unsigned long long* ctr;
+  unsigned long long base;
+  unsigned total, next, stride;
+  __device__ __forceinline__ unsigned claim() {
+    if (ctr) {
+      const unsigned long long g = atomicAdd(ctr, 1ull) - base;
+      return g < total ? (unsigned)g : 0xFFFFFFFFu;
+    }
+    const unsigned u = next;
+    next += stride;
+    return u < total ? u : 0xFFFFFFFFu;
+  }
+};
+
 template <int kPiece, int kStages, bool kSrcPool, bool kDstPool>
-__global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(Endpoint src, Endpoint dst,
-                                                                    int j0, int nj,
-                                                                    long long chunk,
-                                                                    unsigned pieces_per_chunk,
-                                                                    unsigned total_units) {
+__global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
+    Endpoint src, Endpoint dst, int j0, int nj, long long chunk, unsigned pieces_per_chunk,
+    unsigned total_units, unsigned long long* ctr, unsigned long long base) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   if (threadIdx.x != 0) return;
   for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  // units of this CTA: u_k = blockIdx.x + k * gridDim.x
-  const unsigned n_mine =
-      blockIdx.x < total_units ? (total_units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  UnitSource units{ctr, base, total_units, blockIdx.x, gridDim.x};
   const char* sp;
   char* dp;
   uint32_t bytes;
   char* dsts[kStages];
   uint32_t lens[kStages];
-  for (unsigned k = 0; k < n_mine && k < (unsigned)kStages; ++k) {
-    unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
-                                          blockIdx.x + k * gridDim.x, &sp, &dp, &bytes);
+  bool live[kStages];
+  // prime the ring
+  unsigned u = units.claim();
+  for (int k = 0; k < kStages; ++k) {
+    live[k] = u != 0xFFFFFFFFu;
+    if (!live[k]) continue;
+    unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk, u, &sp, &dp,
+                                          &bytes);
     dsts[k] = dp;
     lens[k] = bytes;
     mbar_expect_tx(&bars[k], bytes);
     bulk_load(smem + (size_t)k * kPiece, sp, bytes, &bars[k]);
+    u = units.claim();  // in flight while the loads are
   }
-  for (unsigned k = 0; k < n_mine; ++k) {
+  // consume stage k % kStages; refill the stage the previous store read from
+  for (unsigned k = 0;; ++k) {
     const unsigned s = k % kStages;
+    if (!live[s]) break;
     mbar_wait(&bars[s], (k / kStages) & 1u);
     bulk_store(dsts[s], smem + (size_t)s * kPiece, lens[s]);
-    // refill the stage the previous store used, once that store has read it
-    if (k >= 1 && k - 1 + kStages < n_mine) {
-      bulk_wait_read<1>();
+    if (k >= 1) {
       const unsigned r = (k - 1) % kStages;
-      unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk,
-                                            blockIdx.x + (k - 1 + kStages) * gridDim.x, &sp,
-                                            &dp, &bytes);
-      dsts[r] = dp;
-      lens[r] = bytes;
-      mbar_expect_tx(&bars[r], bytes);
-      bulk_load(smem + (size_t)r * kPiece, sp, bytes, &bars[r]);
+      live[r] = u != 0xFFFFFFFFu;
+      if (live[r]) {
+        bulk_wait_read<1>();
+        unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk, u, &sp,
+                                              &dp, &bytes);
+        dsts[r] = dp;
+        lens[r] = bytes;
+        mbar_expect_tx(&bars[r], bytes);
+        bulk_load(smem + (size_t)r * kPiece, sp, bytes, &bars[r]);
+        u = units.claim();
+      }
     }
   }
   bulk_wait_all();
@@ -305,9 +334,20 @@ int sm_count(int device) {
   return v > 0 ? v : 148;
 }
 
+// MP_BULK_SCHED=static turns the dynamic unit claiming off (comparison knob).
+static bool bulk_dynamic() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MP_BULK_SCHED");
+    v = (e && e[0] == 's') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int kPieceT, int kStagesT, bool kSrcPool, bool kDstPool>
 static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
-                               long long chunk, int max_ctas, cudaStream_t stream) {
+                               long long chunk, int max_ctas, cudaStream_t stream,
+                               const Sched* sched) {
   auto kern = migrate_bulk_kernel<kPieceT, kStagesT, kSrcPool, kDstPool>;
   const unsigned pieces = (unsigned)((chunk + kPieceT - 1) / kPieceT);
   const unsigned long long total = (unsigned long long)n * nj * pieces;
@@ -328,25 +368,32 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
     cap = cached_cap[dev];
   }
   const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
-  kern<<<grid, kBulkThreads, smem, stream>>>(src, dst, j0, nj, chunk, pieces, (unsigned)total);
-  return cudaGetLastError();
+  const bool dyn = sched && sched->ctr && bulk_dynamic();
+  kern<<<grid, kBulkThreads, smem, stream>>>(src, dst, j0, nj, chunk, pieces, (unsigned)total,
+                                             dyn ? sched->ctr : nullptr, dyn ? *sched->base : 0);
+  const cudaError_t e = cudaGetLastError();
+  if (dyn && e == cudaSuccess) *sched->base += total + (unsigned long long)grid;
+  return e;
 }
 
 template <int kPieceT, int kStagesT>
 static cudaError_t launch_bulk_any(const Endpoint& src, const Endpoint& dst, int n, int j0,
-                                   int nj, long long chunk, int max_ctas, cudaStream_t stream) {
+                                   int nj, long long chunk, int max_ctas, cudaStream_t stream,
+                                   const Sched* sc) {
   const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
   if (sp && dp)
-    return launch_bulk<kPieceT, kStagesT, true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+    return launch_bulk<kPieceT, kStagesT, true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream,
+                                                      sc);
   if (sp)
     return launch_bulk<kPieceT, kStagesT, true, false>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                       stream);
+                                                       stream, sc);
   if (dp)
     return launch_bulk<kPieceT, kStagesT, false, true>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                       stream);
+                                                       stream, sc);
   return launch_bulk<kPieceT, kStagesT, false, false>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                      stream);
+                                                      stream, sc);
 }
+
 
 // Ring geometry of the bulk engine; MP_BULK_CFG=<0..5> selects one (tuning
 // knob, read once).  Measured on B200 (profiles/kernel_sweep_r01.jsonl):
@@ -365,16 +412,17 @@ static int bulk_cfg() {
 }
 
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
-                           long long chunk, int max_ctas, cudaStream_t stream, int variant) {
+                           long long chunk, int max_ctas, cudaStream_t stream, int variant,
+                           const Sched* sched) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
   if (variant == kCopyBulk) {
     switch (bulk_cfg()) {
-      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream);
-      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream);
+      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
+      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
+      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
+      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
+      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
+      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
     }
   }
   const unsigned units_per_chunk = (unsigned)((chunk + kUnitBytes - 1) / kUnitBytes);

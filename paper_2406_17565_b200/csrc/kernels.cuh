@@ -26,6 +26,14 @@ struct Endpoint {
   long long off;       // byte offset of the copied range inside each chunk
 };
 
+// Dynamic work distribution of the bulk engine: a device counter of the
+// launching stream plus the host's running start value for it (advanced by
+// the launcher; launches sharing a counter must be stream-serialised).
+struct Sched {
+  unsigned long long* ctr;
+  unsigned long long* base;
+};
+
 // Copy engines of the migration kernel.
 enum CopyVariant { kCopyAuto = 0, kCopyVector = 1, kCopyBulk = 2 };
 
@@ -35,8 +43,10 @@ enum CopyVariant { kCopyAuto = 0, kCopyVector = 1, kCopyBulk = 2 };
 // variant kCopyVector: 16-byte vector loads/stores by every lane;
 // kCopyBulk: cp.async.bulk (TMA engine) ring through shared memory.
 // max_ctas <= 0: one full wave (occupancy x SMs).
+// sched (nullable, bulk only): claim units dynamically instead of statically.
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
-                           long long len, int max_ctas, cudaStream_t stream, int variant);
+                           long long len, int max_ctas, cudaStream_t stream, int variant,
+                           const Sched* sched = nullptr);
 
 // Lowest-first allocation of n blocks from a bitmap (bit = 1: free).  Writes
 // the ids ascending into out_dev (device) and out_host (mapped pinned host,

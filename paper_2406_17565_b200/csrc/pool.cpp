@@ -334,7 +334,9 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
   int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyBulk : p->copy_kernel;
   if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
-  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant));
+  const mpk::Sched sched{p->d_sched, &p->sched_base};
+  CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant,
+                         s == p->stream ? &sched : nullptr));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});
@@ -399,6 +401,7 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->d_slabs) cudaFree(p->d_slabs);
     if (p->d_bitmap) cudaFree(p->d_bitmap);
     if (p->d_err) cudaFree(p->d_err);
+    if (p->d_sched) cudaFree(p->d_sched);
     if (p->ar.d) cudaFree(p->ar.d);
     if (p->bsrc) cudaFree(p->bsrc);
     if (p->bdst) cudaFree(p->bdst);
@@ -531,6 +534,8 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   CKC(cudaMemcpy(p->d_bitmap, bm.data(), sizeof(uint32_t) * p->nwords, cudaMemcpyHostToDevice));
   CKC(cudaMalloc(&p->d_err, sizeof(int)));
   CKC(cudaMemset(p->d_err, 0, sizeof(int)));
+  CKC(cudaMalloc(&p->d_sched, sizeof(unsigned long long)));
+  CKC(cudaMemset(p->d_sched, 0, sizeof(unsigned long long)));
   p->ar.cap = 16 * std::max<int64_t>(std::max(p->n_hbm, p->n_dram), 4096);
   CKC(cudaMalloc(&p->ar.d, sizeof(int) * p->ar.cap));
   p->coalesce = cfg->coalesce_mib >= 0;

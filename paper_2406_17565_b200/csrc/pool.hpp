@@ -144,6 +144,9 @@ struct mp_pool {
   uint32_t* d_bitmap = nullptr;
   int nwords = 0;
   int* d_err = nullptr;
+  // dynamic unit claiming of bulk launches on `stream` (kernels.cuh Sched)
+  unsigned long long* d_sched = nullptr;
+  unsigned long long sched_base = 0;
   mp::Arena ar;
   char* dram = nullptr;      // host pointer of the pinned DRAM pool
   char* dram_dev = nullptr;  // device-visible (mapped) pointer

@@ -2,7 +2,9 @@
 the key counters of a --set full capture.  Usage:
   python scripts/ncu_summary.py launches <launches.csv>
   python scripts/ncu_summary.py full <prof.ncu-rep>
+  python scripts/ncu_summary.py traffic <out.json> vector=<rep> bulk=<rep> [note]
 """
+import json
 import collections
 import csv
 import io
@@ -46,5 +48,59 @@ def full(path):
                 print(f"  {k:60s} {r[i]:>16s} {units[i]}")
 
 
+def _raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    return [dict(zip(hdr, r)) for r in rows[2:]], dict(zip(hdr, units))
+
+
+def _mb(v, unit):
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[unit]
+    return float(v.replace(",", "")) * scale
+
+
+def _us(v, unit):
+    return float(v.replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[unit]
+
+
+def traffic(out_path, *specs):
+    """DRAM traffic vs the algorithmic bytes of every captured migrate launch:
+    algorithmic = what the kernel requested (L2 sectors from the SMs, read +
+    write: lts__t_sectors_srcunit_tex_op_{read,write} x 32 B = 2 x payload);
+    traffic = dram__bytes_{read,write}."""
+    res = {"source": " ".join(a for a in specs if "=" not in a) or
+           "ncu --set full --clock-control none, bench.py --steps 2 (one transfer_with_insert per "
+           "launch under ncu's serialisation)"}
+    for spec in specs:
+        if "=" not in spec:
+            continue
+        label, path = spec.split("=", 1)
+        rows, units = _raw(path)
+        lst = []
+        for r in rows:
+            rd = _mb(r["dram__bytes_read.sum"], units["dram__bytes_read.sum"])
+            wr = _mb(r["dram__bytes_write.sum"], units["dram__bytes_write.sum"])
+            # bytes the kernel itself requested from L2 (TMA / LSU), read + write
+            tr = float(r["lts__t_sectors_srcunit_tex_op_read.sum"].replace(",", "")) * 32e-6
+            tw = float(r["lts__t_sectors_srcunit_tex_op_write.sum"].replace(",", "")) * 32e-6
+            alg = tr + tw
+            lst.append({"kernel": r.get("Kernel Name", "?")[:60],
+                        "duration_us": _us(r["gpu__time_duration.sum"],
+                                           units["gpu__time_duration.sum"]),
+                        "dram_read_MB": rd, "dram_write_MB": wr, "algorithmic_MB": round(alg, 3),
+                        "sm_read_MB": round(tr, 3), "sm_write_MB": round(tw, 3),
+                        "traffic_MB": rd + wr,
+                        "traffic_over_algorithmic": round((rd + wr) / alg, 4)})
+        res[label] = lst
+    with open(out_path, "w") as f:
+        json.dump(res, f, indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "traffic":
+        traffic(*sys.argv[2:])
+        sys.exit(0)
     {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
