@@ -30,27 +30,92 @@
 
 namespace mpi {
 
+// Hot fields of a walk / touch first: line 0 holds the links and R7/R8/R12
+// state, line 1 the block's tokens (B <= 16); the rest is touched rarely.
 struct Node {
   Node* parent = nullptr;
   std::vector<Node*> kids;       // children (any medium)
-  int32_t pos_in_parent = -1;    // index in parent->kids
-  int32_t small[16];             // the B tokens of this block (inline when B <= 16)
-  std::vector<int32_t> big;      //   (heap when B > 16)
-  const int32_t* chunk() const { return big.empty() ? small : big.data(); }
-  uint64_t hkey = 0;             // key in the child hash map
-  int32_t medium = 0, idx = -1;  // where the KV block lives (P:328 "anywhere")
   uint64_t last_access = 0;      // R7
   int32_t ref = 0;               // R12 pins
-  bool terminal = false;         // R6
+  int32_t medium = 0, idx = -1;  // where the KV block lives (P:328 "anywhere")
   int32_t n_hbm_kids = 0;
+  bool terminal = false;         // R6
+  bool in_leaf = false, in_front = false;  // membership in the candidate sets
+  int32_t small[16];             // the B tokens of this block (inline when B <= 16)
+  std::vector<int32_t> big;      //   (heap when B > 16)
+  const int32_t* chunk(int B) const { return B <= 16 ? small : big.data(); }
+  uint64_t hkey = 0;             // key in the child hash map
   uint64_t id = 0;
-  // membership in the candidate sets
-  bool in_leaf = false, in_front = false;
+  int32_t pos_in_parent = -1;    // index in parent->kids
   int32_t leaf_medium = 0;
   std::pair<uint64_t, int32_t> leaf_key{0, 0}, front_key{0, 0};
+  int32_t leaf_pos = -1, front_pos = -1;  // slots in the candidate heaps
+  // scratch of evictable_at_least (generation-stamped, no clearing)
+  uint64_t peel_gen = 0, pin_gen = 0;
+  int64_t peel_left = 0;
 };
 
 using Key = std::pair<uint64_t, int32_t>;  // (last_access, block index)
+
+// Binary min-heap of nodes by a Key member, each node knowing its slot, so a
+// candidate set supports min / insert / erase / re-key in O(log n) without
+// allocating (eviction of a long chain re-keys one parent per step).
+template <Key Node::*kKey, int32_t Node::*kPos>
+class NodeHeap {
+ public:
+  bool empty() const { return a_.empty(); }
+  size_t size() const { return a_.size(); }
+  Node* top() const { return a_.front(); }
+  const std::vector<Node*>& items() const { return a_; }
+  void clear() {
+    for (Node* n : a_) n->*kPos = -1;
+    a_.clear();
+  }
+  void push(Node* n) {
+    n->*kPos = (int32_t)a_.size();
+    a_.push_back(n);
+    up((size_t)(n->*kPos));
+  }
+  void erase(Node* n) {
+    const size_t i = (size_t)(n->*kPos);
+    Node* last = a_.back();
+    a_.pop_back();
+    n->*kPos = -1;
+    if (i < a_.size()) {
+      a_[i] = last;
+      last->*kPos = (int32_t)i;
+      fix(i);
+    }
+  }
+  void rekey(Node* n) { fix((size_t)(n->*kPos)); }
+
+ private:
+  bool less(size_t i, size_t j) const { return a_[i]->*kKey < a_[j]->*kKey; }
+  void swap_at(size_t i, size_t j) {
+    std::swap(a_[i], a_[j]);
+    a_[i]->*kPos = (int32_t)i;
+    a_[j]->*kPos = (int32_t)j;
+  }
+  void up(size_t i) {
+    while (i > 0 && less(i, (i - 1) / 2)) {
+      swap_at(i, (i - 1) / 2);
+      i = (i - 1) / 2;
+    }
+  }
+  void fix(size_t i) {
+    up(i);
+    for (;;) {
+      size_t m = i;
+      const size_t l = 2 * i + 1, r = l + 1;
+      if (l < a_.size() && less(l, m)) m = l;
+      if (r < a_.size() && less(r, m)) m = r;
+      if (m == i) return;
+      swap_at(i, m);
+      i = m;
+    }
+  }
+  std::vector<Node*> a_;
+};
 
 class Index {
  public:
@@ -270,12 +335,52 @@ class Index {
   // R8: least (last_access, idx) leaf of `medium` with ref == 0, or nullptr.
   Node* lru_leaf(int medium) const {
     if (leaves_[medium].empty()) return nullptr;
-    return owner_[medium][(size_t)leaves_[medium].begin()->second];
+    return leaves_[medium].top();
   }
   // R9: least (last_access, idx) HBM node with ref == 0 and no HBM child.
   Node* lru_frontier() const {
     if (front_.empty()) return nullptr;
-    return owner_[0][(size_t)front_.begin()->second];
+    return front_.top();
+  }
+
+  // Current R8 candidates of `medium` (unpinned leaves), minus those on
+  // `pinned_path`: a lower bound of evictable(), O(|pinned_path|).
+  int64_t evictable_leaves(int medium, const std::vector<Node*>& pinned_path) const {
+    int64_t n = (int64_t)leaves_[medium].size();
+    for (const Node* p : pinned_path)
+      if (p->in_leaf && p->leaf_medium == medium) --n;
+    return n;
+  }
+
+  // evictable(medium, pinned_path) >= need, in O(need + |pinned_path| +
+  // candidate leaves) instead of a walk of the whole tree: peel the tree from
+  // its unpinned leaves upwards (a parent joins once all its children have
+  // been peeled and it is an unpinned node of `medium` -- exactly the closure
+  // evictable() counts) and stop at `need`.
+  bool evictable_at_least(int medium, const std::vector<Node*>& pinned_path, int64_t need) {
+    if (need <= 0) return true;
+    const uint64_t g = ++peel_gen_;
+    for (Node* p : pinned_path) p->pin_gen = g;
+    int64_t count = 0;
+    std::vector<Node*> stack;
+    for (Node* leaf : leaves_[medium].items()) {
+      if (leaf->pin_gen == g) continue;
+      stack.push_back(leaf);
+      while (!stack.empty()) {
+        Node* n = stack.back();
+        stack.pop_back();
+        if (++count >= need) return true;
+        Node* par = n->parent;
+        if (par == &root_) continue;
+        if (par->peel_gen != g) {
+          par->peel_gen = g;
+          par->peel_left = (int64_t)par->kids.size();
+        }
+        if (--par->peel_left == 0 && par->medium == medium && par->ref == 0 && par->pin_gen != g)
+          stack.push_back(par);
+      }
+    }
+    return false;
   }
 
   // Number of nodes of `medium` that repeated leaf eviction could remove:
@@ -314,7 +419,7 @@ class Index {
     while (!stack.empty()) {
       auto [n, pre] = stack.back();
       stack.pop_back();
-      pre.insert(pre.end(), n->chunk(), n->chunk() + B_);
+      pre.insert(pre.end(), n->chunk(B_), n->chunk(B_) + B_);
       std::string line = std::to_string(pre.size() / (size_t)B_) + "\t" + std::to_string(n->medium) +
                          "\t" + std::to_string(n->idx) + "\t" + std::to_string(n->last_access) +
                          "\t" + std::to_string(n->ref) + "\t" + (n->terminal ? "1" : "0") + "\t";
@@ -334,6 +439,9 @@ class Index {
   }
 
   void clear() {
+    leaves_[0].clear();  // before the nodes go (the heaps reset their slots)
+    leaves_[1].clear();
+    front_.clear();
     std::vector<Node*> stack(root_.kids.begin(), root_.kids.end());
     while (!stack.empty()) {
       Node* n = stack.back();
@@ -345,9 +453,6 @@ class Index {
     root_.n_hbm_kids = 0;
     map_.clear();
     ++unlinks_;
-    leaves_[0].clear();
-    leaves_[1].clear();
-    front_.clear();
     for (auto& o : owner_) std::fill(o.begin(), o.end(), nullptr);
     size_ = 0;
   }
@@ -415,7 +520,7 @@ class Index {
       for (size_t i = (size_t)key & mask; slots_[i].node; i = (i + 1) & mask) {
         const Slot& s = slots_[i];
         if (s.key == key && s.node->parent == parent &&
-            std::memcmp(s.node->chunk(), toks, sizeof(int32_t) * (size_t)B) == 0)
+            std::memcmp(s.node->chunk(B), toks, sizeof(int32_t) * (size_t)B) == 0)
           return s.node;
       }
       return nullptr;
@@ -445,28 +550,49 @@ class Index {
 
   void drop_from_sets(Node* n) {
     if (n->in_leaf) {
-      leaves_[n->leaf_medium].erase(n->leaf_key);
+      leaves_[n->leaf_medium].erase(n);
       n->in_leaf = false;
     }
     if (n->in_front) {
-      front_.erase(n->front_key);
+      front_.erase(n);
       n->in_front = false;
     }
   }
 
+  // Re-derive n's membership and keys in the R8 / R9 candidate sets.
   void refresh(Node* n) {
     if (n == &root_) return;
-    drop_from_sets(n);
-    if (n->ref == 0 && n->kids.empty()) {
-      n->leaf_key = {n->last_access, n->idx};
-      n->leaf_medium = n->medium;
-      leaves_[n->medium].insert(n->leaf_key);
-      n->in_leaf = true;
+    const Key k{n->last_access, n->idx};
+    const bool leaf = n->ref == 0 && n->kids.empty();
+    if (n->in_leaf && (!leaf || n->leaf_medium != n->medium)) {
+      leaves_[n->leaf_medium].erase(n);
+      n->in_leaf = false;
     }
-    if (n->ref == 0 && n->medium == 0 && n->n_hbm_kids == 0) {
-      n->front_key = {n->last_access, n->idx};
-      front_.insert(n->front_key);
-      n->in_front = true;
+    if (leaf) {
+      if (!n->in_leaf) {
+        n->leaf_key = k;
+        n->leaf_medium = n->medium;
+        leaves_[n->medium].push(n);
+        n->in_leaf = true;
+      } else if (n->leaf_key != k) {
+        n->leaf_key = k;
+        leaves_[n->medium].rekey(n);
+      }
+    }
+    const bool front = n->ref == 0 && n->medium == 0 && n->n_hbm_kids == 0;
+    if (n->in_front && !front) {
+      front_.erase(n);
+      n->in_front = false;
+    }
+    if (front) {
+      if (!n->in_front) {
+        n->front_key = k;
+        front_.push(n);
+        n->in_front = true;
+      } else if (n->front_key != k) {
+        n->front_key = k;
+        front_.rekey(n);
+      }
     }
   }
 
@@ -474,11 +600,12 @@ class Index {
   Node root_;
   ChildTable map_;
   uint64_t unlinks_ = 0;  // bumps invalidate the memo
+  uint64_t peel_gen_ = 0;
   mutable std::vector<int32_t> memo_toks_;
   mutable std::vector<Node*> memo_nodes_;
   mutable uint64_t memo_unlinks_ = ~0ull;
-  std::set<Key> leaves_[2];
-  std::set<Key> front_;
+  NodeHeap<&Node::leaf_key, &Node::leaf_pos> leaves_[2];
+  NodeHeap<&Node::front_key, &Node::front_pos> front_;
   std::vector<Node*> owner_[2];
   uint64_t clock_ = 0;
   uint64_t next_id_ = 1;

@@ -245,7 +245,8 @@ void evict_internal(mp_pool* p, int64_t n, int med, std::vector<int32_t>* freed)
 // R2 feasibility: free + eventually-evictable (excluding the pinned path) >= n.
 bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>& pinned) {
   if (p->nfree[med] >= n) return true;
-  return p->nfree[med] + p->index->evictable(med, pinned) >= n;
+  // the pool is full (the cache regime): peel only as much as is needed
+  return p->index->evictable_at_least(med, pinned, n - p->nfree[med]);
 }
 
 mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,

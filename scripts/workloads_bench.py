@@ -40,6 +40,7 @@ S = LLAMA2_13B
 B = S.block_tokens
 FLAGS = M.XFER_DEDUP | M.XFER_ASYNC
 STREAM_ORDERED = True
+RETAIN = False          # --retain: sessions stay cached; full pools evict (R8)
 
 
 class Timed:
@@ -95,8 +96,9 @@ def loogle_session(P, D, sess):
     for prompt, p_part, d_part in prompts:       # the session ends: both sides retire it
         P.free_mem(p_part)
         D.free_mem(d_part)
-        P.delete(prompt)
-        D.delete(prompt)
+        if not RETAIN:
+            P.delete(prompt)
+            D.delete(prompt)
     return moved
 
 
@@ -116,7 +118,7 @@ def react_session(P, D, sess):
         D.free_mem(d_addrs[len(whole) // B:])
         P.free_mem(src[k:])
         retire.append(whole)
-    for whole in retire:
+    for whole in retire if not RETAIN else ():
         P.delete(whole)
         D.delete(whole)
     return moved
@@ -132,11 +134,15 @@ def main():
                     help="engine allocations drain the pool (no MP_ALLOC_STREAM_ORDERED)")
     ap.add_argument("--phase-times", action="store_true",
                     help="host time per pool method in the timed loop (stderr)")
+    ap.add_argument("--retain", action="store_true",
+                    help="keep finished sessions cached (pools fill up and evict LRU leaves)")
     ap.add_argument("--prof", action="store_true", help="cProfile the timed loop (stderr)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     global STREAM_ORDERED
     STREAM_ORDERED = not args.drain_alloc
+    global RETAIN
+    RETAIN = args.retain
     idx = 2 if args.workload == "loogle" else 3
     seed = seed_for(idx)
     if args.workload == "loogle":
@@ -201,6 +207,7 @@ def main():
                      "idle_between_launches_share": round(sum(s["gap_ms"] for s in st) / ms, 4),
                      "host_ms": round(host_ms, 3)},
         "engine_alloc": "drain" if args.drain_alloc else "stream_ordered",
+        "sessions_retained": RETAIN,
         "clocks": clocks.summary()}))
 
 

@@ -71,6 +71,26 @@ int64_t ix_evictable(void* h, int medium) {
   return ((Index*)h)->evictable(medium, std::vector<Node*>());
 }
 
+int64_t ix_evictable_leaves(void* h, int medium) {
+  return ((Index*)h)->evictable_leaves(medium, std::vector<Node*>());
+}
+
+// pinned = the stored path of toks; returns evictable(medium, pinned) and
+// writes whether evictable_at_least agrees for need = 0..that+1 (1 = yes)
+int64_t ix_evictable_pinned(void* h, int medium, const int32_t* toks, int64_t n_tok, int* agree) {
+  Index* ix = (Index*)h;
+  const std::vector<Node*> pin = ix->path(toks, n_tok / ix->block_tokens());
+  const int64_t full = ix->evictable(medium, pin);
+  *agree = 1;
+  for (int64_t k = 0; k <= full + 1; ++k)
+    if (ix->evictable_at_least(medium, pin, k) != (full >= k)) *agree = 0;
+  return full;
+}
+
+int ix_evictable_at_least(void* h, int medium, int64_t need) {
+  return ((Index*)h)->evictable_at_least(medium, std::vector<Node*>(), need) ? 1 : 0;
+}
+
 int64_t ix_dump(void* h, char* buf, int64_t cap) {
   const std::string s = ((Index*)h)->dump();
   if (buf && cap > (int64_t)s.size()) {

@@ -50,6 +50,13 @@ def lib(tmp_path_factory):
     L.ix_rebind.argtypes = [P, C.c_int, C.c_int32, C.c_int, C.c_int32]
     L.ix_evictable.restype = C.c_int64
     L.ix_evictable.argtypes = [P, C.c_int]
+    L.ix_evictable_leaves.restype = C.c_int64
+    L.ix_evictable_leaves.argtypes = [P, C.c_int]
+    L.ix_evictable_pinned.restype = C.c_int64
+    L.ix_evictable_pinned.argtypes = [P, C.c_int, C.POINTER(C.c_int32), C.c_int64,
+                                      C.POINTER(C.c_int)]
+    L.ix_evictable_at_least.restype = C.c_int
+    L.ix_evictable_at_least.argtypes = [P, C.c_int, C.c_int64]
     L.ix_dump.restype = C.c_int64
     L.ix_dump.argtypes = [P, C.c_char_p, C.c_int64]
     return L
@@ -154,7 +161,20 @@ def run(L, seed, B, n_ops):
             if step % 20 == 0:
                 for med in (O.HBM, O.DRAM):
                     trial = pool._clone_meta()
-                    assert L.ix_evictable(h, med) == len(trial._evict(10 ** 9, med))
+                    full = len(trial._evict(10 ** 9, med))
+                    assert L.ix_evictable(h, med) == full
+                    # the fast feasibility bound (unpinned leaves) never over-promises
+                    assert 0 <= L.ix_evictable_leaves(h, med) <= full
+                    # the early-stopping peel decides "at least k" exactly
+                    for k in {0, 1, full // 2, full, full + 1}:
+                        assert L.ix_evictable_at_least(h, med, k) == (full >= k)
+                    if stored:   # with a stored prefix pinned (the receiver's match, R12)
+                        t = stored[rng.integers(len(stored))]
+                        t = t[: int(rng.integers(0, len(t) + 1))]
+                        ta, tp = arr(t)
+                        agree = C.c_int(0)
+                        L.ix_evictable_pinned(h, med, tp, len(t), C.byref(agree))
+                        assert agree.value == 1
         assert dump(L, h) == pool.dump_index()
     finally:
         L.ix_free(h)
