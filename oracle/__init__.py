@@ -13,12 +13,15 @@ code with it; the only shared module is ``workloads`` (seeded input
 generators, no method arithmetic).
 
 Parity status: see DESIGN.md §3.  Pinned: allocator (lowest-first, S:131-133
-examples, conservation), match/insert/delete (brute-force longest-prefix model,
-S:207, SPEC examples), migration bytes (closed form dst[d_j] == src[s_j],
-np.take cross-check), golden worked example.  Parity unpinned (our readings,
-pinned only by our own derivations): the LRU clock and tie-breaks (R7-R9),
-delete's terminal rule (R6), suffix/DEDUP semantics of transfer_with_insert
-(R3), eviction-before-OOM feasibility (R2).
+examples, conservation), match/insert/delete incl. R6 (brute-force set-of-
+sequences model, SPEC examples), migration bytes (closed form
+dst[d_j] == src[s_j], np.take cross-check), golden worked example; and by
+independent models in tests/test_oracle_pins.py: LRU eviction and swap-out
+victims (R7-R9, recency recomputed from the op history), evict-before-OOM
+feasibility (R2, subset brute force), DEDUP reuse of the receiver's cached
+prefix (R3, bytes + reuse + conservation).  Tie-breaks between equally recent
+blocks (lowest block index) are a reading no model can pin: a single op
+never leaves two leaves equally recent, so it only orders the initial state.
 """
 from .mempool_oracle import (  # noqa: F401
     HBM, DRAM, MIXED, FREE, ACTIVE, INDEXED, ORPHAN,

@@ -242,9 +242,14 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
 // exclusive scan, then every thread emits its lowest set bits in order, so
 // the ids come out ascending (R2 lowest-first).
 __global__ void __launch_bounds__(1024) alloc_kernel(uint32_t* bitmap, int nwords, int n,
-                                                     int* out_dev, int* out_host, int* err) {
+                                                     int* out_dev, int* out_host, int* err,
+                                                     const InlineIds frees) {
   __shared__ int warp_tot[32];
   const int t = threadIdx.x;
+  // frees queued since the last allocation go first (lowest-first reuses them)
+  for (int i = t; i < frees.n; i += blockDim.x)
+    atomicOr(bitmap + (frees.ids[i] >> 5), 1u << (frees.ids[i] & 31));
+  __syncthreads();
   const int wpt = (nwords + blockDim.x - 1) / blockDim.x;
   const int w0 = min(nwords, t * wpt), w1 = min(nwords, w0 + wpt);
   int cnt = 0;
@@ -288,6 +293,11 @@ __global__ void __launch_bounds__(1024) alloc_kernel(uint32_t* bitmap, int nword
     }
     bitmap[w] &= ~taken;
   }
+}
+
+__global__ void free_inline_kernel(uint32_t* bitmap, const InlineIds frees) {
+  for (int i = threadIdx.x; i < frees.n; i += blockDim.x)
+    atomicOr(bitmap + (frees.ids[i] >> 5), 1u << (frees.ids[i] & 31));
 }
 
 __global__ void free_kernel(uint32_t* bitmap, const int* ids, int n) {
@@ -465,11 +475,19 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
 }
 
 cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,
-                         int* err, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
+                         int* err, cudaStream_t stream, const InlineIds* frees) {
+  static const InlineIds none{};
+  if (n <= 0) {
+    if (frees && frees->n > 0) {
+      free_inline_kernel<<<1, 256, 0, stream>>>(bitmap, *frees);
+      return cudaGetLastError();
+    }
+    return cudaSuccess;
+  }
   // 256 threads: <= 8 bitmap words each up to 65536 blocks; small enough to
   // slot in beside retiring migration CTAs
-  alloc_kernel<<<1, 256, 0, stream>>>(bitmap, nwords, n, out_dev, out_host, err);
+  alloc_kernel<<<1, 256, 0, stream>>>(bitmap, nwords, n, out_dev, out_host, err,
+                                      frees ? *frees : none);
   return cudaGetLastError();
 }
 

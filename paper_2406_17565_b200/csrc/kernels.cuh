@@ -48,12 +48,22 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
                            long long len, int max_ctas, cudaStream_t stream, int variant,
                            const Sched* sched = nullptr);
 
-// Lowest-first allocation of n blocks from a bitmap (bit = 1: free).  Writes
-// the ids ascending into out_dev (device) and out_host (mapped pinned host,
-// may be nullptr), clears their bits.  *err (device) := 1 if fewer than n
-// were free (the host shadow makes this impossible; checked in verify mode).
+// Up to kInlineIds block ids passed by value in the kernel parameters (no
+// host-to-device copy call: 3.7 us of host time each on B200).
+constexpr int kInlineIds = 1000;
+struct InlineIds {
+  int n;
+  int ids[kInlineIds];
+};
+
+// Lowest-first allocation of n blocks from a bitmap (bit = 1: free), after
+// setting the bits of `frees` (nullable; applied first, so lowest-first sees
+// them).  Writes the ids ascending into out_dev (device) and out_host (mapped
+// pinned host, may be nullptr), clears their bits.  *err (device) := 1 if
+// fewer than n were free (the host shadow makes this impossible; checked in
+// verify mode).  n == 0 with frees: just the frees.
 cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,
-                         int* err, cudaStream_t stream);
+                         int* err, cudaStream_t stream, const InlineIds* frees = nullptr);
 
 // Sets the bits of ids[0..n) (device array).
 cudaError_t launch_free(uint32_t* bitmap, const int* ids, int n, cudaStream_t stream);

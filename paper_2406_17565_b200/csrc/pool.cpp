@@ -45,13 +45,30 @@ mp_status upload_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d_out) {
 }
 
 // ------------------------------------------------------- sync / ordering
+// Frees of HBM blocks reach the device bitmap lazily, on the meta stream:
+// small sets by value in a kernel's parameters (folded into the next
+// allocation when there is one), large ones through the id arena.
+static bool take_inline_frees(mp_pool* p, mpk::InlineIds* f) {
+  f->n = 0;
+  if (p->pending_free.empty() || (int)p->pending_free.size() > mpk::kInlineIds) return false;
+  f->n = (int)p->pending_free.size();
+  std::memcpy(f->ids, p->pending_free.data(), p->pending_free.size() * sizeof(int32_t));
+  p->pending_free.clear();
+  return true;
+}
+
 mp_status flush_frees(mp_pool* p) {
   if (p->pending_free.empty()) return MP_OK;
-  std::vector<int32_t> ids;
-  ids.swap(p->pending_free);
-  int* d = nullptr;
-  TRY(upload_ids(p, ids, &d));
-  CK(mpk::launch_free(p->d_bitmap, d, (int)ids.size(), p->meta));
+  mpk::InlineIds f;
+  if (take_inline_frees(p, &f)) {
+    CK(mpk::launch_alloc(p->d_bitmap, p->nwords, 0, nullptr, nullptr, p->d_err, p->meta, &f));
+  } else {
+    std::vector<int32_t> ids;
+    ids.swap(p->pending_free);
+    int* d = nullptr;
+    TRY(upload_ids(p, ids, &d));
+    CK(mpk::launch_free(p->d_bitmap, d, (int)ids.size(), p->meta));
+  }
   p->stats.aux_launches += 1;
   return MP_OK;
 }
@@ -278,7 +295,10 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
   bool hazard = false;
   for (int32_t id : *ids) hazard = hazard || p->pend_w[(size_t)id] || p->pend_r[(size_t)id];
   if (hazard) TRY(flush_involving(p));
-  TRY(flush_frees(p));  // the device bitmap must see every earlier free first
+  // the device bitmap must see every earlier free first: small sets ride in
+  // the allocation kernel's parameters
+  mpk::InlineIds f;
+  if (!take_inline_frees(p, &f)) TRY(flush_frees(p));
   int* h = nullptr;
   int* d = arena_take(p, n, &h);
   if (!d) {
@@ -286,7 +306,7 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
     return MP_ERR_INTERNAL;
   }
   CK(mpk::launch_alloc(p->d_bitmap, p->nwords, (int)n, d, p->verify ? h : nullptr, p->d_err,
-                       p->meta));
+                       p->meta, f.n ? &f : nullptr));
   p->stats.aux_launches += 1;
   if (p->verify) p->pending_verify.push_back({h, *ids});
   *d_ids = d;
