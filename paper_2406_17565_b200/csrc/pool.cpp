@@ -16,13 +16,37 @@ void set_err(const std::string& s) { g_err = s; }
 const std::string& get_err() { return g_err; }
 
 // ----------------------------------------------------------------- arena
+// Arena ranges a peer process may still read: the device-allocated block
+// table of a remote transfer between its allocation reply and its completion
+// (the sender's copy reads it over IPC; a drain here cannot wait for it).
+static int64_t skip_live(const mp_pool* p, int64_t start, int64_t n) {
+  for (bool moved = true; moved;) {
+    moved = false;
+    for (const auto& kv : p->remotes) {
+      const RemotePeer* r = kv.second;
+      if (!r->has_pending || r->pending.d_dst_off < 0) continue;
+      const int64_t o = r->pending.d_dst_off, e = o + std::max<int64_t>(r->pending.nm, 1);
+      if (start < e && o < start + n) {
+        start = e;
+        moved = true;
+      }
+    }
+  }
+  return start;
+}
+
 int* arena_take(mp_pool* p, int64_t n, int** host) {
   n = std::max<int64_t>(n, 1);
   if (n > p->ar.cap) return nullptr;
-  if (p->ar.used + n > p->ar.cap) {
+  int64_t at = p->remotes.empty() ? p->ar.used : skip_live(p, p->ar.used, n);
+  if (at + n > p->ar.cap) {
+    // wrap: everything this process issued (and every completed inbound
+    // copy) is done after the drain; in-flight remote ranges are skipped
     if (drain(p) != MP_OK) return nullptr;
-    p->ar.used = 0;
+    at = p->remotes.empty() ? 0 : skip_live(p, 0, n);
+    if (at + n > p->ar.cap) return nullptr;
   }
+  p->ar.used = at;
   int* d = p->ar.d + p->ar.used;
   *host = p->ar.h + p->ar.used;
   p->ar.used += n;
@@ -139,6 +163,14 @@ mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     b.bytes = 0;
     b.sids.clear();
     b.dids.clear();
+    // next id table of the ring; its last reader must be done before the
+    // meta stream overwrites it
+    const int k = dst->btab_next;
+    dst->btab_next = (k + 1) % mp_pool::kBatchTabs;
+    if (dst->btab_used[k]) CK(cudaStreamWaitEvent(dst->meta, dst->btab_ev[k], 0));
+    b.tab = k;
+    dst->bsrc = dst->bsrc_ring[k];
+    dst->bdst = dst->bdst_ring[k];
   }
   // id tables: source ids from the host, destination ids from the device
   // allocator's output (or the caller's ids)
@@ -190,6 +222,8 @@ mp_status flush_batch(mp_pool* dst) {
     DevGuard g(dst->dev);
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, dst->bsrc),
                              pool_ep(dst->d_slabs, dst->bdst), n, b.j0, b.nj));
+    CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
+    dst->btab_used[b.tab] = true;
   }
   TRY(link(dst, src));
   for (int32_t id : b.sids) src->pend_r[(size_t)id] = 0;
@@ -424,8 +458,11 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_sched) cudaFree(p->d_sched);
     if (p->ar.d) cudaFree(p->ar.d);
-    if (p->bsrc) cudaFree(p->bsrc);
-    if (p->bdst) cudaFree(p->bdst);
+    for (int k = 0; k < mp_pool::kBatchTabs; ++k) {
+      if (p->bsrc_ring[k]) cudaFree(p->bsrc_ring[k]);
+      if (p->bdst_ring[k]) cudaFree(p->bdst_ring[k]);
+      if (p->btab_ev[k]) cudaEventDestroy(p->btab_ev[k]);
+    }
     if (p->ar.h) cudaFreeHost(p->ar.h);
     if (p->own_dram && p->dram) cudaFreeHost(p->dram);
     if (p->staging) cudaFree(p->staging);
@@ -568,8 +605,13 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->batch_cap = p->n_hbm;
   p->pend_w.assign((size_t)p->n_hbm, 0);
   p->pend_r.assign((size_t)p->n_hbm, 0);
-  CKC(cudaMalloc(&p->bsrc, sizeof(int) * (size_t)p->batch_cap));
-  CKC(cudaMalloc(&p->bdst, sizeof(int) * (size_t)p->batch_cap));
+  for (int k = 0; k < mp_pool::kBatchTabs; ++k) {
+    CKC(cudaMalloc(&p->bsrc_ring[k], sizeof(int) * (size_t)p->batch_cap));
+    CKC(cudaMalloc(&p->bdst_ring[k], sizeof(int) * (size_t)p->batch_cap));
+    CKC(cudaEventCreateWithFlags(&p->btab_ev[k], cudaEventDisableTiming));
+  }
+  p->bsrc = p->bsrc_ring[0];
+  p->bdst = p->bdst_ring[0];
   CKC(cudaHostAlloc(&p->ar.h, sizeof(int) * p->ar.cap, cudaHostAllocMapped | cudaHostAllocPortable));
   if (p->n_dram > 0) {
     if (cfg->dram_base) {

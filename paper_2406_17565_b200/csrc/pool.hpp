@@ -196,8 +196,18 @@ struct mp_pool {
     int64_t count = 0;
     uint64_t bytes = 0;
     std::vector<int32_t> sids, dids;  // host copies (to clear the pending marks)
+    int tab = 0;                       // which of the kBatchTabs id tables it fills
   } batch;
-  int* bsrc = nullptr;
+  // The id tables are filled on the meta stream while earlier launches may
+  // still read theirs on the data stream: a ring of kBatchTabs tables, and a
+  // new batch's meta work waits for the launch that last read its table.
+  static constexpr int kBatchTabs = 4;
+  int* bsrc_ring[kBatchTabs] = {};
+  int* bdst_ring[kBatchTabs] = {};
+  cudaEvent_t btab_ev[kBatchTabs] = {};
+  bool btab_used[kBatchTabs] = {};
+  int btab_next = 0;
+  int* bsrc = nullptr;  // = bsrc_ring[batch.tab] of the batch being built
   int* bdst = nullptr;
   int64_t batch_cap = 0;
   uint64_t batch_limit = 0;
