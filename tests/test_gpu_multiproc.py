@@ -138,3 +138,89 @@ def test_two_process_golden(dedup):
     want_msgs = [(1 if k == "transfer_with_insert" else 0, src, priv, [a[2] for a in addrs])
                  for (k, src, priv, addrs) in oD.inbox]
     assert res[1]["msgs"] == want_msgs
+
+
+def _stress(rank, port, q):
+    """Rank 0 streams back-to-back ASYNC transfers (random scattered 7B
+    blocks) into rank 1's pool through the cross-process path, rank 1 serves;
+    then every received block is compared with its source by weighted
+    checksums of sampled chunks computed in each process on its own slabs."""
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import LLAMA2_7B as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        n = 512
+        c = S.chunk_bytes
+        region = torch.empty(2 * S.layers * n * c, dtype=torch.uint8, device="cuda:0")
+        slabs = [region.data_ptr() + j * n * c for j in range(2 * S.layers)]
+        pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, n,
+                      slabs=slabs, verify=True)
+        blobs = M.exchange_handles(pool)
+        pool.import_peer(blobs[1 - rank][1])
+        dist.barrier()
+        pairs = []
+        if rank == 0:
+            rng = np.random.default_rng(3)
+            src = pool.alloc_mem(n)
+            pool.debug_fill(src, 41)
+            for rnd in range(3):
+                for _ in range(30):
+                    sel = src[rng.choice(n, int(rng.integers(1, 12)), replace=False)]
+                    d = pool.transfer(1, sel, flags=M.XFER_ASYNC)
+                    if rnd == 2:
+                        pairs += list(zip(M.addr_indices(sel).tolist(),
+                                          M.addr_indices(d).tolist()))
+                pool.send_mark(1, rnd)
+                dist.barrier()
+        else:
+            for rnd in range(3):
+                _served, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+                assert mark == rnd, (mark, rnd)
+                pool.sync()
+                while True:
+                    m = pool.recv_poll()
+                    if m is None:
+                        break
+                    if rnd < 2:   # freed: the next round re-allocates these ids
+                        pool.free_mem(m[3])
+                dist.barrier()
+        pool.sync()
+        torch.cuda.synchronize()
+        g = torch.Generator(device="cuda:0").manual_seed(5)
+        w = torch.randint(-2**31, 2**31, (c // 8,), generator=g, device="cuda:0")
+        view = region.view(2 * S.layers, n, c).view(torch.int64)
+        sums = torch.stack([(view[j] * w).sum(-1) for j in (0, 17, 63)], 1).cpu().numpy()
+        out = {"pairs": pairs, "sums": sums.tolist()}
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+def test_two_process_back_to_back_async():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29950 + (os.getpid() % 40)
+    ps = [ctx.Process(target=_stress, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in ps:
+        r, out = q.get(timeout=300)
+        res[r] = out
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in res[r], res[r].get("error")
+    sums_p, sums_d = res[0]["sums"], res[1]["sums"]
+    assert len(res[0]["pairs"]) > 30
+    bad = [(s, d) for s, d in res[0]["pairs"] if sums_p[s] != sums_d[d]]
+    assert not bad, f"{len(bad)} received blocks differ from their sources"
