@@ -499,7 +499,15 @@ class OracleArm:
         O, B = self.O, self.B
         t0 = time.perf_counter()
         done, moved, n_req = [], 0, 0
-        while time.perf_counter() - t0 < budget_s and n_req < len(self.reqs):
+        def retire():
+            for prompt, part in done:
+                self.D.free_mem(part)
+                self.D.delete(prompt)
+            done.clear()
+
+        # whole passes over the request set until the budget is spent; D
+        # retires each pass (as bench.py's D retires each batch)
+        while time.perf_counter() - t0 < budget_s:
             (sid, prompt), partial = self.reqs[self.next], self.srcs[self.next]
             self.next = (self.next + 1) % len(self.reqs)
             _, matched = self.P.match(prompt)
@@ -508,9 +516,9 @@ class OracleArm:
             moved += nm
             n_req += 1
             done.append((prompt, final[len(prompt) // B:]))
-        for prompt, part in done:
-            self.D.free_mem(part)
-            self.D.delete(prompt)
+            if self.next == 0:
+                retire()
+        retire()
         return moved, n_req, time.perf_counter() - t0
 
     def sample(self, n_req, steps):
