@@ -44,12 +44,21 @@ __device__ __forceinline__ char* chunk_ptr(const Endpoint& e, unsigned j, unsign
                : e.base + id * e.stride + (long long)jr * e.cstride + e.off;
 }
 
+// Source block id of copy slot i: from the launch parameters when the host
+// passed the (short) list inline, else from the id table, else i itself.
+__device__ __forceinline__ long long src_id(const Endpoint& src, const InlineIds& sinl,
+                                            unsigned i) {
+  if (sinl.n) return sinl.ids[i];
+  return src.ids ? __ldg(src.ids + i) : (long long)i;
+}
+
 // Copies `len` bytes per chunk (the whole chunk, or a head range of it).
 template <bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endpoint dst, int j0,
                                                            int nj, long long len,
                                                            unsigned units_per_chunk,
-                                                           unsigned total_units) {
+                                                           unsigned total_units,
+                                                           const __grid_constant__ InlineIds sinl) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned warp = (blockIdx.x * (unsigned)kThreads + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * (unsigned)kThreads) >> 5;
@@ -60,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
     const unsigned part = u - ch * units_per_chunk;
     const unsigned i = ch / (unsigned)nj;
     const unsigned jr = ch - i * (unsigned)nj;
-    const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
+    const long long sid = src_id(src, sinl, i);
     const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
     const char* sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid);
     char* dp = chunk_ptr<kDstPool>(dst, j0 + jr, jr, did);
@@ -146,14 +155,15 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 
 template <int kPieceT, bool kSrcPool, bool kDstPool>
-__device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& dst, int j0, int nj,
+__device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& dst,
+                                          const InlineIds& sinl, int j0, int nj,
                                           long long chunk, unsigned pieces_per_chunk, unsigned u,
                                           const char** sp, char** dp, uint32_t* bytes) {
   const unsigned ch = u / pieces_per_chunk;
   const unsigned part = u - ch * pieces_per_chunk;
   const unsigned i = ch / (unsigned)nj;
   const unsigned jr = ch - i * (unsigned)nj;
-  const long long sid = src.ids ? __ldg(src.ids + i) : (long long)i;
+  const long long sid = src_id(src, sinl, i);
   const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
   const long long off = (long long)part * kPieceT;
   *sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid) + off;
@@ -188,7 +198,8 @@ struct UnitSource {
 template <int kPiece, int kStages, bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     Endpoint src, Endpoint dst, int j0, int nj, long long chunk, unsigned pieces_per_chunk,
-    unsigned total_units, unsigned long long* ctr, unsigned long long base) {
+    unsigned total_units, unsigned long long* ctr, unsigned long long base,
+    const __grid_constant__ InlineIds sinl) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   if (threadIdx.x != 0) return;
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
   for (int k = 0; k < kStages; ++k) {
     live[k] = u != 0xFFFFFFFFu;
     if (!live[k]) continue;
-    unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk, u, &sp, &dp,
+    unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, sinl, j0, nj, chunk, pieces_per_chunk, u, &sp, &dp,
                                           &bytes);
     dsts[k] = dp;
     lens[k] = bytes;
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
       live[r] = u != 0xFFFFFFFFu;
       if (live[r]) {
         bulk_wait_read<1>();
-        unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, j0, nj, chunk, pieces_per_chunk, u, &sp,
+        unit_addr<kPiece, kSrcPool, kDstPool>(src, dst, sinl, j0, nj, chunk, pieces_per_chunk, u, &sp,
                                               &dp, &bytes);
         dsts[r] = dp;
         lens[r] = bytes;
@@ -357,7 +368,7 @@ static bool bulk_dynamic() {
 template <int kPieceT, int kStagesT, bool kSrcPool, bool kDstPool>
 static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                                long long chunk, int max_ctas, cudaStream_t stream,
-                               const Sched* sched) {
+                               const Sched* sched, const InlineIds& sinl) {
   auto kern = migrate_bulk_kernel<kPieceT, kStagesT, kSrcPool, kDstPool>;
   const unsigned pieces = (unsigned)((chunk + kPieceT - 1) / kPieceT);
   const unsigned long long total = (unsigned long long)n * nj * pieces;
@@ -380,7 +391,8 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
   const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
   const bool dyn = sched && sched->ctr && bulk_dynamic();
   kern<<<grid, kBulkThreads, smem, stream>>>(src, dst, j0, nj, chunk, pieces, (unsigned)total,
-                                             dyn ? sched->ctr : nullptr, dyn ? *sched->base : 0);
+                                             dyn ? sched->ctr : nullptr, dyn ? *sched->base : 0,
+                                             sinl);
   const cudaError_t e = cudaGetLastError();
   if (dyn && e == cudaSuccess) *sched->base += total + (unsigned long long)grid;
   return e;
@@ -389,19 +401,19 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
 template <int kPieceT, int kStagesT>
 static cudaError_t launch_bulk_any(const Endpoint& src, const Endpoint& dst, int n, int j0,
                                    int nj, long long chunk, int max_ctas, cudaStream_t stream,
-                                   const Sched* sc) {
+                                   const Sched* sc, const InlineIds& si) {
   const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
   if (sp && dp)
     return launch_bulk<kPieceT, kStagesT, true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream,
-                                                      sc);
+                                                      sc, si);
   if (sp)
     return launch_bulk<kPieceT, kStagesT, true, false>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                       stream, sc);
+                                                       stream, sc, si);
   if (dp)
     return launch_bulk<kPieceT, kStagesT, false, true>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                       stream, sc);
+                                                       stream, sc, si);
   return launch_bulk<kPieceT, kStagesT, false, false>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                      stream, sc);
+                                                      stream, sc, si);
 }
 
 
@@ -423,16 +435,19 @@ static int bulk_cfg() {
 
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                            long long chunk, int max_ctas, cudaStream_t stream, int variant,
-                           const Sched* sched) {
+                           const Sched* sched, const InlineIds* src_inline) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
+  static const InlineIds no_ids{};
+  if (src_inline && src_inline->n != n) return cudaErrorInvalidValue;
+  const InlineIds& si = src_inline ? *src_inline : no_ids;
   if (variant == kCopyBulk) {
     switch (bulk_cfg()) {
-      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
-      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
-      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
-      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
-      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
-      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched);
+      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
+      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
+      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
+      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
+      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
+      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
     }
   }
   const unsigned units_per_chunk = (unsigned)((chunk + kUnitBytes - 1) / kUnitBytes);
@@ -461,16 +476,16 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   const int grid = (int)(want < (unsigned long long)cap ? want : (unsigned long long)cap);
   if (sp && dp)
     migrate_kernel<true, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                              units_per_chunk, (unsigned)total);
+                                                              units_per_chunk, (unsigned)total, si);
   else if (sp)
     migrate_kernel<true, false><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                               units_per_chunk, (unsigned)total);
+                                                               units_per_chunk, (unsigned)total, si);
   else if (dp)
     migrate_kernel<false, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                               units_per_chunk, (unsigned)total);
+                                                               units_per_chunk, (unsigned)total, si);
   else
     migrate_kernel<false, false><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                                units_per_chunk, (unsigned)total);
+                                                                units_per_chunk, (unsigned)total, si);
   return cudaGetLastError();
 }
 

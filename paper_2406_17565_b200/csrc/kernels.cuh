@@ -26,6 +26,14 @@ struct Endpoint {
   long long off;       // byte offset of the copied range inside each chunk
 };
 
+// Up to kInlineIds block ids passed by value in the kernel parameters (no
+// host-to-device copy call: 3.7 us of host time each on B200).
+constexpr int kInlineIds = 1000;
+struct InlineIds {
+  int n;
+  int ids[kInlineIds];
+};
+
 // Dynamic work distribution of the bulk engine: a device counter of the
 // launching stream plus the host's running start value for it (advanced by
 // the launcher; launches sharing a counter must be stream-serialised).
@@ -44,17 +52,12 @@ enum CopyVariant { kCopyAuto = 0, kCopyVector = 1, kCopyBulk = 2 };
 // kCopyBulk: cp.async.bulk (TMA engine) ring through shared memory.
 // max_ctas <= 0: one full wave (occupancy x SMs).
 // sched (nullable, bulk only): claim units dynamically instead of statically.
+// src_inline (nullable): the n source ids by value in the launch parameters
+// (n <= kInlineIds); src.ids is then ignored.
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                            long long len, int max_ctas, cudaStream_t stream, int variant,
-                           const Sched* sched = nullptr);
+                           const Sched* sched = nullptr, const InlineIds* src_inline = nullptr);
 
-// Up to kInlineIds block ids passed by value in the kernel parameters (no
-// host-to-device copy call: 3.7 us of host time each on B200).
-constexpr int kInlineIds = 1000;
-struct InlineIds {
-  int n;
-  int ids[kInlineIds];
-};
 
 // Lowest-first allocation of n blocks from a bitmap (bit = 1: free), after
 // setting the bits of `frees` (nullable; applied first, so lowest-first sees

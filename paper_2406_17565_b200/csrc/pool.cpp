@@ -172,16 +172,9 @@ mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     dst->bsrc = dst->bsrc_ring[k];
     dst->bdst = dst->bdst_ring[k];
   }
-  // id tables: source ids from the host, destination ids from the device
+  // id tables: source ids stay on the host until the launch (kernel
+  // parameters, or one upload per launch); destination ids are the device
   // allocator's output (or the caller's ids)
-  int* h = nullptr;
-  if (!arena_take(dst, n, &h)) {
-    set_err("id arena exhausted");
-    return MP_ERR_INTERNAL;
-  }
-  std::memcpy(h, sids.data(), (size_t)n * sizeof(int32_t));
-  CK(cudaMemcpyAsync(dst->bsrc + b.count, h, (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice,
-                     dst->meta));
   if (d_dst) {
     CK(cudaMemcpyAsync(dst->bdst + b.count, d_dst, (size_t)n * sizeof(int32_t),
                        cudaMemcpyDeviceToDevice, dst->meta));
@@ -220,8 +213,20 @@ mp_status flush_batch(mp_pool* dst) {
   TRY(link(src, dst));
   {
     DevGuard g(dst->dev);
-    TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, dst->bsrc),
-                             pool_ep(dst->d_slabs, dst->bdst), n, b.j0, b.nj));
+    // source ids: by value in the launch parameters when they fit, else one
+    // upload into this batch's table (ordered before the launch by meta_fence)
+    mpk::InlineIds sinl;
+    const bool inl = n <= mpk::kInlineIds;
+    if (inl) {
+      sinl.n = (int)n;
+      std::memcpy(sinl.ids, b.sids.data(), (size_t)n * sizeof(int32_t));
+    } else {
+      CK(cudaMemcpyAsync(dst->bsrc, b.sids.data(), (size_t)n * sizeof(int32_t),
+                         cudaMemcpyHostToDevice, dst->meta));
+    }
+    TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, inl ? nullptr : dst->bsrc),
+                             pool_ep(dst->d_slabs, dst->bdst), n, b.j0, b.nj, false, 0,
+                             inl ? &sinl : nullptr));
     CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
     dst->btab_used[b.tab] = true;
   }
@@ -363,7 +368,7 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester) {
 // ------------------------------------------------------------ migration
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a0,
                                const mpk::Endpoint& b0, int64_t n, int j0, int nj, bool peer,
-                               int64_t len) {
+                               int64_t len, const mpk::InlineIds* src_inline) {
   if (n <= 0) return MP_OK;
   if (len <= 0) len = p->chunk;
   mpk::Endpoint a = a0, b = b0;
@@ -391,7 +396,7 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
   const mpk::Sched sched{p->d_sched, &p->sched_base};
   CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant,
-                         s == p->stream ? &sched : nullptr));
+                         s == p->stream ? &sched : nullptr, src_inline));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});

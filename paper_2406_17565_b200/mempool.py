@@ -112,8 +112,10 @@ _I64 = C.c_int64
 _I32 = C.c_int32
 _U32 = C.c_uint32
 _U64 = C.c_uint64
-_PU64 = C.POINTER(C.c_uint64)
-_PI32 = C.POINTER(C.c_int32)
+# array arguments travel as plain addresses (c_void_p): numpy's
+# `a.ctypes.data` is half the cost of building a typed ctypes pointer
+_PU64 = C.c_void_p
+_PI32 = C.c_void_p
 _PI64 = C.POINTER(C.c_int64)
 
 # name -> (restype, argtypes); the list is also the export check of the tests.
@@ -199,11 +201,11 @@ def _i32(a) -> np.ndarray:
 
 
 def _pu64(a: np.ndarray):
-    return a.ctypes.data_as(_PU64)
+    return a.ctypes.data
 
 
 def _pi32(a: np.ndarray):
-    return a.ctypes.data_as(_PI32)
+    return a.ctypes.data
 
 
 def _event_handle(event) -> int:
@@ -533,7 +535,7 @@ def tp_plan(H: int, p: int, q: int):
     k = C.c_int64(0)
     _check(_lib.mp_tp_plan(H, p, q, None, 0, C.byref(k)), "tp_plan")
     out = np.zeros(5 * max(k.value, 1), np.int32)
-    _check(_lib.mp_tp_plan(H, p, q, out.ctypes.data_as(_PI32), k.value, C.byref(k)), "tp_plan")
+    _check(_lib.mp_tp_plan(H, p, q, out.ctypes.data, k.value, C.byref(k)), "tp_plan")
     return [tuple(int(x) for x in out[5 * i: 5 * i + 5]) for i in range(k.value)]
 
 
