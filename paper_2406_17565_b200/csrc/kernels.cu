@@ -53,18 +53,22 @@ __device__ __forceinline__ long long src_id(const Endpoint& src, const InlineIds
 }
 
 // Copies `len` bytes per chunk (the whole chunk, or a head range of it).
+constexpr unsigned kGroup = 8;  // units per dynamic claim (32 KiB per warp)
+
 template <bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endpoint dst, int j0,
                                                            int nj, long long len,
                                                            unsigned units_per_chunk,
                                                            unsigned total_units,
-                                                           const __grid_constant__ InlineIds sinl) {
+                                                           const __grid_constant__ InlineIds sinl,
+                                                           unsigned long long* ctr,
+                                                           unsigned long long base) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned warp = (blockIdx.x * (unsigned)kThreads + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * (unsigned)kThreads) >> 5;
   const bool full_units = (len % kUnitBytes) == 0;
   const long long chunk = len;
-  for (unsigned u = warp; u < total_units; u += nwarps) {
+  auto copy_unit = [&](unsigned u) {
     const unsigned ch = u / units_per_chunk;
     const unsigned part = u - ch * units_per_chunk;
     const unsigned i = ch / (unsigned)nj;
@@ -88,6 +92,28 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
       for (int k = 0; k < kVec; ++k)
         if (off + k * 512 < chunk) st_stream(dp + off + k * 512, v[k]);
     }
+  };
+  if (!ctr) {  // static grid-stride split
+    for (unsigned u = warp; u < total_units; u += nwarps) copy_unit(u);
+    return;
+  }
+  // dynamic: warp w starts on group w; later groups (nwarps + claim) come
+  // from lane 0's atomicAdd, issued while the current group is copied so the
+  // thousands of warps' claims queue behind copies, not in front of them.
+  // One failing claim per warp: the launcher advances `base` by
+  // max(groups - warps, 0) + warps.
+  const unsigned long long ngroups = (total_units + kGroup - 1) / kGroup;
+  unsigned long long g = warp;
+  for (;;) {
+    unsigned long long next = 0;
+    if (lane == 0) next = nwarps + (atomicAdd(ctr, 1ull) - base);
+    if (g < ngroups) {
+      const unsigned u0 = (unsigned)g * kGroup;
+      const unsigned u1 = min(u0 + kGroup, total_units);
+      for (unsigned u = u0; u < u1; ++u) copy_unit(u);
+    }
+    g = __shfl_sync(0xffffffffu, next, 0);
+    if (g >= ngroups) break;
   }
 }
 
@@ -474,19 +500,28 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   }
   const unsigned long long want = (total + (kThreads / 32) - 1) / (kThreads / 32);
   const int grid = (int)(want < (unsigned long long)cap ? want : (unsigned long long)cap);
+  const bool dyn = sched && sched->ctr && bulk_dynamic();
+  unsigned long long* ctr = dyn ? sched->ctr : nullptr;
+  const unsigned long long sbase = dyn ? *sched->base : 0;
   if (sp && dp)
-    migrate_kernel<true, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                              units_per_chunk, (unsigned)total, si);
+    migrate_kernel<true, true><<<grid, kThreads, 0, stream>>>(
+        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
   else if (sp)
-    migrate_kernel<true, false><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                               units_per_chunk, (unsigned)total, si);
+    migrate_kernel<true, false><<<grid, kThreads, 0, stream>>>(
+        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
   else if (dp)
-    migrate_kernel<false, true><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                               units_per_chunk, (unsigned)total, si);
+    migrate_kernel<false, true><<<grid, kThreads, 0, stream>>>(
+        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
   else
-    migrate_kernel<false, false><<<grid, kThreads, 0, stream>>>(src, dst, j0, nj, chunk,
-                                                                units_per_chunk, (unsigned)total, si);
-  return cudaGetLastError();
+    migrate_kernel<false, false><<<grid, kThreads, 0, stream>>>(
+        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
+  const cudaError_t e = cudaGetLastError();
+  if (dyn && e == cudaSuccess) {
+    const unsigned long long groups = (total + kGroup - 1) / kGroup;
+    const unsigned long long warps = (unsigned long long)grid * (kThreads / 32);
+    *sched->base += (groups > warps ? groups - warps : 0) + warps;
+  }
+  return e;
 }
 
 cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,

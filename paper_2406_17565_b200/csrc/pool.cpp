@@ -394,9 +394,14 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
   int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyBulk : p->copy_kernel;
   if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
+  // dynamic unit claiming on the pool's data stream (launches serialised);
+  // stores into a peer's memory keep the static split: on the one-GPU
+  // two-process run (IPC-mapped pool) it was 4% ahead of claiming
+  // (profiles/sched_r01.txt), and an NVLink-bound copy gains nothing from
+  // rebalancing SMs
   const mpk::Sched sched{p->d_sched, &p->sched_base};
   CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant,
-                         s == p->stream ? &sched : nullptr, src_inline));
+                         (s == p->stream && !peer) ? &sched : nullptr, src_inline));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});
