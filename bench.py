@@ -315,10 +315,13 @@ def run_ours(args, rank, world, dist):
     peak, peak_src = load_peaks()
     kernel_ms = st["kernel_ms"] / max(st["timed_launches"], 1)
     payload_per_launch = st["timed_bytes"] / max(st["timed_launches"], 1)
-    if role.kind == "PD":
+    same_gpu = role.kind == "PD" or args.device >= 0   # --device: every rank on one GPU
+    if same_gpu:
         # loopback: the kernel reads Pb and writes Pb of HBM per block
         alg = 2.0 * payload_per_launch
-        roof = {"kernel": "migrate_kernel<pool,pool> (fused gather->store, A6f), loopback",
+        roof = {"kernel": "migrate_kernel<pool,pool> (fused gather->store, A6f), "
+                          + ("loopback" if role.kind == "PD" else
+                             "two processes on one GPU (IPC-mapped receiver pool)"),
                 "bound": "hbm", "peak": peak, "peak_source": peak_src}
     else:
         # across GPUs the bound is the NVLink direction P -> D: Pb per block
@@ -333,8 +336,8 @@ def run_ours(args, rank, world, dist):
     roof.update({
         "achieved": round(achieved, 1) if achieved else None, "unit": "GB/s",
         "frac": round(achieved / roof["peak"], 4) if achieved else None,
-        "nominal_peak": NOMINAL_HBM_GBS if role.kind == "PD" else NVLINK_GBS,
-        "frac_of_nominal": (round(achieved / (NOMINAL_HBM_GBS if role.kind == "PD" else NVLINK_GBS), 4)
+        "nominal_peak": NOMINAL_HBM_GBS if same_gpu else NVLINK_GBS,
+        "frac_of_nominal": (round(achieved / (NOMINAL_HBM_GBS if same_gpu else NVLINK_GBS), 4)
                             if achieved else None),
         "traffic": round(ratio * alg) if ratio else None,
         "traffic_note": (f"dram read+write per launch = {ratio} x algorithmic, from the ncu "
