@@ -14,12 +14,63 @@
 // called directly for an in-process peer and from the mailbox server
 // (remote.cpp) for a peer in another process.
 // Readings R3, R4, R12, R13.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 
 #include "pool.hpp"
 
 namespace mp {
+namespace {
+
+// Host-time breakdown of mp_transfer_with_insert (MP_HOST_TIMING=1 prints it
+// when a pool is destroyed): [0] source validation, [1] receiver allocation
+// step (match, pin, allocation kernel), [2] transmission (batch append or
+// launch), [3] receiver insertion + delivery, [4] completion (sync unless ASYNC).
+struct HostPhases {
+  double t[10] = {};
+  uint64_t n = 0, m[10] = {};
+};
+thread_local HostPhases g_host;
+bool host_timing_on_impl() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MP_HOST_TIMING");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+double host_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
+
+bool host_timing_on() { return host_timing_on_impl(); }
+double host_clock() { return host_now(); }
+void host_lap(int slot, double dt) {
+  g_host.t[slot] += dt;
+  ++g_host.m[slot];
+}
+
+void host_report_timing() {
+  if (!host_timing_on() || g_host.n == 0) return;
+  const char* names[10] = {"validate_src", "dst_prepare", "transmit", "dst_commit", "finish",
+                           "append:preflush", "append:ids", "append:query", "append:flush",
+                           "flush_batch"};
+  for (int i = 0; i < 5; ++i)
+    fprintf(stderr, "[mempool host] twi %-16s %8llu calls %8.2f us avg\n", names[i],
+            (unsigned long long)g_host.n, g_host.t[i] / (double)g_host.n * 1e6);
+  for (int i = 5; i < 10; ++i)
+    if (g_host.m[i])
+      fprintf(stderr, "[mempool host]     %-16s %8llu calls %8.2f us avg\n", names[i],
+              (unsigned long long)g_host.m[i], g_host.t[i] / (double)g_host.m[i] * 1e6);
+  g_host = HostPhases{};
+}
+
 namespace {
 
 // R13 (memory asymmetry): a source block may be in HBM or, swapped
@@ -279,6 +330,21 @@ mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
   return transmit_dram(src, dst, ds, dd, j0, nj);
 }
 
+// A transfer transmit_hbm will append to dst's coalescing batch: let the
+// receiver's allocation write its ids straight into the batch table.
+void hint_slot(mp_pool* src, mp_pool* dst, uint32_t flags, const std::vector<uint8_t>& smeds,
+               int j0, int nj) {
+  const uint32_t path = flags & MP_XFER_PATH_MASK;
+  if (!(path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED) || src->dev != dst->dev ||
+      !dst->coalesce || (flags & MP_XFER_DST_GIVEN))
+    return;
+  for (uint8_t m : smeds)
+    if (m != MP_HBM) return;
+  dst->slot_hint.src = src;
+  dst->slot_hint.j0 = j0;
+  dst->slot_hint.nj = nj;
+}
+
 mp_status finish(mp_pool* src, mp_pool* dst, uint32_t flags) {
   if (flags & MP_XFER_ASYNC) return MP_OK;
   {
@@ -314,7 +380,8 @@ mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t f
     DevGuard g(dst->dev);
     if (dst->nfree[MP_HBM] < n) evict_internal(dst, n - dst->nfree[MP_HBM], MP_HBM, nullptr);
     TRY(alloc_hbm(dst, n, src_inst, &st->dids, &st->d_dst));
-    if (st->d_dst) st->d_dst_off = st->d_dst - dst->ar.d;
+    if (st->d_dst && st->d_dst >= dst->ar.d && st->d_dst < dst->ar.d + dst->ar.cap)
+      st->d_dst_off = st->d_dst - dst->ar.d;
   }
   return MP_OK;
 }
@@ -363,7 +430,8 @@ mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, 
     if (dst->nfree[MP_HBM] < st->nm)
       evict_internal(dst, st->nm - dst->nfree[MP_HBM], MP_HBM, nullptr);
     TRY(alloc_hbm(dst, st->nm, src_inst, &st->dids, &st->d_dst));
-    if (st->d_dst) st->d_dst_off = st->d_dst - dst->ar.d;
+    if (st->d_dst && st->d_dst >= dst->ar.d && st->d_dst < dst->ar.d + dst->ar.cap)
+      st->d_dst_off = st->d_dst - dst->ar.d;
   }
   return MP_OK;
 }
@@ -420,7 +488,10 @@ mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t
                            priv_len, nullptr);
   // ---- (1) allocation at the receiver ----
   DstPrep st;
-  TRY(dst_prepare_xfer(dst, src->inst, n, flags, da, priv, priv_len, &st));
+  hint_slot(src, dst, flags, smeds, 2 * l0, 2 * (l1 - l0));
+  const mp_status ps = dst_prepare_xfer(dst, src->inst, n, flags, da, priv, priv_len, &st);
+  dst->slot_hint.src = nullptr;
+  TRY(ps);
   // ---- (2) transmission ----
   TRY(transmit(src, dst, sids, smeds, st.dids, st.d_dst, 2 * l0, 2 * (l1 - l0),
                flags & MP_XFER_PATH_MASK));
@@ -443,24 +514,43 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
   if ((flags & MP_XFER_DST_GIVEN) && (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
   const int64_t B = src->B, ceil_b = (n_tok + B - 1) / B;
   if (m > ceil_b) return MP_ERR_ADDR_COUNT;
+  const bool tm = host_timing_on_impl();
+  double t0 = tm ? host_now() : 0.0;
+  auto lap = [&](int i) {
+    if (!tm) return;
+    const double t = host_now();
+    g_host.t[i] += t - t0;
+    t0 = t;
+  };
   std::vector<int32_t> sids;
   std::vector<uint8_t> smeds;
   TRY(validate_src(src, sa, m, &sids, &smeds));
   if (rp)
     return remote_transfer(src, rp, 1, toks, n_tok, sids, smeds, m, da, flags, 0, src->L, priv,
                            priv_len, n_moved);
+  lap(0);
   // ---- (1) allocation at the receiver, with its DEDUP match ----
   DstPrep st;
-  TRY(dst_prepare_twi(dst, src->inst, toks, n_tok, m, flags, da, priv, priv_len, &st));
+  hint_slot(src, dst, flags, smeds, 0, src->nch);
+  const mp_status ps =
+      dst_prepare_twi(dst, src->inst, toks, n_tok, m, flags, da, priv, priv_len, &st);
+  dst->slot_hint.src = nullptr;
+  TRY(ps);
+  lap(1);
   // ---- (2) transmission of all layers ----
   std::vector<int32_t> moved_src(sids.begin() + st.skip, sids.end());
   std::vector<uint8_t> moved_med(smeds.begin() + st.skip, smeds.end());
   TRY(transmit(src, dst, moved_src, moved_med, st.dids, st.d_dst, 0, src->nch,
                flags & MP_XFER_PATH_MASK));
+  lap(2);
   // ---- (3) insertion at the receiver, ok ----
   TRY(dst_commit(dst, st, da));
   if (n_moved) *n_moved = st.nm;
-  return finish(src, dst, flags);
+  lap(3);
+  const mp_status fs = finish(src, dst, flags);
+  lap(4);
+  if (tm) ++g_host.n;
+  return fs;
 }
 
 // ---------------------------------------------------------------------------

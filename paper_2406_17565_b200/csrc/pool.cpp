@@ -142,40 +142,60 @@ mp_status sync(mp_pool* p) {
 }
 
 // --------------------------------------------------------- coalescing
-mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
-                       const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj) {
-  const int64_t n = (int64_t)sids.size();
+// Make dst's batch ready for n more transfers from src over slabs [j0, j0+nj):
+// a batch from another source / range, or one without room, goes first, and
+// so does everything pending that reads dst's or writes src's blocks; an
+// empty batch gets the next id table of the ring once its last reader is done.
+mp_status batch_open(mp_pool* src, mp_pool* dst, int64_t n, int j0, int nj) {
   auto& b = dst->batch;
-  if (b.count > 0 && (b.src != src || b.j0 != j0 || b.nj != nj || b.count + n > dst->batch_cap))
+  if (b.open && (b.src != src || b.j0 != j0 || b.nj != nj || b.count + n > dst->batch_cap))
     TRY(flush_batch(dst));
-  // Everything else pending on the two pools goes first: a batch that writes
-  // src's blocks or reads dst's blocks must not be overtaken by this one.
   for (auto& kv : src->peers)
     if (kv.second != dst && kv.second->batch.src == src && kv.second->batch.count)
       TRY(flush_batch(kv.second));
   if (src->batch.count) TRY(flush_batch(src));
   for (auto& kv : dst->peers)
     if (kv.second->batch.src == dst && kv.second->batch.count) TRY(flush_batch(kv.second));
-  if (b.count == 0) {
+  if (!b.open) {
     b.src = src;
     b.j0 = j0;
     b.nj = nj;
+    b.count = 0;
     b.bytes = 0;
     b.sids.clear();
     b.dids.clear();
-    // next id table of the ring; its last reader must be done before the
-    // meta stream overwrites it
     const int k = dst->btab_next;
     dst->btab_next = (k + 1) % mp_pool::kBatchTabs;
     if (dst->btab_used[k]) CK(cudaStreamWaitEvent(dst->meta, dst->btab_ev[k], 0));
     b.tab = k;
     dst->bsrc = dst->bsrc_ring[k];
     dst->bdst = dst->bdst_ring[k];
+    b.open = true;
   }
+  return MP_OK;
+}
+
+mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
+                       const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj) {
+  const int64_t n = (int64_t)sids.size();
+  auto& b = dst->batch;
+  const bool tm = host_timing_on();
+  double t0 = tm ? host_clock() : 0.0;
+  auto lap = [&](int i) {
+    if (!tm) return;
+    const double t = host_clock();
+    host_lap(i, t - t0);
+    t0 = t;
+  };
+  TRY(batch_open(src, dst, n, j0, nj));
+  lap(5);
   // id tables: source ids stay on the host until the launch (kernel
   // parameters, or one upload per launch); destination ids are the device
-  // allocator's output (or the caller's ids)
-  if (d_dst) {
+  // allocator's output -- already in place when it allocated into this
+  // batch's table -- or the caller's ids
+  if (d_dst == dst->bdst + b.count) {
+    // written there by the allocation kernel (slot_hint)
+  } else if (d_dst) {
     CK(cudaMemcpyAsync(dst->bdst + b.count, d_dst, (size_t)n * sizeof(int32_t),
                        cudaMemcpyDeviceToDevice, dst->meta));
   } else {
@@ -197,16 +217,23 @@ mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
   b.count += n;
   b.bytes += (uint64_t)n * (uint64_t)nj * (uint64_t)dst->chunk;
   dst->stats.blocks_moved += (uint64_t)n;
+  lap(6);
   // keep the device busy: go now if its data stream has run dry
-  if (b.bytes >= dst->batch_limit ||
-      (dst->idle_flush && cudaStreamQuery(dst->stream) == cudaSuccess))
-    TRY(flush_batch(dst));
+  const bool go = b.bytes >= dst->batch_limit ||
+                  (dst->idle_flush && cudaStreamQuery(dst->stream) == cudaSuccess);
+  lap(7);
+  if (go) TRY(flush_batch(dst));
+  lap(8);
   return MP_OK;
 }
 
 mp_status flush_batch(mp_pool* dst) {
   auto& b = dst->batch;
-  if (b.count == 0) return MP_OK;
+  if (b.count == 0) {
+    b.open = false;  // an empty batch just gives its table back
+    return MP_OK;
+  }
+  b.open = false;
   mp_pool* src = b.src;
   const int64_t n = b.count;
   b.count = 0;  // reentrancy guard: link / launch below do not flush
@@ -343,6 +370,12 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
   if (!d) {
     set_err("id arena exhausted");
     return MP_ERR_INTERNAL;
+  }
+  if (p->slot_hint.src) {  // coalesced transfer: allocate into the batch table
+    mp_pool* src = p->slot_hint.src;
+    p->slot_hint.src = nullptr;
+    TRY(batch_open(src, p, n, p->slot_hint.j0, p->slot_hint.nj));
+    d = p->bdst + p->batch.count;
   }
   CK(mpk::launch_alloc(p->d_bitmap, p->nwords, (int)n, d, p->verify ? h : nullptr, p->d_err,
                        p->meta, f.n ? &f : nullptr));

@@ -197,7 +197,15 @@ struct mp_pool {
     uint64_t bytes = 0;
     std::vector<int32_t> sids, dids;  // host copies (to clear the pending marks)
     int tab = 0;                       // which of the kBatchTabs id tables it fills
+    bool open = false;                 // a table is assigned (count may still be 0)
   } batch;
+  // Set by an in-process transfer that will be coalesced: the receiver's
+  // allocation kernel then writes the new ids straight into the open batch's
+  // destination table (no device-to-device copy per transfer).
+  struct {
+    mp_pool* src = nullptr;
+    int j0 = 0, nj = 0;
+  } slot_hint;
   // The id tables are filled on the meta stream while earlier launches may
   // still read theirs on the data stream: a ring of kBatchTabs tables, and a
   // new batch's meta work waits for the launch that last read its table.
@@ -242,6 +250,7 @@ void evict_internal(mp_pool* p, int64_t n, int med, std::vector<int32_t>* freed)
 bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>& pinned);
 // Lowest-first HBM allocation: host shadow ids + the device allocator writing
 // the same ids into HBM (d_ids) for the kernels that follow on the stream.
+mp_status batch_open(mp_pool* src, mp_pool* dst, int64_t n, int j0, int nj);
 mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,
                     int** d_ids);
 std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
@@ -299,6 +308,10 @@ uint64_t new_uid();
 mp_status remote_apply_waits(mp_pool* p);
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
 void remote_close_all(mp_pool* p);
+void host_report_timing();  // MP_HOST_TIMING=1 (api_transfer.cpp)
+bool host_timing_on();
+double host_clock();
+void host_lap(int slot, double dt);
 mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,
                           int64_t n_tok, const std::vector<int32_t>& sids,
                           const std::vector<uint8_t>& smeds, int64_t n, mp_addr* da,

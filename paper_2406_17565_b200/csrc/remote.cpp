@@ -576,6 +576,7 @@ std::string chan_name(uint64_t from, uint64_t to) {
 
 void remote_close_all(mp_pool* p) {
   if (!p->remotes.empty()) remote_report_timing();
+  host_report_timing();
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
     {
