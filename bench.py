@@ -43,6 +43,8 @@ NOMINAL_HBM_GBS = 7700.0    # B200_PROFILING.md: HBM3e 7.7 TB/s (HGX figure); th
 NVLINK_GBS = 900.0          # nominal per direction per GPU (BJ:5)
 NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction
 METRIC = "KV migration GB/s (P->D transfer_with_insert payload)"
+WORKLOAD = ("configs[1]: Llama-2-7B-shaped KV (L32 H32 D128 fp16 B16, Pb=8 MiB) ShareGPT-like "
+            "1P1D per pair, PD-Caching-2 P->D with DEDUP")
 DTYPE = "u16 (fp16 KV copied as opaque 16-bit words)"
 
 
@@ -370,8 +372,7 @@ def run_ours(args, rank, world, dist):
         "dtype": DTYPE,
         "data": "synthetic (seeded ShareGPT-like token traces; counter-based KV fill)",
         "config": {
-            "workload": "configs[1]: Llama-2-7B-shaped KV (L32 H32 D128 fp16 B16, "
-                        "Pb=8 MiB) ShareGPT-like 1P1D per pair, PD-Caching-2 P->D with DEDUP",
+            "workload": WORKLOAD,
             "placement": placement,
             "pool_blocks_per_instance": n_blocks,
             "batch_blocks": args.batch_blocks,
@@ -555,8 +556,8 @@ def run_reference(args, world):
         "ms_per_step": round(secs * 1e3 / max(args.steps, 1), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": DTYPE, "data": "synthetic",
-        "config": {"workload": "configs[1]: Llama-2-7B-shaped KV ShareGPT-like 1P1D "
-                               "(bounded sample per step, CPU oracle)"},
+        "config": {"workload": WORKLOAD,
+                   "sample": "bounded sample of the workload per step (CPU oracle)"},
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": arm.cores,
                          "kind": "oracle", "sample": arm.sample(n_req, args.steps)},
         "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
