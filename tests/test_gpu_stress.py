@@ -105,3 +105,18 @@ def test_bench_pattern_dedup_retire_bytes(coalesce_mib):
             D.delete(prompt)
     P.close()
     D.close()
+
+
+def test_static_split_engines():
+    """MP_BULK_SCHED=static (the comparison knob, read once per process): the
+    static round-robin split of both engines still moves every byte."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MP_BULK_SCHED="static")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        "tests/test_gpu_stress.py::test_back_to_back_async_transfers_bytes",
+                        "tests/test_gpu_stress.py::test_bench_pattern_dedup_retire_bytes"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
