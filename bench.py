@@ -374,6 +374,10 @@ def run_ours(args, rank, world, dist):
         "config": {
             "workload": WORKLOAD,
             "placement": placement,
+            "wire_bound": ("HBM read+write of one GPU (loopback; N=1 has no wire)" if world == 1
+                           else f"NVLink per direction, {world // 2} independent pair(s): "
+                                "N=1 -> 2 changes the bound from HBM to NVLink, so weak "
+                                "scaling is meaningful from N=2 on"),
             "pool_blocks_per_instance": n_blocks,
             "batch_blocks": args.batch_blocks,
             "copy_kernel": ["auto (bulk cp.async ring in HBM)", "vector LD/ST",
