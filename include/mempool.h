@@ -256,7 +256,10 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_instance, const mp_t
                                   int64_t priv_len, int64_t* n_moved);
 /* Receiver side of `private` delivery: pops the oldest message.  Returns
  * MP_ERR_PRECONDITION when the queue is empty; BUFFER_TOO_SMALL (message kept)
- * when priv_cap < priv_len or addr_cap < n_addrs. */
+ * when priv_cap < priv_len or addr_cap < n_addrs.  Every transfer into a pool
+ * queues one message (its kind, sender, final addrs and `private` bytes); a
+ * receiver that never polls keeps them all (host memory, ~8 bytes per block
+ * plus the payload), so a long-running engine polls or the pool owner drains. */
 mp_status mp_recv_poll(mp_pool* dst, mp_recv_msg* out, void* priv_buf, int64_t priv_cap,
                        mp_addr* addrs, int64_t addr_cap);
 
