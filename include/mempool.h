@@ -8,7 +8,7 @@
  * allocation."), §4.2 indexing, §4.3 transfer workflow
  * (P:360-369), §5.2 block aggregation; SPEC.md signatures/errors
  * (S:125-203).  Where the paper is silent the behaviour follows the
- * readings R1-R13 in DESIGN.md §3.
+ * readings R1-R17 in DESIGN.md §3.
  *
  * Conventions (apply to every function):
  *  - All array arguments are HOST pointers owned by the caller; the library
@@ -27,7 +27,7 @@
  *    receiver's allocation, insert and `private` delivery -- is already done);
  *    mp_sync(pool) waits for it.  Every later call on either pool is
  *    stream-ordered after it, and mp_alloc_mem drains the pool before handing
- *    blocks to the caller.  Frees of HBM blocks are applied to the device
+ *    blocks to the caller (unless MP_ALLOC_STREAM_ORDERED, see there).  Frees of HBM blocks are applied to the device
  *    bitmap lazily, stream-ordered before the pool's next allocation.
  *  - Layout: the HBM pool of an instance is 2*L "slabs" (K_0, V_0, K_1, V_1,
  *    ...), each hbm_blocks chunks of c = B*H*D*elem bytes (vLLM's per-layer
