@@ -4,7 +4,7 @@ A plain, slow, obviously-correct CPU model of MemPool's block pool, prompt
 index and KV-block migration (§4 "Elastic Memory Pool", Table
 tbl-mempool-api P:261-290; §4.2 indexing P:326-337; §4.3 transfer workflow
 P:360-369; §5.2 aggregation P:549-550), with every place the paper is silent
-filled by the readings R1-R13 listed in DESIGN.md §3 (= SURVEY.md §8(c)).
+filled by the readings R1-R17 listed in DESIGN.md §3 (R1-R13 = SURVEY.md §8(c)).
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 ``--impl reference`` legs may import this package.  The product path

@@ -1,7 +1,8 @@
 """Plain CPU oracle of MemPool (test infrastructure only -- see oracle/__init__.py).
 
 Every function cites the PAPER.md (P:n) / SPEC.md (S:n) passage it follows and
-the reading R1-R13 it takes where the paper is silent.
+the reading R1-R16 it takes where the paper is silent
+(R17, global scheduling, is in gs_oracle.py).
 
 Model
 -----
