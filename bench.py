@@ -607,7 +607,7 @@ def main():
         dist = dist_mod
     res = run_ours(args, rank, world, dist)
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N=1 only
             res["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
         print(json.dumps(res))
     if dist is not None:
