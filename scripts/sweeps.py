@@ -10,7 +10,10 @@
             n in {1, 2, 4, ..., 4096}, 7B pool of 8192 HBM blocks (64 GiB) and
             4096 pinned DRAM blocks (32 GiB), plus the pinned-memcpy peak.
 
-Usage: python scripts/sweeps.py {transfer|swap} > out.json
+  dram_source  SURVEY f1: transfer of swapped-out blocks straight from the
+            sender's pinned DRAM vs swap_in + HBM transfer.
+
+Usage: python scripts/sweeps.py {transfer|swap|api|dram_source} > out.json
 """
 import json
 import os
@@ -177,6 +180,52 @@ def swap_sweep():
     return out
 
 
+def dram_source_sweep():
+    """SURVEY f1 (memory asymmetry): historical KV swapped out to the
+    sender's pinned DRAM goes straight into the receiver's HBM (one kernel
+    reading mapped host memory), vs the two-step alternative swap_in + HBM
+    transfer.  Payload GB/s, synchronous calls, loopback receiver."""
+    seed = seed_for(4)
+    P = pool(0, 1024, dram_blocks=1024)
+    D = pool(1, 1024)
+    M.connect(P, D)
+    a = P.alloc_mem(768)
+    P.debug_fill(a, seed)
+    toks = (np.arange(768 * SHAPE.block_tokens, dtype=np.int64) % 31000 + 3).astype(np.int32)
+    P.insert(toks, a)
+    _old, dram = P.swap_out(512)
+    rng = np.random.default_rng(seed)
+    out = {"workload": "Llama-2-7B blocks (8 MiB) in the sender's pinned DRAM -> receiver "
+                       "HBM on one B200, synchronous calls", "results": []}
+    for n in (1, 16, 128, 256):
+        best = None
+        for _ in range(3):       # direct: the DRAM blocks stay where they are
+            sel = dram[np.sort(rng.permutation(len(dram))[:n])]
+            t0 = time.perf_counter()
+            d = P.transfer(1, sel)
+            t1 = time.perf_counter()
+            D.free_mem(d)
+            best = t1 - t0 if best is None else min(best, t1 - t0)
+        out["results"].append({"mode": "direct_dram_to_peer_hbm", "n": n,
+                               "GBps": round(n * Pb / best / 1e9, 2), "ms": round(best * 1e3, 3)})
+        print(json.dumps(out["results"][-1]), file=sys.stderr)
+    fresh = list(dram)           # the two-step mode consumes DRAM blocks (swap_in frees them)
+    for n in (1, 16, 128, 256):
+        sel, fresh = np.array(fresh[:n], np.uint64), fresh[n:]
+        t0 = time.perf_counter()
+        hb = P.swap_in(sel)
+        d = P.transfer(1, hb)
+        t1 = time.perf_counter()
+        D.free_mem(d)
+        out["results"].append({"mode": "swap_in_then_hbm_transfer", "n": n,
+                               "GBps": round(n * Pb / (t1 - t0) / 1e9, 2),
+                               "ms": round((t1 - t0) * 1e3, 3)})
+        print(json.dumps(out["results"][-1]), file=sys.stderr)
+    P.close()
+    D.close()
+    return out
+
+
 def api_latency():
     """The paper's MemPool API study: memory-API latency vs block
     count ("~800 ns per block, linear") and index insert / match of a 4K-token
@@ -232,5 +281,6 @@ def api_latency():
 
 
 if __name__ == "__main__":
-    fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency}[sys.argv[1]]
+    fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency,
+          "dram_source": dram_source_sweep}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))
