@@ -153,7 +153,8 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     TRY(link(src, dst));
     DevGuard g(dst->dev);
     int* ds = nullptr;
-    TRY(upload_ids(dst, sids, &ds));
+    mpk::InlineIds si;
+    TRY(src_ids(dst, sids, &ds, &si));
     const int* dd = d_dst;
     if (!dd) {
       int* t = nullptr;
@@ -161,7 +162,8 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
       dd = t;
     }
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, ds),
-                             pool_ep(dst->d_slabs, dd), n, j0, nj));
+                             pool_ep(dst->d_slabs, dd), n, j0, nj, false, 0,
+                             si.n ? &si : nullptr));
     dst->stats.blocks_moved += (uint64_t)n;
     return link(dst, src);
   }
@@ -173,10 +175,12 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     TRY(link(dst, src));
     DevGuard g(src->dev);
     int *ds = nullptr, *dd = nullptr;
-    TRY(upload_ids(src, sids, &ds));
+    mpk::InlineIds si;
+    TRY(src_ids(src, sids, &ds, &si));
     TRY(upload_ids(src, dids, &dd));
     TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
-                             pool_ep(it->second, dd), n, j0, nj, /*peer=*/true));
+                             pool_ep(it->second, dd), n, j0, nj, /*peer=*/true, 0,
+                             si.n ? &si : nullptr));
     src->stats.blocks_moved += (uint64_t)n;
     return link(src, dst);
   }
@@ -296,7 +300,8 @@ mp_status transmit_dram(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& 
   {
     DevGuard g(ex->dev);
     int *ds = nullptr, *dd = nullptr;
-    TRY(upload_ids(ex, sids, &ds));
+    mpk::InlineIds si;
+    TRY(src_ids(ex, sids, &ds, &si));
     TRY(upload_ids(ex, dids, &dd));
     char** dslabs = dst->d_slabs;
     if (!same_dev) {
@@ -305,7 +310,7 @@ mp_status transmit_dram(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& 
       dslabs = it->second;
     }
     TRY(launch_migrate_timed(ex, ex->stream, agg_ep(base, src->Pb, ds), pool_ep(dslabs, dd), n,
-                             j0, nj, /*peer=*/!same_dev));
+                             j0, nj, /*peer=*/!same_dev, 0, si.n ? &si : nullptr));
     ex->stats.blocks_moved += (uint64_t)n;
   }
   return same_dev ? link(dst, src) : link(src, dst);
@@ -595,12 +600,14 @@ mp_status mp_transfer_heads(mp_pool* src, int32_t dst_inst, const mp_addr* sa, i
   {
     DevGuard g(ex->dev);
     int *ds = nullptr, *dd = nullptr;
-    TRY(upload_ids(ex, sids, &ds));
+    mpk::InlineIds si;
+    TRY(src_ids(ex, sids, &ds, &si));
     TRY(upload_ids(ex, dids, &dd));
     TRY(launch_migrate_timed(ex, ex->stream,
                              pool_ep(src->d_slabs, ds, src->chunk, src_head0 * head_bytes),
                              pool_ep(dslabs, dd, dst->chunk, dst_head0 * head_bytes), n, 2 * l0,
-                             2 * (l1 - l0), /*peer=*/!same_dev, n_heads * head_bytes));
+                             2 * (l1 - l0), /*peer=*/!same_dev, n_heads * head_bytes,
+                             si.n ? &si : nullptr));
     ex->stats.blocks_moved += (uint64_t)n;
   }
   TRY(same_dev ? link(dst, src) : link(src, dst));

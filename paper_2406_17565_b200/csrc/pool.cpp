@@ -68,6 +68,19 @@ mp_status upload_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d_out) {
   return MP_OK;
 }
 
+// Source ids of a launch: by value in its parameters when they fit (no copy
+// call), else uploaded to the arena.  *d is nullptr in the inline case.
+mp_status src_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d, mpk::InlineIds* inl) {
+  inl->n = 0;
+  *d = nullptr;
+  if (!ids.empty() && (int64_t)ids.size() <= mpk::kInlineIds) {
+    inl->n = (int)ids.size();
+    std::memcpy(inl->ids, ids.data(), ids.size() * sizeof(int32_t));
+    return MP_OK;
+  }
+  return upload_ids(p, ids, d);
+}
+
 // ------------------------------------------------------- sync / ordering
 // Frees of HBM blocks reach the device bitmap lazily, on the meta stream:
 // small sets by value in a kernel's parameters (folded into the next

@@ -251,6 +251,7 @@ bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>
 // Lowest-first HBM allocation: host shadow ids + the device allocator writing
 // the same ids into HBM (d_ids) for the kernels that follow on the stream.
 mp_status batch_open(mp_pool* src, mp_pool* dst, int64_t n, int j0, int nj);
+mp_status src_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d, mpk::InlineIds* inl);
 mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,
                     int** d_ids);
 std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);

@@ -462,7 +462,8 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     if (xs == MP_OK && !hs.empty()) {
       int* d_s = nullptr;
       const int* d_d = nullptr;
-      xs = upload_ids(src, hs, &d_s);
+      mpk::InlineIds si;
+      xs = src_ids(src, hs, &d_s, &si);
       if (xs == MP_OK) {
         if (off >= 0 && !mixed) {
           d_d = r->arena + off;  // the receiver's device allocator output, IPC mapped
@@ -475,17 +476,18 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
       if (xs == MP_OK)
         xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
                                   pool_ep(r->d_slabs, d_d), (int64_t)hs.size(), j0, nj,
-                                  /*peer=*/true);
+                                  /*peer=*/true, 0, si.n ? &si : nullptr);
     }
     if (xs == MP_OK && !ds_.empty()) {
       int *d_s = nullptr, *d_d = nullptr;
-      xs = upload_ids(src, ds_, &d_s);
+      mpk::InlineIds si;
+      xs = src_ids(src, ds_, &d_s, &si);
       if (xs == MP_OK) xs = upload_ids(src, dd_, &d_d);
       if (xs == MP_OK)
         xs = launch_migrate_timed(src, src->stream,
                                   agg_ep(src->dram_dev + (int64_t)j0 * src->chunk, src->Pb, d_s),
                                   pool_ep(r->d_slabs, d_d), (int64_t)ds_.size(), j0, nj,
-                                  /*peer=*/true);
+                                  /*peer=*/true, 0, si.n ? &si : nullptr);
     }
     if (xs == MP_OK && cudaEventRecord(src->ev_ipc, src->stream) != cudaSuccess) xs = MP_ERR_CUDA;
     if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);

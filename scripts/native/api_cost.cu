@@ -35,6 +35,11 @@ int main() {
   big.n = 3;
   T("kernel launch with 4 KB of parameters", [&](int) { noop_params<<<1, 32, 0, s1>>>(d, big); });
   T("cudaEventRecord (no timing)", [&](int) { cudaEventRecord(ev, s1); });
+  cudaEvent_t evi;
+  cudaEventCreateWithFlags(&evi, cudaEventDisableTiming | cudaEventInterprocess);
+  T("cudaEventRecord (interprocess event)", [&](int) { cudaEventRecord(evi, s1); });
+  T("cudaStreamWaitEvent (interprocess event)", [&](int) { cudaStreamWaitEvent(s2, evi, 0); });
+  T("record + wait (interprocess)", [&](int) { cudaEventRecord(evi, s1); cudaStreamWaitEvent(s2, evi, 0); });
   T("cudaEventRecord (timing)", [&](int) { cudaEventRecord(evt, s1); });
   T("cudaStreamWaitEvent", [&](int) { cudaStreamWaitEvent(s2, ev, 0); });
   T("record + wait (one link)", [&](int) { cudaEventRecord(ev, s1); cudaStreamWaitEvent(s2, ev, 0); });
