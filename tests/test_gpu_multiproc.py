@@ -224,3 +224,113 @@ def test_two_process_back_to_back_async():
     assert len(res[0]["pairs"]) > 30
     bad = [(s, d) for s, d in res[0]["pairs"] if sums_p[s] != sums_d[d]]
     assert not bad, f"{len(bad)} received blocks differ from their sources"
+
+
+def _fanin(rank, port, q, rounds, per_round):
+    """Rank 0 receives from ranks 1 and 2 at once (fan-in), enough transfers
+    that its id arena wraps several times while the other sender's transfer
+    sits between allocation reply and completion.  `private` carries the
+    source ids; every received block is checksummed at the receiver before it
+    is freed and compared with the sender's own checksum of the source."""
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import TINY as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=3)
+        torch.cuda.set_device(0)
+        n = 1024 if rank == 0 else 64
+        c = S.chunk_bytes
+        region = torch.empty(2 * S.layers * n * c, dtype=torch.uint8, device="cuda:0")
+        slabs = [region.data_ptr() + j * n * c for j in range(2 * S.layers)]
+        pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, n,
+                      slabs=slabs, verify=True)
+        blobs = M.exchange_handles(pool)
+        for r in range(3):
+            if r != rank and (rank == 0 or r == 0):
+                pool.import_peer(blobs[r][1])
+        dist.barrier()
+        g = torch.Generator(device="cuda:0").manual_seed(5)
+        w = torch.randint(-2**31, 2**31, (c // 8,), generator=g, device="cuda:0")
+        view = region.view(2 * S.layers, n, c).view(torch.int64)
+
+        def sums(ids):
+            t = torch.as_tensor(np.asarray(ids, np.int64), device="cuda:0")
+            return torch.stack([(view[j][t] * w).sum(-1) for j in range(2 * S.layers)],
+                               1).cpu().numpy().tolist()
+
+        out = {}
+        if rank == 0:
+            got = []          # (sender, src id, checksum of the received block)
+            for rnd in range(rounds):
+                marks = 0
+                while marks < 2:
+                    _s, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+                    marks += mark is not None
+                pool.sync()
+                msgs = []
+                while True:
+                    m = pool.recv_poll()
+                    if m is None:
+                        break
+                    msgs.append(m)
+                ids = [int(x) for m in msgs for x in M.addr_indices(m[3])]
+                cs = sums(ids) if ids else []
+                k = 0
+                for m in msgs:
+                    srcs = np.frombuffer(m[2], np.int32)
+                    for sid in srcs:
+                        got.append((int(m[1]), int(sid), cs[k]))
+                        k += 1
+                    pool.free_mem(m[3])
+                dist.barrier()
+            out["got"] = got
+            out["arena_wraps_min"] = 0
+        else:
+            rng = np.random.default_rng(rank)
+            src = pool.alloc_mem(n)
+            pool.debug_fill(src, 77)
+            pool.sync()
+            out["sums"] = sums(list(range(n)))
+            for rnd in range(rounds):
+                for _ in range(per_round):
+                    k = int(rng.integers(1, 7))
+                    sel = np.sort(rng.choice(n, k, replace=False))
+                    pool.transfer(0, src[sel], flags=M.XFER_ASYNC,
+                                  priv=sel.astype(np.int32).tobytes())
+                pool.send_mark(0, rnd)
+                dist.barrier()
+        pool.sync()
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+def test_fan_in_two_senders_arena_wraps():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + (os.getpid() % 40)
+    # 2 senders x 160 rounds x 120 transfers x 3.5 blocks ~ 134K receiver ids:
+    # the 65536-id arena wraps twice
+    rounds, per_round = 160, 120
+    ps = [ctx.Process(target=_fanin, args=(r, port, q, rounds, per_round)) for r in range(3)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in ps:
+        r, out = q.get(timeout=900)
+        res[r] = out
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1, 2):
+        assert "error" not in res[r], res[r].get("error")
+    got = res[0]["got"]
+    assert len(got) > 2 * rounds * per_round
+    bad = [(s, i) for s, i, cs in got if res[s]["sums"][i] != cs]
+    assert not bad, f"{len(bad)} of {len(got)} received blocks differ from their sources"
