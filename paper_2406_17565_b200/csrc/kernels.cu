@@ -1,14 +1,20 @@
 // kernels.cu -- sm_100a kernels of libmempool.
 //
-//  * migrate_kernel : the KV-block gather/scatter of the migration path --
-//    pack (A4, pool -> aggregated staging), unpack (A6, staging -> pool), the
-//    fused gather -> (peer) store (A6f, pool -> pool, P2P over NVLink when the
-//    destination slabs live on a peer GPU) and swap (A8/A9, pool <-> mapped
-//    pinned DRAM).  HBM-bound: every chunk is a contiguous run of c bytes
-//    (c = B*H*D*2 = 128 KiB at Llama-2-7B), so each warp streams 4 KiB
-//    pieces with 8 independent 16-byte loads in flight per lane.
+//  * migrate_kernel / migrate_bulk_kernel : the KV-block gather/scatter of
+//    the migration path -- pack (A4, pool -> aggregated staging), unpack (A6,
+//    staging -> pool), the fused gather -> (peer) store (A6f, pool -> pool,
+//    P2P over NVLink when the destination slabs live on a peer GPU) and
+//    DRAM-side copies (A8/A9, mapped pinned DRAM).  HBM-bound: every chunk is
+//    a contiguous run of c bytes (c = B*H*D*2 = 128 KiB at Llama-2-7B).
+//    Two engines: 16-byte vector LD/ST (4 KiB warp units) and a
+//    cp.async.bulk (TMA) ring through shared memory (64 KiB units, one
+//    elected lane per CTA, the default inside one GPU's HBM).  Units are
+//    claimed dynamically from a per-pool device counter (the fast SMs take
+//    more), source ids of short lists come by value in the launch
+//    parameters, destination ids from the device allocator's table.
 //  * alloc_kernel / free_kernel : the device-resident block allocator
-//    (BASELINE.json north_star item 1) over a bitmap, lowest-first.
+//    (BASELINE.json north_star item 1) over a bitmap, lowest-first; pending
+//    frees ride in the allocation kernel's parameters.
 //  * fill_kernel : test/bench-only synthetic KV writer (content model).
 #include <cstdlib>
 
