@@ -334,3 +334,224 @@ def test_fan_in_two_senders_arena_wraps():
     assert len(got) > 2 * rounds * per_round
     bad = [(s, i) for s, i, cs in got if res[s]["sums"][i] != cs]
     assert not bad, f"{len(bad)} of {len(got)} received blocks differ from their sources"
+
+
+# ---------------------------------------------------------------------------
+# Randomized cross-process parity: rank 0 (P) runs a seeded op list -- engine
+# prefill + transfer_with_insert with / without DEDUP, sync / async, swap_out,
+# transfers of swapped-out (DRAM) blocks, deletes -- against rank 1 (D), which
+# serves and, at every end-of-phase mark, frees the partial / plain-transfer
+# blocks it received and deletes some of the prompts.  The parent replays the
+# same list on two oracle pools; per-op results, index dumps, block states and
+# every written block's bytes must match.
+def _rand_ops(seed, n_phases=10, per_phase=14):
+    rng = np.random.default_rng(seed)
+    B = 16
+    base = [rng.integers(3, 40, size=int(rng.integers(2, 5)) * B).astype(np.int32)
+            for _ in range(3)]
+    prompts, phases = [], []
+    for ph in range(n_phases):
+        ops = []
+        for _ in range(per_phase):
+            r = rng.random()
+            if r < 0.6 or not prompts:
+                b = base[int(rng.integers(len(base)))]
+                cut = int(rng.integers(0, len(b) + 1))
+                tail = rng.integers(3, 40, size=int(rng.integers(1, 3 * B))).astype(np.int32)
+                prompts.append(np.concatenate([b[:cut], tail]).astype(np.int32))
+                ops.append(("twi", len(prompts) - 1, bool(rng.random() < 0.6),
+                            bool(rng.random() < 0.5)))
+            elif r < 0.75:
+                ops.append(("swap_out", int(rng.integers(1, 4))))
+            elif r < 0.88:
+                ops.append(("xfer_dram", int(rng.integers(1, 3))))
+            else:
+                ops.append(("p_delete", int(rng.integers(len(prompts)))))
+        phases.append(ops)
+    return prompts, phases
+
+
+def _d_retire(msgs, prompts, phase_ops):
+    """D's end-of-phase work, from its delivered messages (kind 1 =
+    transfer_with_insert, 0 = plain transfer) -- returns the ops to apply."""
+    frees, deletes = [], []
+    twis = [op for op in phase_ops if op[0] == "twi"]
+    k = 0
+    for kind, addrs in msgs:
+        if kind == 0:
+            frees.extend(addrs)
+        else:
+            i = twis[k][1]
+            k += 1
+            if len(prompts[i]) % 16:
+                frees.append(addrs[-1])              # the trailing partial block
+            if i % 2 == 0:
+                deletes.append(i)                    # odd prompts stay cached
+    return frees, deletes
+
+
+def _rand_worker(rank, port, seed, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import TINY as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        prompts, phases = _rand_ops(seed)
+        pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens,
+                      48 if rank == 0 else 24, dram_blocks=12 if rank == 0 else 0, verify=True)
+        blobs = M.exchange_handles(pool)
+        pool.import_peer(blobs[1 - rank][1])
+        dist.barrier()
+        res = []
+        for ph, ops in enumerate(phases):
+            if rank == 0:
+                for op in ops:
+                    try:
+                        if op[0] == "twi":
+                            _, i, dedup, asy = op
+                            t = prompts[i]
+                            _, m = pool.match(t)
+                            new = pool.alloc_mem(-(-len(t) // 16) - len(m))
+                            pool.debug_fill(new, 17565)
+                            full = np.concatenate([m, new])
+                            pool.insert(t, full[: len(t) // 16])
+                            fl = (M.XFER_DEDUP if dedup else 0) | (M.XFER_ASYNC if asy else 0)
+                            fin, moved = pool.transfer_with_insert(1, t, full, flags=fl)
+                            if len(t) % 16:
+                                pool.free_mem(full[-1:])
+                            res.append(("twi", M.addr_indices(fin).tolist(), moved))
+                        elif op[0] == "swap_out":
+                            o, nw = pool.swap_out(op[1])
+                            res.append(("swap_out", M.addr_indices(o).tolist(),
+                                        M.addr_indices(nw).tolist()))
+                        elif op[0] == "xfer_dram":
+                            st = pool.block_states(M.DRAM)
+                            ids = [i for i, s in enumerate(st) if s in (1, 2)][: op[1]]
+                            if ids:
+                                src = np.array([M.make_addr(0, M.DRAM, i) for i in ids],
+                                               np.uint64)
+                                d = pool.transfer(1, src)
+                                res.append(("xfer_dram", ids, M.addr_indices(d).tolist()))
+                        elif op[0] == "p_delete":
+                            pool.delete(prompts[op[1]])
+                    except M.MempoolError as e:
+                        res.append(("error", op[0], e.name))
+                pool.send_mark(1, ph)
+            else:
+                _s, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+                assert mark == ph, (mark, ph)
+                pool.sync()
+                msgs = []
+                while True:
+                    m = pool.recv_poll()
+                    if m is None:
+                        break
+                    msgs.append((m[0], [int(a) for a in m[3]]))
+                frees, deletes = _d_retire(msgs, prompts, ops)
+                if frees:
+                    pool.free_mem(np.array(frees, np.uint64))
+                for i in deletes:
+                    pool.delete(prompts[i])
+            dist.barrier()
+        pool.sync()
+        out = {"res": res, "dump": pool.dump_index(),
+               "states": [pool.block_states(M.HBM).tolist(),
+                          pool.block_states(M.DRAM).tolist() if rank == 0 else []]}
+        out["bytes"] = {}
+        for med in (0, 1):
+            for i, s in enumerate(out["states"][med]):
+                if s != 0:
+                    out["bytes"][(med, i)] = pool.debug_read_block(M.make_addr(rank, med, i))
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+def _rand_oracle(seed):
+    import oracle as O
+    from workloads.configs import TINY as S
+    prompts, phases = _rand_ops(seed)
+    mk = lambda inst, n, nd: O.OraclePool(inst, S.layers, S.kv_heads,  # noqa: E731
+                                          S.head_dim, S.block_tokens, n, n_dram=nd,
+                                          seed=17565)
+    P, D = mk(0, 48, 12), mk(1, 24, 0)   # a small receiver: it evicts (R2, R8)
+    res = []
+    for ph, ops in enumerate(phases):
+        msgs = []
+        for op in ops:
+            try:
+                if op[0] == "twi":
+                    _, i, dedup, _asy = op
+                    t = prompts[i]
+                    _, m = P.match(t)
+                    new = P.alloc_mem(-(-len(t) // 16) - len(m), O.HBM)
+                    P.fill(new)
+                    full = list(m) + new
+                    P.insert(t, full[: len(t) // 16])
+                    fin, moved, _ = O.transfer_with_insert(P, D, t, full,
+                                                           flags=O.FLAG_DEDUP if dedup else 0)
+                    if len(t) % 16:
+                        P.free_mem(full[-1:])
+                    res.append(("twi", [a[2] for a in fin], moved))
+                    msgs.append((1, fin))
+                elif op[0] == "swap_out":
+                    mv = P.swap_out(op[1])
+                    res.append(("swap_out", [o[2] for o, _ in mv], [n[2] for _, n in mv]))
+                elif op[0] == "xfer_dram":
+                    ids = [i for i, s in enumerate(P.state[O.DRAM])
+                           if s in (O.ACTIVE, O.INDEXED)][: op[1]]
+                    if ids:
+                        d = O.transfer(P, D, [(0, O.DRAM, i) for i in ids])
+                        res.append(("xfer_dram", ids, [a[2] for a in d]))
+                        msgs.append((0, d))
+                elif op[0] == "p_delete":
+                    P.delete(prompts[op[1]])
+            except O.MPError as e:
+                res.append(("error", op[0], e.name))
+        frees, deletes = _d_retire(msgs, prompts, ops)
+        if frees:
+            D.free_mem(frees)
+        for i in deletes:
+            D.delete(prompts[i])
+    return P, D, res
+
+
+@pytest.mark.parametrize("seed", [3, 11, 29])
+def test_two_process_random_ops(seed):
+    import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29990 + (os.getpid() % 8) + seed
+    ps = [ctx.Process(target=_rand_worker, args=(r, port, seed, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in ps:
+        r, out = q.get(timeout=600)
+        got[r] = out
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in got[r], got[r].get("error")
+    P, D, res = _rand_oracle(seed)
+    assert got[0]["res"] == res
+    smap = {O.FREE: 0, O.ACTIVE: 1, O.INDEXED: 2, O.ORPHAN: 3}
+    for pool_o, r in ((P, 0), (D, 1)):
+        assert got[r]["dump"] == pool_o.dump_index(), r
+        assert got[r]["states"][0] == [smap[x] for x in pool_o.state[O.HBM]], r
+        if r == 0:
+            assert got[r]["states"][1] == [smap[x] for x in pool_o.state[O.DRAM]]
+        n = 0
+        for (med, i), b in got[r]["bytes"].items():
+            if all(t is not None for t in pool_o.tags[med][i]):
+                assert np.array_equal(b, pool_o.block_bytes((r, med, i))), (r, med, i)
+                n += 1
+        assert n > 0
