@@ -119,15 +119,18 @@ def test_dram_source_memory_asymmetry(path):
 
 
 def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coalesce_mib=0,
-               swap_flags=0, staging_bytes=0):
+               swap_flags=0, staging_bytes=0, n_pools=2):
     rng = np.random.default_rng(seed)
     kw = dict(copy_kernel=copy_kernel, coalesce_mib=coalesce_mib, staging_bytes=staging_bytes)
-    P = Twin(0, shape, n_hbm, n_dram, **kw)
-    D = Twin(1, shape, n_hbm, n_dram, **kw)
-    P.swap_flags = D.swap_flags = swap_flags
-    connect(P, D)
+    twins = [Twin(i, shape, n_hbm, n_dram, **kw) for i in range(n_pools)]
+    for t in twins:
+        t.swap_flags = swap_flags
+    for i in range(n_pools):
+        for j in range(i + 1, n_pools):
+            connect(twins[i], twins[j])
+    P, D = twins[0], twins[1]
     B = shape.block_tokens
-    pools = {0: P, 1: D}
+    pools = dict(enumerate(twins))
     seqs = []
     vocab = 4
 
@@ -140,8 +143,9 @@ def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coa
         return rng.integers(0, vocab, int(rng.integers(1, 6 * B)), dtype=np.int32)
 
     for step in range(n_ops):
-        X = pools[int(rng.integers(2))]
-        Y = D if X is P else P
+        x = int(rng.integers(n_pools))
+        X = pools[x]
+        Y = pools[(x + 1 + int(rng.integers(n_pools - 1))) % n_pools]
         op = rng.random()
         try:
             if op < 0.22:
@@ -207,10 +211,10 @@ def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coa
         except O.MPError:
             pass
         if step % 25 == 24:
-            P.check_state()
-            D.check_state()
-    P.check_state()
-    D.check_state()
+            for t in twins:
+                t.check_state()
+    for t in twins:
+        t.check_state()
 
 
 @pytest.mark.parametrize("path", PATHS + PATHS_ASYNC)
@@ -227,6 +231,18 @@ def test_random_ops_coalesced_launches(path, monkeypatch):
     monkeypatch.setenv("MP_COALESCE_NO_IDLE_FLUSH", "1")
     for seed in range(3):
         random_ops(200 + seed, TINY, 400, path, coalesce_mib=1)
+
+
+@pytest.mark.parametrize("path", [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_FUSED])
+def test_random_ops_three_pools_coalesced(path, monkeypatch):
+    """Three connected pools, transfers between every pair in both
+    directions, size-only coalescing: batches from different sources into one
+    pool, and batches reading a pool while another writes it, must flush in
+    hazard order (batch_open) with the allocator writing into the open
+    batch's id table."""
+    monkeypatch.setenv("MP_COALESCE_NO_IDLE_FLUSH", "1")
+    for seed in range(3):
+        random_ops(500 + seed, TINY, 400, path, coalesce_mib=1, n_pools=3)
 
 
 def test_random_ops_ce_batch_and_swap_ce():
