@@ -120,3 +120,52 @@ def test_static_split_engines():
                         "tests/test_gpu_stress.py::test_bench_pattern_dedup_retire_bytes"],
                        env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_three_pools_crossing_transfers_bytes():
+    """Three pools at host speed, ASYNC transfers between every ordered pair in
+    random order (fan-in from two sources into one pool, opposite directions
+    interleaved): coalesced batches from different sources and batches that
+    read a pool another batch writes must flush in hazard order.  Every
+    received block is compared with its source on the device."""
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    from workloads.configs import LLAMA2_7B as S
+    n, n_src = 512, 160
+    pools = [_pool(M, torch, i, S, n, coalesce_mib=256) for i in range(3)]
+    for i in range(3):
+        for j in range(i + 1, 3):
+            M.connect(pools[i][0], pools[j][0])
+    srcs = []
+    for i, (p, _r) in enumerate(pools):
+        a = p.alloc_mem(n_src)
+        p.debug_fill(a, 100 + i)
+        srcs.append(a)
+    for p, _r in pools:
+        p.sync()
+    rng = np.random.default_rng(9)
+    for rnd in range(5):
+        moves = []
+        for _ in range(60):
+            x = int(rng.integers(3))
+            y = (x + 1 + int(rng.integers(2))) % 3
+            sel = srcs[x][rng.choice(n_src, int(rng.integers(1, 8)), replace=False)]
+            d = pools[x][0].transfer(y, sel, flags=M.XFER_ASYNC)
+            moves.append((x, M.addr_indices(sel), y, d))
+        for p, _r in pools:
+            p.sync()
+        for j in (0, 33, 63):
+            for x in range(3):
+                for y in range(3):
+                    mv = [(s, d) for xx, s, yy, d in moves if xx == x and yy == y]
+                    if not mv:
+                        continue
+                    s_ids = torch.as_tensor(np.concatenate([s for s, _ in mv]), device="cuda:0")
+                    d_ids = torch.as_tensor(np.concatenate([M.addr_indices(d) for _, d in mv]),
+                                            device="cuda:0")
+                    bad = (pools[y][1][j, d_ids] != pools[x][1][j, s_ids]).any(dim=1)
+                    assert not bool(bad.any()), f"round {rnd}: {x}->{y} chunk {j}"
+        for x, _s, y, d in moves:
+            pools[y][0].free_mem(d)
+    for p, _r in pools:
+        p.close()
