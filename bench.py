@@ -150,7 +150,15 @@ class Clocks:
 
 
 def make_pool(M, torch, inst, dev, shape, n_blocks, **kw):
-    """HBM slabs are torch allocations (PyTorch owns device memory)."""
+    """HBM slabs are torch allocations (PyTorch owns device memory).  With the
+    caching allocator's expandable segments (cuMemMap-backed, no CUDA-IPC
+    handle) the library cudaMallocs the slabs itself, so the cross-process
+    path can still export them."""
+    if "expandable_segments:true" in os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "").lower():
+        p = M.Pool(inst, dev, shape.layers, shape.kv_heads, shape.head_dim, shape.block_tokens,
+                   n_blocks, **kw)
+        p._region = None
+        return p
     c = shape.chunk_bytes
     region = torch.empty(2 * shape.layers * n_blocks * c, dtype=torch.uint8, device=f"cuda:{dev}")
     slabs = [region.data_ptr() + j * n_blocks * c for j in range(2 * shape.layers)]
