@@ -22,23 +22,45 @@
 #include <cstring>
 #include <map>
 #include <memory>
-#include <string>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "../../include/mempool.h"
 
 namespace {
 
+// One trie node per block-aligned prefix.  Children are found by a 64-bit
+// hash of the block's tokens (confirmed token by token); holders are a short
+// unsorted list (a handful of instances per prefix).
 struct GsNode {
-  std::unordered_map<std::string, std::unique_ptr<GsNode>> kids;  // key: the B tokens
-  std::map<int32_t, double> holders;                               // instance -> expiry
+  std::vector<mp_token> chunk;                                   // the B tokens
+  std::unordered_multimap<uint64_t, std::unique_ptr<GsNode>> kids;
+  std::vector<std::pair<int32_t, double>> holders;                // instance -> expiry
 };
 
 struct Inst {
   int32_t kind = 0;
   double load = 0.0;
 };
+
+uint64_t chunk_hash(const mp_token* t, int32_t B) {
+  uint64_t h = 1469598103934665603ull;
+  for (int32_t i = 0; i < B; ++i) {
+    h ^= (uint32_t)t[i];
+    h *= 1099511628211ull;
+    h ^= h >> 29;
+  }
+  return h;
+}
+
+GsNode* find_kid(const GsNode* n, const mp_token* t, int32_t B, uint64_t h) {
+  auto range = n->kids.equal_range(h);
+  for (auto it = range.first; it != range.second; ++it)
+    if (std::memcmp(it->second->chunk.data(), t, sizeof(mp_token) * (size_t)B) == 0)
+      return it->second.get();
+  return nullptr;
+}
 
 }  // namespace
 
@@ -51,20 +73,23 @@ struct mp_gs {
 
 namespace {
 
-std::string chunk_key(const mp_token* t, int32_t B) {
-  return std::string((const char*)t, (size_t)B * sizeof(mp_token));
-}
-
 // Deepest unexpired prefix (in blocks) held by every instance of one tree.
 void tree_match(const mp_gs* g, const GsNode* root, const mp_token* toks, int64_t n_tok,
-                double now, std::map<int32_t, int64_t>* best) {
+                double now, std::vector<std::pair<int32_t, int64_t>>* best) {
   const GsNode* cur = root;
   for (int64_t i = 0; i < n_tok / g->B; ++i) {
-    auto it = cur->kids.find(chunk_key(toks + i * g->B, g->B));
-    if (it == cur->kids.end()) break;
-    cur = it->second.get();
-    for (const auto& h : cur->holders)
-      if (h.second > now) (*best)[h.first] = i + 1;
+    const mp_token* t = toks + i * g->B;
+    cur = find_kid(cur, t, g->B, chunk_hash(t, g->B));
+    if (!cur) break;
+    for (const auto& h : cur->holders) {
+      if (!(h.second > now)) continue;
+      auto it = std::find_if(best->begin(), best->end(),
+                             [&](const std::pair<int32_t, int64_t>& b) { return b.first == h.first; });
+      if (it == best->end())
+        best->push_back({h.first, i + 1});
+      else
+        it->second = i + 1;
+    }
   }
 }
 
@@ -100,10 +125,22 @@ mp_status mp_gs_update(mp_gs* g, int32_t instance, const mp_token* toks, int64_t
   if (!g || n_tok < 0 || (n_tok > 0 && !toks) || !g->insts.count(instance)) return MP_ERR_CONFIG;
   GsNode* cur = &g->roots[g->insts[instance].kind];
   for (int64_t i = 0; i < n_tok / g->B; ++i) {
-    auto& slot = cur->kids[chunk_key(toks + i * g->B, g->B)];
-    if (!slot) slot.reset(new GsNode());
-    cur = slot.get();
-    cur->holders[instance] = now + g->ttl;
+    const mp_token* t = toks + i * g->B;
+    const uint64_t h = chunk_hash(t, g->B);
+    GsNode* nx = find_kid(cur, t, g->B, h);
+    if (!nx) {
+      std::unique_ptr<GsNode> fresh(new GsNode());
+      fresh->chunk.assign(t, t + g->B);
+      nx = fresh.get();
+      cur->kids.emplace(h, std::move(fresh));
+    }
+    cur = nx;
+    auto it = std::find_if(cur->holders.begin(), cur->holders.end(),
+                           [&](const std::pair<int32_t, double>& x) { return x.first == instance; });
+    if (it == cur->holders.end())
+      cur->holders.push_back({instance, now + g->ttl});
+    else
+      it->second = now + g->ttl;
   }
   return MP_OK;
 }
@@ -113,14 +150,17 @@ mp_status mp_gs_route(mp_gs* g, int32_t kind, const mp_token* toks, int64_t n_to
                       int64_t* extra_tokens, int64_t cap, int64_t* n_extra) {
   if (!g || kind < 0 || kind > 2 || n_tok < 0 || (n_tok > 0 && !toks) || !instance)
     return MP_ERR_CONFIG;
-  std::map<int32_t, int64_t> got;  // instance -> blocks, all tree types ("concurrently")
+  // instance -> blocks, all tree types ("concurrently")
+  std::vector<std::pair<int32_t, int64_t>> got;
   for (int t = 0; t < 3; ++t) tree_match(g, &g->roots[t], toks, n_tok, now, &got);
   int32_t pick = -1;
   int64_t pick_blocks = -1;
   double pick_load = 0.0;
   for (const auto& kv : g->insts) {
     if (kv.second.kind != kind) continue;
-    auto it = got.find(kv.first);
+    auto it = std::find_if(got.begin(), got.end(), [&](const std::pair<int32_t, int64_t>& x) {
+      return x.first == kv.first;
+    });
     const int64_t b = it == got.end() ? 0 : it->second;
     if (b > pick_blocks || (b == pick_blocks && kv.second.load < pick_load)) {
       pick = kv.first;

@@ -505,6 +505,7 @@ class GlobalScheduler:
 
     def register(self, instance: int, kind: int):
         _check(_lib.mp_gs_register(self._h, instance, kind), "gs_register")
+        self._n_inst = getattr(self, "_n_inst", 0) + 1
 
     def set_load(self, instance: int, load: float):
         _check(_lib.mp_gs_set_load(self._h, instance, load), "gs_set_load")
@@ -519,12 +520,11 @@ class GlobalScheduler:
         inst = C.c_int32(-1)
         mt = C.c_int64(0)
         n = C.c_int64(0)
+        cap = max(getattr(self, "_n_inst", 0), 1)   # extra holders <= registered instances
+        ei = np.zeros(cap, np.int32)
+        et = np.zeros(cap, np.int64)
         _check(_lib.mp_gs_route(self._h, kind, _pi32(t), len(t), now, C.byref(inst),
-                                C.byref(mt), None, None, 0, C.byref(n)), "gs_route")
-        ei = np.zeros(max(n.value, 1), np.int32)
-        et = np.zeros(max(n.value, 1), np.int64)
-        _check(_lib.mp_gs_route(self._h, kind, _pi32(t), len(t), now, C.byref(inst),
-                                C.byref(mt), _pi32(ei), et.ctypes.data_as(_PI64), len(ei),
+                                C.byref(mt), _pi32(ei), et.ctypes.data_as(_PI64), cap,
                                 C.byref(n)), "gs_route")
         return inst.value, mt.value, [(int(ei[i]), int(et[i])) for i in range(n.value)]
 

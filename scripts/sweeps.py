@@ -226,6 +226,43 @@ def dram_source_sweep():
     return out
 
 
+def gs_latency():
+    """global prompt trees, host-only.  8 instances
+    (4 prefill, 4 decode), ShareGPT-like sessions: every turn routes its
+    prompt to a prefill instance and the chosen instance's tree is updated
+    (P:645); per-call host time vs the number of prompts held."""
+    from workloads import traces
+    gs = M.GlobalScheduler(16, 3600.0)
+    for i in range(8):
+        gs.register(i, gs.PREFILL if i < 4 else gs.DECODE)
+    sessions = traces.sharegpt_like(seed_for(1), n_sessions=3000)
+    prompts = [t.prompt for s_ in sessions for t in s_.turns]
+    out = {"workload": "global scheduler: 8 instances, ShareGPT-like prompts (route to a "
+                       "prefill instance, then update its tree)", "results": []}
+    now, done, t_route, t_upd = 0.0, 0, 0.0, 0.0
+    marks = {500, 2000, 5000, len(prompts)}
+    for p_ in prompts:
+        now += 0.001
+        t0 = time.perf_counter()
+        inst, mt, extra = gs.route(gs.PREFILL, p_, now)
+        t1 = time.perf_counter()
+        gs.update(inst, p_, now)
+        gs.update(4 + inst, p_, now)          # its decode partner holds it too
+        t2 = time.perf_counter()
+        t_route += t1 - t0
+        t_upd += (t2 - t1) / 2
+        done += 1
+        if done in marks:
+            out["results"].append({"prompts_seen": done,
+                                   "route_us": round(t_route / done * 1e6, 2),
+                                   "update_us": round(t_upd / done * 1e6, 2),
+                                   "avg_prompt_tokens": int(np.mean([len(x) for x in
+                                                                     prompts[:done]]))})
+            print(json.dumps(out["results"][-1]), file=sys.stderr)
+    gs.close()
+    return out
+
+
 def api_latency():
     """The paper's MemPool API study: memory-API latency vs block
     count ("~800 ns per block, linear") and index insert / match of a 4K-token
@@ -282,5 +319,5 @@ def api_latency():
 
 if __name__ == "__main__":
     fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency,
-          "dram_source": dram_source_sweep}[sys.argv[1]]
+          "dram_source": dram_source_sweep, "gs": gs_latency}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))
