@@ -480,8 +480,23 @@ class Index {
     return map_.find(mix(p->id, hash_chunk(toks)), p, toks, B_);
   }
 
+  // Keep the longer of the memo and this path when one extends the other
+  // (match then insert of one prompt, a next turn's longer prompt): only the
+  // new tail is copied.  Equal node pointers mean equal prefixes.
   void remember(const int32_t* toks, const std::vector<Node*>& nodes) const {
-    memo_toks_.assign(toks, toks + nodes.size() * (size_t)B_);
+    const size_t k = nodes.size(), m = memo_nodes_.size();
+    if (memo_unlinks_ == unlinks_) {
+      size_t h = 0;
+      const size_t c = std::min(k, m);
+      while (h < c && memo_nodes_[h] == nodes[h]) ++h;
+      if (h == k) return;  // a prefix of the memo
+      if (h == m) {        // extends the memo
+        memo_nodes_.insert(memo_nodes_.end(), nodes.begin() + (std::ptrdiff_t)m, nodes.end());
+        memo_toks_.insert(memo_toks_.end(), toks + m * (size_t)B_, toks + k * (size_t)B_);
+        return;
+      }
+    }
+    memo_toks_.assign(toks, toks + k * (size_t)B_);
     memo_nodes_ = nodes;
     memo_unlinks_ = unlinks_;
   }
