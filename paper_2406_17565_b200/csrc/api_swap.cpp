@@ -62,24 +62,42 @@ mp_status mp_swap_out(mp_pool* p, int64_t n, uint32_t flags, mp_addr* out_old, m
     ds.push_back(it->second);
   }
   if (!hs.empty() && use_ce(p, flags)) {
-    // pack into device staging (aggregated), then one copy-engine
-    // D2H per block; the victims stay allocated on the device bitmap until
-    // the queued frees are flushed behind these copies (sync below)
-    const int64_t k = std::max<int64_t>(1, p->staging_bytes / p->Pb);
+    // pack into device staging (aggregated), then copy-engine D2H
+    // (one copy per run of consecutive DRAM blocks) on the copy stream; the
+    // two halves of the staging alternate so the next pack overlaps the
+    // current D2H.  The victims stay allocated on the device bitmap until the
+    // queued frees are flushed behind these copies (sync below).
     if (p->staging_bytes < p->Pb) {
       set_err("staging smaller than one block");
       return MP_ERR_CONFIG;
     }
-    for (size_t b0 = 0; b0 < hs.size(); b0 += (size_t)k) {
+    const int64_t per = p->staging_bytes / p->Pb;
+    const int halves = per >= 2 ? 2 : 1;
+    const int64_t k = per / halves;
+    TRY(meta_fence(p));
+    for (size_t b0 = 0, r = 0; b0 < hs.size(); b0 += (size_t)k, ++r) {
       const size_t nb = std::min(hs.size() - b0, (size_t)k);
+      const int h = (int)(r % (size_t)halves);
+      char* stg = p->staging + (int64_t)h * k * p->Pb;
+      if (r >= (size_t)halves) CK(cudaStreamWaitEvent(p->stream, p->swap_ev[2 + h], 0));
       int* dh = nullptr;
-      TRY(upload_ids(p, std::vector<int32_t>(hs.begin() + b0, hs.begin() + b0 + nb), &dh));
-      TRY(launch_migrate_timed(p, p->stream, pool_ep(p->d_slabs, dh),
-                               agg_ep(p->staging, p->Pb, nullptr), (int64_t)nb, 0, p->nch));
-      for (size_t i = 0; i < nb; ++i)
-        CK(cudaMemcpyAsync(p->dram + (int64_t)ds[b0 + i] * p->Pb, p->staging + i * p->Pb,
-                           (size_t)p->Pb, cudaMemcpyDeviceToHost, p->stream));
+      mpk::InlineIds si;
+      TRY(src_ids(p, std::vector<int32_t>(hs.begin() + b0, hs.begin() + b0 + nb), &dh, &si));
+      TRY(launch_migrate_timed(p, p->stream, pool_ep(p->d_slabs, dh), agg_ep(stg, p->Pb, nullptr),
+                               (int64_t)nb, 0, p->nch, false, 0, si.n ? &si : nullptr));
+      CK(cudaEventRecord(p->swap_ev[h], p->stream));
+      CK(cudaStreamWaitEvent(p->copy_stream, p->swap_ev[h], 0));
+      for (size_t i = 0; i < nb;) {
+        size_t j = i + 1;
+        while (j < nb && ds[b0 + j] == ds[b0 + j - 1] + 1) ++j;
+        CK(cudaMemcpyAsync(p->dram + (int64_t)ds[b0 + i] * p->Pb, stg + (int64_t)i * p->Pb,
+                           (size_t)p->Pb * (j - i), cudaMemcpyDeviceToHost, p->copy_stream));
+        i = j;
+      }
+      CK(cudaEventRecord(p->swap_ev[2 + h], p->copy_stream));
     }
+    CK(cudaEventRecord(p->swap_ev[0], p->copy_stream));   // join: the data stream
+    CK(cudaStreamWaitEvent(p->stream, p->swap_ev[0], 0));  // waits for every D2H
   } else if (!hs.empty()) {
     int *dh = nullptr, *dd = nullptr;
     TRY(upload_ids(p, hs, &dh));
@@ -126,14 +144,32 @@ mp_status mp_swap_in(mp_pool* p, const mp_addr* a, int64_t n, uint32_t flags, mp
       set_err("staging smaller than one block");
       return MP_ERR_CONFIG;
     }
-    const int64_t k = p->staging_bytes / p->Pb;
-    for (int64_t b0 = 0; b0 < n; b0 += k) {
+    // H2D (one copy per run of consecutive DRAM blocks) into one half of the
+    // staging on the copy stream while the data stream unpacks the other
+    const int64_t per = p->staging_bytes / p->Pb;
+    const int halves = per >= 2 ? 2 : 1;
+    const int64_t k = per / halves;
+    TRY(meta_fence(p));   // the allocation above (dh) is on the meta stream
+    CK(cudaEventRecord(p->swap_ev[0], p->stream));         // everything earlier on
+    CK(cudaStreamWaitEvent(p->copy_stream, p->swap_ev[0], 0));  // the pool goes first
+    for (int64_t b0 = 0, r = 0; b0 < n; b0 += k, ++r) {
       const int64_t nb = std::min(n - b0, k);
-      for (int64_t i = 0; i < nb; ++i)
-        CK(cudaMemcpyAsync(p->staging + i * p->Pb, p->dram + (int64_t)dids[(size_t)(b0 + i)] * p->Pb,
-                           (size_t)p->Pb, cudaMemcpyHostToDevice, p->stream));
-      TRY(launch_migrate_timed(p, p->stream, agg_ep(p->staging, p->Pb, nullptr),
+      const int h = (int)(r % halves);
+      char* stg = p->staging + (int64_t)h * k * p->Pb;
+      if (r >= halves) CK(cudaStreamWaitEvent(p->copy_stream, p->swap_ev[2 + h], 0));
+      for (int64_t i = 0; i < nb;) {
+        int64_t j = i + 1;
+        while (j < nb && dids[(size_t)(b0 + j)] == dids[(size_t)(b0 + j - 1)] + 1) ++j;
+        CK(cudaMemcpyAsync(stg + i * p->Pb, p->dram + (int64_t)dids[(size_t)(b0 + i)] * p->Pb,
+                           (size_t)p->Pb * (size_t)(j - i), cudaMemcpyHostToDevice,
+                           p->copy_stream));
+        i = j;
+      }
+      CK(cudaEventRecord(p->swap_ev[h], p->copy_stream));
+      CK(cudaStreamWaitEvent(p->stream, p->swap_ev[h], 0));
+      TRY(launch_migrate_timed(p, p->stream, agg_ep(stg, p->Pb, nullptr),
                                pool_ep(p->d_slabs, dh + b0), nb, 0, p->nch));
+      CK(cudaEventRecord(p->swap_ev[2 + h], p->stream));
     }
   } else {
     TRY(upload_ids(p, dids, &dd));

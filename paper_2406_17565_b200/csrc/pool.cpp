@@ -526,6 +526,8 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->ev_meta) cudaEventDestroy(p->ev_meta);
     if (p->ev_ipc) cudaEventDestroy(p->ev_ipc);
     for (auto e : p->slot_ev) cudaEventDestroy(e);
+    for (auto e : p->swap_ev)
+      if (e) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->meta) cudaStreamDestroy(p->meta);
@@ -622,6 +624,7 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->uid = new_uid();
   p->slot_ev.resize((size_t)p->staging_slots);
   for (auto& e : p->slot_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : p->swap_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   p->tev.resize(2 * (size_t)kTimedPairs);
   for (auto& e : p->tev) CKC(cudaEventCreate(&e));
   p->slabs.resize((size_t)p->nch);

@@ -163,6 +163,9 @@ struct mp_pool {
   cudaStream_t stream = nullptr, meta = nullptr, copy_stream = nullptr;
   cudaEvent_t ev_order = nullptr, ev_meta = nullptr;
   std::vector<cudaEvent_t> slot_ev;
+  // swap through device staging, double-buffered: [0,1] the halves' fill done
+  // (pack / H2D), [2,3] their drain done (D2H / unpack)
+  cudaEvent_t swap_ev[4] = {};
   // profiling: a ring of (start, end) event pairs per migration launch
   bool profiling = false;
   std::vector<cudaEvent_t> tev;
