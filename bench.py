@@ -472,8 +472,10 @@ def swap_point(M, torch, shape, seed):
         t2 = time.perf_counter()
         res[f"n{n}"] = {"swap_out_GBps": round(len(old) * Pb / (t1 - t0) / 1e9, 2),
                         "swap_in_GBps": round(len(back) * Pb / (t2 - t1) / 1e9, 2),
-                        "path": "default swap transport: pack into device staging + "
-                                "copy-engine D2H/H2D per aggregated block",
+                        "path": "default swap transport: double-buffered device staging "
+                                "(pack / unpack of one half overlaps the copy-engine D2H / "
+                                "H2D of the other, one copy per run of consecutive DRAM "
+                                "blocks)",
                         "bound": "PCIe Gen5 x16 (pinned 1 GiB memcpy ~56 GB/s on this box)"}
     S.close()
     return res
