@@ -27,8 +27,9 @@
  *    receiver's allocation, insert and `private` delivery -- is already done);
  *    mp_sync(pool) waits for it.  Every later call on either pool is
  *    stream-ordered after it, and mp_alloc_mem drains the pool before handing
- *    blocks to the caller (unless MP_ALLOC_STREAM_ORDERED, see there).  Frees of HBM blocks are applied to the device
- *    bitmap lazily, stream-ordered before the pool's next allocation.
+ *    blocks to the caller (unless MP_ALLOC_STREAM_ORDERED, see there).  Frees
+ *    of HBM blocks (and mp_alloc_mem's claims) are applied to the device
+ *    bitmap lazily, stream-ordered before the pool's next device allocation.
  *  - Layout: the HBM pool of an instance is 2*L "slabs" (K_0, V_0, K_1, V_1,
  *    ...), each hbm_blocks chunks of c = B*H*D*elem bytes (vLLM's per-layer
  *    paged layout: "two blocks per LLM layer").  Block id b is chunk b
@@ -187,8 +188,11 @@ const char* mp_last_error(void); /* thread-local detail of the last failure */
 /* alloc_mem(size, type, id): the n lowest-index free blocks, ascending; MIXED
  * takes HBM first then DRAM; on shortage evicts unreferenced
  * historical blocks of that medium first, else MP_ERR_OOM.  HBM ids
- * come from the device bitmap allocator.  requester_id is recorded as the
- * allocating instance.  out: n addrs. */
+ * follow the device bitmap allocator's lowest-first rule; here the host
+ * shadow picks them (nothing on the device reads them) and the claim reaches
+ * the device bitmap with its next stream-ordered update -- no kernel launch
+ * per call.  The receiver's allocations inside a transfer run on the device.
+ * requester_id is recorded as the allocating instance.  out: n addrs. */
 mp_status mp_alloc_mem(mp_pool* pool, int64_t n, int32_t type, int32_t requester_id,
                        mp_addr* out);
 /* OR'd into alloc_mem's `type`: return without draining the pool (the

@@ -9,6 +9,7 @@ depend on torch's copy of libcudart.
 import os
 import subprocess
 import sys
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -29,6 +30,12 @@ NVCC_FLAGS = [
 ]
 
 
+# CPython binding of the per-request calls (csrc/pyfast.c), linked against the
+# library above (rpath $ORIGIN: both live in _lib/).
+PYEXT_SRC = os.path.join(CSRC, "pyfast.c")
+PYEXT = os.path.join(LIBDIR, "_mpfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
 def _nvcc():
     cand = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
     return cand if os.path.exists(cand) else "nvcc"
@@ -43,8 +50,32 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def pyext_stale() -> bool:
+    if not os.path.exists(PYEXT):
+        return True
+    t = os.path.getmtime(PYEXT)
+    return any(os.path.getmtime(d) > t for d in (PYEXT_SRC, LIB, os.path.join(INCLUDE, "mempool.h")))
+
+
+def build_pyext(verbose: bool = False) -> str:
+    import numpy
+    tmp = PYEXT + ".tmp"
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-Wno-missing-field-initializers",
+           "-I", sysconfig.get_paths()["include"], "-I", numpy.get_include(), "-I", INCLUDE,
+           PYEXT_SRC, "-o", tmp, "-L", LIBDIR, "-lmempool", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError("gcc failed building the _mpfast binding")
+    os.replace(tmp, PYEXT)
+    return PYEXT
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
+        if pyext_stale():
+            build_pyext(verbose)
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
@@ -58,6 +89,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(tmp, LIB)
     with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
         f.write(res.stderr)
+    build_pyext(verbose)
     return LIB
 
 

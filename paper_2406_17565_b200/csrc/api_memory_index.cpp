@@ -84,7 +84,9 @@ mp_status mp_alloc_mem(mp_pool* p, int64_t n, int32_t type, int32_t requester, m
   if (p->nfree[MP_DRAM] < nd) evict_internal(p, nd - p->nfree[MP_DRAM], MP_DRAM, nullptr);
   std::vector<int32_t> ids;
   int* d = nullptr;
-  TRY(alloc_hbm(p, nh, requester, &ids, &d));
+  // nothing on the device reads these ids: no allocation kernel, the device
+  // bitmap learns the claim with its next update
+  TRY(alloc_hbm(p, nh, requester, &ids, &d, /*defer=*/true));
   // The caller will write these blocks from its own streams: every earlier
   // device op of this pool (e.g. an async copy still reading a block that was
   // freed since) must be complete first -- unless the caller orders its

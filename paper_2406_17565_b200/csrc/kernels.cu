@@ -284,14 +284,21 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
 // Single CTA of 1024 threads: popcount per thread-range of words, block-wide
 // exclusive scan, then every thread emits its lowest set bits in order, so
 // the ids come out ascending (R2 lowest-first).
+// One pending bitmap update: id >= 0 frees (bit := 1), -(id+1) claims (bit := 0).
+__device__ __forceinline__ void apply_update(uint32_t* bitmap, int e) {
+  if (e >= 0) atomicOr(bitmap + (e >> 5), 1u << (e & 31));
+  else atomicAnd(bitmap + ((-e - 1) >> 5), ~(1u << ((-e - 1) & 31)));
+}
+
 __global__ void __launch_bounds__(1024) alloc_kernel(uint32_t* bitmap, int nwords, int n,
                                                      int* out_dev, int* out_host, int* err,
                                                      const InlineIds frees) {
   __shared__ int warp_tot[32];
   const int t = threadIdx.x;
-  // frees queued since the last allocation go first (lowest-first reuses them)
-  for (int i = t; i < frees.n; i += blockDim.x)
-    atomicOr(bitmap + (frees.ids[i] >> 5), 1u << (frees.ids[i] & 31));
+  // updates queued since the last allocation go first (lowest-first reuses
+  // the frees): id >= 0 sets its bit (a free), -(id+1) clears it (a claim
+  // made on the host by mp_alloc_mem); the two sets are disjoint
+  for (int i = t; i < frees.n; i += blockDim.x) apply_update(bitmap, frees.ids[i]);
   __syncthreads();
   const int wpt = (nwords + blockDim.x - 1) / blockDim.x;
   const int w0 = min(nwords, t * wpt), w1 = min(nwords, w0 + wpt);
@@ -339,15 +346,12 @@ __global__ void __launch_bounds__(1024) alloc_kernel(uint32_t* bitmap, int nword
 }
 
 __global__ void free_inline_kernel(uint32_t* bitmap, const InlineIds frees) {
-  for (int i = threadIdx.x; i < frees.n; i += blockDim.x)
-    atomicOr(bitmap + (frees.ids[i] >> 5), 1u << (frees.ids[i] & 31));
+  for (int i = threadIdx.x; i < frees.n; i += blockDim.x) apply_update(bitmap, frees.ids[i]);
 }
 
 __global__ void free_kernel(uint32_t* bitmap, const int* ids, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int id = ids[i];
-    atomicOr(bitmap + (id >> 5), 1u << (id & 31));
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    apply_update(bitmap, ids[i]);
 }
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {

@@ -60,15 +60,16 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
 
 
 // Lowest-first allocation of n blocks from a bitmap (bit = 1: free), after
-// setting the bits of `frees` (nullable; applied first, so lowest-first sees
-// them).  Writes the ids ascending into out_dev (device) and out_host (mapped
+// applying `frees` (nullable; applied first, so lowest-first sees them):
+// an entry id >= 0 sets bit id, an entry -(id+1) clears it (a claim made on
+// the host; the two sets are disjoint).  Writes the ids ascending into out_dev (device) and out_host (mapped
 // pinned host, may be nullptr), clears their bits.  *err (device) := 1 if
 // fewer than n were free (the host shadow makes this impossible; checked in
 // verify mode).  n == 0 with frees: just the frees.
 cudaError_t launch_alloc(uint32_t* bitmap, int nwords, int n, int* out_dev, int* out_host,
                          int* err, cudaStream_t stream, const InlineIds* frees = nullptr);
 
-// Sets the bits of ids[0..n) (device array).
+// Applies the updates ids[0..n) (device array; same encoding as `frees`).
 cudaError_t launch_free(uint32_t* bitmap, const int* ids, int n, cudaStream_t stream);
 
 // Synthetic KV write of n blocks (content model):

@@ -85,30 +85,44 @@ mp_status src_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d, mpk::Inl
 // Frees of HBM blocks reach the device bitmap lazily, on the meta stream:
 // small sets by value in a kernel's parameters (folded into the next
 // allocation when there is one), large ones through the id arena.
-static bool take_inline_frees(mp_pool* p, mpk::InlineIds* f) {
-  f->n = 0;
-  if (p->pending_free.empty() || (int)p->pending_free.size() > mpk::kInlineIds) return false;
-  f->n = (int)p->pending_free.size();
-  std::memcpy(f->ids, p->pending_free.data(), p->pending_free.size() * sizeof(int32_t));
+// Deferred claims (mp_alloc_mem) travel the same way, encoded -(id+1).
+static void take_pending(mp_pool* p, std::vector<int32_t>* out) {
+  out->clear();
+  for (int32_t id : p->pending_free) {
+    uint8_t& d = p->dev_pend[(size_t)id];
+    if (d == DEV_FREE) out->push_back(id);
+    else if (d == DEV_CLAIM) out->push_back(-id - 1);
+    d = DEV_NONE;  // later duplicates of this id are stale
+  }
   p->pending_free.clear();
-  return true;
 }
 
-mp_status flush_frees(mp_pool* p) {
+// Applies every pending update before the next device-bitmap scan: a short
+// list is returned in *f for the caller's allocation kernel (f nullable:
+// launched here), a long one goes through the id arena now.
+static mp_status apply_pending(mp_pool* p, mpk::InlineIds* f) {
+  if (f) f->n = 0;
   if (p->pending_free.empty()) return MP_OK;
-  mpk::InlineIds f;
-  if (take_inline_frees(p, &f)) {
-    CK(mpk::launch_alloc(p->d_bitmap, p->nwords, 0, nullptr, nullptr, p->d_err, p->meta, &f));
+  std::vector<int32_t> v;
+  take_pending(p, &v);
+  if (v.empty()) return MP_OK;  // everything cancelled out
+  if ((int)v.size() <= mpk::kInlineIds) {
+    mpk::InlineIds local;
+    mpk::InlineIds* g = f ? f : &local;
+    g->n = (int)v.size();
+    std::memcpy(g->ids, v.data(), v.size() * sizeof(int32_t));
+    if (f) return MP_OK;
+    CK(mpk::launch_alloc(p->d_bitmap, p->nwords, 0, nullptr, nullptr, p->d_err, p->meta, g));
   } else {
-    std::vector<int32_t> ids;
-    ids.swap(p->pending_free);
     int* d = nullptr;
-    TRY(upload_ids(p, ids, &d));
-    CK(mpk::launch_free(p->d_bitmap, d, (int)ids.size(), p->meta));
+    TRY(upload_ids(p, v, &d));
+    CK(mpk::launch_free(p->d_bitmap, d, (int)v.size(), p->meta));
   }
   p->stats.aux_launches += 1;
   return MP_OK;
 }
+
+mp_status flush_frees(mp_pool* p) { return apply_pending(p, nullptr); }
 
 mp_status drain(mp_pool* p) {
   TRY(remote_apply_waits(p));  // blocks stored by other processes have landed too
@@ -322,7 +336,13 @@ void free_block(mp_pool* p, int med, int32_t idx) {
   ++p->nfree[med];
   if (med == MP_HBM) {
     p->hfree[(size_t)idx >> 6] |= 1ull << (idx & 63);
-    p->pending_free.push_back(idx);  // device bitmap: stream-ordered, lazily
+    uint8_t& d = p->dev_pend[(size_t)idx];
+    if (d == DEV_CLAIM) {  // claimed on the host only: the device bit is still 1
+      d = DEV_NONE;
+    } else {
+      d = DEV_FREE;
+      p->pending_free.push_back(idx);  // device bitmap: stream-ordered, lazily
+    }
   } else {
     p->dram_free.insert(idx);
   }
@@ -346,7 +366,7 @@ bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>
 }
 
 mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,
-                    int** d_ids) {
+                    int** d_ids, bool defer) {
   ids->clear();
   if (n > p->nfree[MP_HBM]) {
     set_err("alloc_hbm: host shadow short");
@@ -374,10 +394,25 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
   bool hazard = false;
   for (int32_t id : *ids) hazard = hazard || p->pend_w[(size_t)id] || p->pend_r[(size_t)id];
   if (hazard) TRY(flush_involving(p));
+  if (defer) {
+    for (int32_t id : *ids) {
+      uint8_t& dp = p->dev_pend[(size_t)id];
+      if (dp == DEV_FREE) {  // freed on the host only: the device bit is still 0
+        dp = DEV_NONE;
+      } else {
+        dp = DEV_CLAIM;
+        p->pending_free.push_back(id);
+      }
+    }
+    // keep the pending list bounded (stale entries and long claim runs)
+    if (p->pending_free.size() > (size_t)4 * mpk::kInlineIds) TRY(flush_frees(p));
+    *d_ids = nullptr;
+    return MP_OK;
+  }
   // the device bitmap must see every earlier free first: small sets ride in
   // the allocation kernel's parameters
   mpk::InlineIds f;
-  if (!take_inline_frees(p, &f)) TRY(flush_frees(p));
+  TRY(apply_pending(p, &f));
   int* h = nullptr;
   int* d = arena_take(p, n, &h);
   if (!d) {
@@ -663,6 +698,7 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->batch_limit = (uint64_t)(cfg->coalesce_mib > 0 ? cfg->coalesce_mib : 1024) << 20;
   p->batch_cap = p->n_hbm;
   p->pend_w.assign((size_t)p->n_hbm, 0);
+  p->dev_pend.assign((size_t)p->n_hbm, 0);
   p->pend_r.assign((size_t)p->n_hbm, 0);
   for (int k = 0; k < mp_pool::kBatchTabs; ++k) {
     CKC(cudaMalloc(&p->bsrc_ring[k], sizeof(int) * (size_t)p->batch_cap));

@@ -35,6 +35,7 @@ void set_err(const std::string& s);
 const std::string& get_err();
 
 enum : uint8_t { ST_FREE = 0, ST_ACTIVE = 1, ST_INDEXED = 2, ST_ORPHAN = 3 };
+enum : uint8_t { DEV_NONE = 0, DEV_FREE = 1, DEV_CLAIM = 2 };  // mp_pool::dev_pend
 
 struct DevGuard {
   int prev = -1, want;
@@ -179,7 +180,13 @@ struct mp_pool {
   std::vector<uint64_t> hfree;             // HBM shadow bitmap (bit = 1: free)
   std::set<int32_t> dram_free;             // host-managed pinned DRAM allocator
   std::map<int32_t, int32_t> orphan_ref[2];
-  std::vector<int32_t> pending_free;       // HBM ids to set in the device bitmap
+  // Device-bitmap updates not applied yet (stream-ordered, lazily): ids whose
+  // dev_pend is DEV_FREE (host freed, device bit still 0) or DEV_CLAIM (taken
+  // by mp_alloc_mem on the host, device bit still 1).  A free and a claim of
+  // the same id cancel, so the pending set is order-free; entries whose
+  // dev_pend no longer matches are stale and skipped.
+  std::vector<int32_t> pending_free;
+  std::vector<uint8_t> dev_pend;
   std::vector<uint32_t> mark[2];           // scratch duplicate marks (next_mark)
   uint32_t mark_gen = 0;
   std::vector<mp::PendingVerify> pending_verify;
@@ -255,8 +262,10 @@ bool can_make_room(mp_pool* p, int64_t n, int med, const std::vector<mpi::Node*>
 // the same ids into HBM (d_ids) for the kernels that follow on the stream.
 mp_status batch_open(mp_pool* src, mp_pool* dst, int64_t n, int j0, int nj);
 mp_status src_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d, mpk::InlineIds* inl);
+// defer: no allocation kernel -- the ids' device bits are cleared by the next
+// device bitmap update (mp_alloc_mem: nothing on the device reads its ids).
 mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_t>* ids,
-                    int** d_ids);
+                    int** d_ids, bool defer = false);
 std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
 
 // peer: one endpoint is another GPU's / process's memory (P2P or IPC mapped);

@@ -1,4 +1,5 @@
-"""Thin ctypes binding of libmempool.so (include/mempool.h).
+"""Thin binding of libmempool.so (include/mempool.h): the per-request calls
+through the CPython extension _mpfast (csrc/pyfast.c), the rest through ctypes.
 
 Argument marshalling only: every step of the hot path runs in the library's
 C++ runtime and sm_100a kernels.  There is no fallback -- importing this
@@ -186,6 +187,26 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 _lib = load_library()
 
 
+def load_fast(libdir: str = os.path.dirname(LIB_PATH)):
+    """The CPython binding of the per-request calls (csrc/pyfast.c); built
+    next to the library by build.py.  No ctypes fallback: a missing binding
+    fails loudly like a missing library."""
+    import importlib.machinery
+    import importlib.util
+    for suffix in importlib.machinery.EXTENSION_SUFFIXES:
+        path = os.path.join(libdir, "_mpfast" + suffix)
+        if os.path.exists(path):
+            spec = importlib.util.spec_from_file_location("_mpfast", path)
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            return mod
+    raise ImportError(f"_mpfast binding not found in {libdir}; build it with "
+                      "`python paper_2406_17565_b200/build.py`")
+
+
+_F = load_fast()
+
+
 def _check(st: int, where: str):
     if st != 0:
         detail = _lib.mp_last_error().decode() if st in (-13, -14, -15) else ""
@@ -217,6 +238,14 @@ def _event_handle(event) -> int:
     return int(event.cuda_event)
 
 
+def _raise_factory(status: int, where: str):
+    detail = _lib.mp_last_error().decode() if status in (-13, -14, -15) else ""
+    return MempoolError(status, where, detail)
+
+
+_F.set_error_factory(_raise_factory)
+
+
 class Pool:
     """One serving instance's MemPool."""
 
@@ -240,6 +269,7 @@ class Pool:
         h = C.c_void_p()
         _check(_lib.mp_pool_create(C.byref(cfg), C.byref(h)), "mp_pool_create")
         self._h = h
+        self._hv = h.value      # the handle as an int, for the _mpfast calls
         info = self.info()
         self.chunk_bytes = info.chunk_bytes
         self.block_bytes = info.block_bytes
@@ -263,16 +293,16 @@ class Pool:
 
     def sync(self):
         """Wait for all device work issued on this pool (mp_sync)."""
-        _check(_lib.mp_sync(self._h), "sync")
+        _F.sync(self._hv)
 
     def wait_event(self, event):
         """Later device work of this pool waits for a CUDA event (e.g. a
         torch.cuda.Event recorded after the engine wrote the KV)."""
-        _check(_lib.mp_wait_event(self._h, C.c_void_p(_event_handle(event))), "wait_event")
+        _F.wait_event(self._hv, _event_handle(event))
 
     def record_event(self, event):
         """Record a CUDA event after all work issued on this pool so far."""
-        _check(_lib.mp_record_event(self._h, C.c_void_p(_event_handle(event))), "record_event")
+        _F.record_event(self._hv, _event_handle(event))
 
     def info(self) -> PoolInfo:
         o = PoolInfo()
@@ -284,39 +314,24 @@ class Pool:
                   stream_ordered: bool = False) -> np.ndarray:
         """stream_ordered: no drain; order the caller's writes after an event
         from record_event (MP_ALLOC_STREAM_ORDERED, include/mempool.h)."""
-        out = np.zeros(max(n, 1), np.uint64)
-        req = self.inst if requester is None else requester
-        t = medium | (ALLOC_STREAM_ORDERED if stream_ordered else 0)
-        _check(_lib.mp_alloc_mem(self._h, n, t, req, _pu64(out)), "alloc_mem")
-        return out[:n]
+        return _F.alloc_mem(self._hv, n, medium | (ALLOC_STREAM_ORDERED if stream_ordered else 0),
+                            self.inst if requester is None else requester)
 
     def free_mem(self, addrs):
-        a = _u64(addrs)
-        _check(_lib.mp_free_mem(self._h, _pu64(a), len(a)), "free_mem")
+        _F.free_mem(self._hv, addrs)
 
     # --------------------------------------------------------------- index API
     def insert(self, tokens, addrs, flags: int = 0) -> int:
-        t, a = _i32(tokens), _u64(addrs)
-        dup = C.c_int64(0)
-        _check(_lib.mp_insert(self._h, _pi32(t), len(t), _pu64(a), len(a), flags,
-                              C.byref(dup)), "insert")
-        return dup.value
+        return _F.insert(self._hv, tokens, addrs, flags)
 
     def match(self, tokens, flags: int = 0):
-        t = _i32(tokens)
-        out = np.zeros(max(len(t) // self.B, 1), np.uint64)
-        mt = C.c_int64(0)
-        _check(_lib.mp_match(self._h, _pi32(t), len(t), flags, _pu64(out), len(out),
-                             C.byref(mt)), "match")
-        return mt.value, out[: mt.value // self.B]
+        return _F.match(self._hv, tokens, flags, self.B)
 
     def unpin(self, addrs):
-        a = _u64(addrs)
-        _check(_lib.mp_unpin(self._h, _pu64(a), len(a)), "unpin")
+        _F.unpin(self._hv, addrs)
 
     def delete(self, tokens):
-        t = _i32(tokens)
-        _check(_lib.mp_delete(self._h, _pi32(t), len(t)), "delete")
+        _F.delete(self._hv, tokens)
 
     def evict(self, n: int, medium: int = HBM) -> np.ndarray:
         out = np.zeros(max(n, 1), np.uint64)
@@ -342,34 +357,13 @@ class Pool:
     # --------------------------------------------------------- distributed API
     def transfer(self, dst_instance: int, src_addrs, dst_addrs=None, flags: int = 0,
                  layer_begin: int = 0, layer_end: int = None, priv: bytes = b"") -> np.ndarray:
-        s = _u64(src_addrs)
-        if dst_addrs is not None:
-            d = _u64(dst_addrs).copy()
-            flags |= XFER_DST_GIVEN
-        else:
-            d = np.zeros(max(len(s), 1), np.uint64)
-        le = self.L if layer_end is None else layer_end
-        pb = C.create_string_buffer(bytes(priv), len(priv)) if priv else None
-        _check(_lib.mp_transfer(self._h, dst_instance, _pu64(s), len(s), _pu64(d), flags,
-                                layer_begin, le, pb, len(priv)), "transfer")
-        return d[: len(s)]
+        return _F.transfer(self._hv, dst_instance, src_addrs, dst_addrs, flags, layer_begin,
+                           self.L if layer_end is None else layer_end, priv or None)
 
     def transfer_with_insert(self, dst_instance: int, tokens, src_addrs, dst_addrs=None,
                              flags: int = 0, priv: bytes = b""):
-        t, s = _i32(tokens), _u64(src_addrs)
-        ceil_b = -(-len(t) // self.B)
-        if dst_addrs is not None:
-            d = _u64(dst_addrs)
-            d = np.concatenate([d, np.zeros(max(0, ceil_b - len(d)), np.uint64)])
-            flags |= XFER_DST_GIVEN
-        else:
-            d = np.zeros(max(ceil_b, 1), np.uint64)
-        moved = C.c_int64(0)
-        pb = C.create_string_buffer(bytes(priv), len(priv)) if priv else None
-        _check(_lib.mp_transfer_with_insert(self._h, dst_instance, _pi32(t), len(t), _pu64(s),
-                                            len(s), _pu64(d), flags, pb, len(priv),
-                                            C.byref(moved)), "transfer_with_insert")
-        return d[:ceil_b], moved.value
+        return _F.transfer_with_insert(self._hv, dst_instance, tokens, src_addrs, dst_addrs, flags,
+                                       priv or None, self.B)
 
     def recv_poll(self):
         m = RecvMsg()

@@ -55,3 +55,33 @@ def test_bad_config_rejected_before_cuda():
     with pytest.raises(M.MempoolError) as e:
         M.Pool(0, 0, 2, 1, 1, 1, 64, elem_bytes=1)  # chunk 1 byte: not 16-B aligned
     assert e.value.name == "CONFIG"
+
+
+def test_fast_binding_loads_and_reports_status():
+    """The CPython binding of the per-request calls (csrc/pyfast.c) is built
+    next to the library, links the same copy, and maps a non-OK status to
+    MempoolError (a NULL pool handle is rejected before any CUDA call)."""
+    import numpy as np
+    from paper_2406_17565_b200 import mempool as M
+    F = M._F
+    for name in ("alloc_mem", "free_mem", "insert", "match", "unpin", "delete", "transfer",
+                 "transfer_with_insert", "record_event", "wait_event", "sync"):
+        assert callable(getattr(F, name)), name
+    toks = np.arange(40, dtype=np.int32)
+    calls = [
+        lambda: F.alloc_mem(0, 4, M.HBM, 0),
+        lambda: F.free_mem(0, np.zeros(2, np.uint64)),
+        lambda: F.insert(0, toks, np.zeros(2, np.uint64), 0),
+        lambda: F.match(0, toks, 0, 16),
+        lambda: F.unpin(0, [1, 2]),
+        lambda: F.delete(0, toks),
+        lambda: F.transfer(0, 1, [1], None, 0, 0, 2, None),
+        lambda: F.transfer_with_insert(0, 1, toks, [1, 2, 3], None, 0, b"x", 16),
+        lambda: F.sync(0),
+    ]
+    for c in calls:
+        with pytest.raises(M.MempoolError) as e:
+            c()
+        assert e.value.name == "CONFIG"
+    with pytest.raises((TypeError, ValueError)):
+        F.free_mem(0, "not an addr list")
