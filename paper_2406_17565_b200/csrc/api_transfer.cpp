@@ -134,6 +134,18 @@ RemotePeer* remote_of(mp_pool* src, int32_t inst) {
 // dst's device) or nullptr.  Enqueued after all earlier work of both pools and
 // before their later work; STAGED completes before returning, the others are
 // stream-ordered.
+// Both id lists by value in the launch parameters when they fit (the host
+// shadow's dids equal what the allocation kernel wrote on the device).
+bool pair_inline(const std::vector<int32_t>& sids, const std::vector<int32_t>& dids,
+                 mpk::InlineIds* si) {
+  const size_t n = sids.size();
+  if (n == 0 || dids.size() != n || 2 * n > (size_t)mpk::kInlineIds) return false;
+  si->n = si->nd = (int)n;
+  std::memcpy(si->ids, sids.data(), n * sizeof(int32_t));
+  std::memcpy(si->ids + n, dids.data(), n * sizeof(int32_t));
+  return true;
+}
+
 mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
                        const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj,
                        uint32_t path) {
@@ -154,16 +166,17 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     DevGuard g(dst->dev);
     int* ds = nullptr;
     mpk::InlineIds si;
-    TRY(src_ids(dst, sids, &ds, &si));
+    const bool both = pair_inline(sids, dids, &si);  // no id table, no meta wait
+    if (!both) TRY(src_ids(dst, sids, &ds, &si));
     const int* dd = d_dst;
-    if (!dd) {
+    if (!dd && !both) {
       int* t = nullptr;
       TRY(upload_ids(dst, dids, &t));
       dd = t;
     }
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, ds),
-                             pool_ep(dst->d_slabs, dd), n, j0, nj, false, 0,
-                             si.n ? &si : nullptr));
+                             pool_ep(dst->d_slabs, both ? nullptr : dd), n, j0, nj, false, 0,
+                             si.n ? &si : nullptr, /*meta_dep=*/!both));
     dst->stats.blocks_moved += (uint64_t)n;
     return link(dst, src);
   }
@@ -176,11 +189,14 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     DevGuard g(src->dev);
     int *ds = nullptr, *dd = nullptr;
     mpk::InlineIds si;
-    TRY(src_ids(src, sids, &ds, &si));
-    TRY(upload_ids(src, dids, &dd));
+    const bool both = pair_inline(sids, dids, &si);
+    if (!both) {
+      TRY(src_ids(src, sids, &ds, &si));
+      TRY(upload_ids(src, dids, &dd));
+    }
     TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
                              pool_ep(it->second, dd), n, j0, nj, /*peer=*/true, 0,
-                             si.n ? &si : nullptr));
+                             si.n ? &si : nullptr, /*meta_dep=*/!both));
     src->stats.blocks_moved += (uint64_t)n;
     return link(src, dst);
   }

@@ -58,6 +58,14 @@ __device__ __forceinline__ long long src_id(const Endpoint& src, const InlineIds
   return src.ids ? __ldg(src.ids + i) : (long long)i;
 }
 
+// Destination block id of copy slot i: inline after the source ids, else
+// from the id table, else i itself.
+__device__ __forceinline__ long long dst_id(const Endpoint& dst, const InlineIds& sinl,
+                                            unsigned i) {
+  if (sinl.nd) return sinl.ids[sinl.n + i];
+  return dst.ids ? __ldg(dst.ids + i) : (long long)i;
+}
+
 // Copies `len` bytes per chunk (the whole chunk, or a head range of it).
 constexpr unsigned kGroup = 8;  // units per dynamic claim (32 KiB per warp)
 
@@ -80,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
     const unsigned i = ch / (unsigned)nj;
     const unsigned jr = ch - i * (unsigned)nj;
     const long long sid = src_id(src, sinl, i);
-    const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
+    const long long did = dst_id(dst, sinl, i);
     const char* sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid);
     char* dp = chunk_ptr<kDstPool>(dst, j0 + jr, jr, did);
     const long long off = (long long)part * kUnitBytes + lane * 16;
@@ -196,7 +204,7 @@ __device__ __forceinline__ void unit_addr(const Endpoint& src, const Endpoint& d
   const unsigned i = ch / (unsigned)nj;
   const unsigned jr = ch - i * (unsigned)nj;
   const long long sid = src_id(src, sinl, i);
-  const long long did = dst.ids ? __ldg(dst.ids + i) : (long long)i;
+  const long long did = dst_id(dst, sinl, i);
   const long long off = (long long)part * kPieceT;
   *sp = chunk_ptr<kSrcPool>(src, j0 + jr, jr, sid) + off;
   *dp = chunk_ptr<kDstPool>(dst, j0 + jr, jr, did) + off;
@@ -474,7 +482,9 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
                            const Sched* sched, const InlineIds* src_inline) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
   static const InlineIds no_ids{};
-  if (src_inline && src_inline->n != n) return cudaErrorInvalidValue;
+  if (src_inline && (src_inline->n != n || (src_inline->nd && (src_inline->nd != n ||
+                                                                2 * n > kInlineIds))))
+    return cudaErrorInvalidValue;
   const InlineIds& si = src_inline ? *src_inline : no_ids;
   if (variant == kCopyBulk) {
     switch (bulk_cfg()) {

@@ -268,19 +268,27 @@ mp_status flush_batch(mp_pool* dst) {
   {
     DevGuard g(dst->dev);
     // source ids: by value in the launch parameters when they fit, else one
-    // upload into this batch's table (ordered before the launch by meta_fence)
+    // upload into this batch's table (ordered before the launch by meta_fence).
+    // Destination ids too when both lists fit (the host shadow holds the ids
+    // the allocation kernel wrote into the table): the copy then reads no id
+    // table, so it does not wait for the meta stream's allocation kernel.
     mpk::InlineIds sinl;
     const bool inl = n <= mpk::kInlineIds;
+    const bool dinl = 2 * n <= mpk::kInlineIds;
     if (inl) {
       sinl.n = (int)n;
       std::memcpy(sinl.ids, b.sids.data(), (size_t)n * sizeof(int32_t));
+      if (dinl) {
+        sinl.nd = (int)n;
+        std::memcpy(sinl.ids + n, b.dids.data(), (size_t)n * sizeof(int32_t));
+      }
     } else {
       CK(cudaMemcpyAsync(dst->bsrc, b.sids.data(), (size_t)n * sizeof(int32_t),
                          cudaMemcpyHostToDevice, dst->meta));
     }
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, inl ? nullptr : dst->bsrc),
-                             pool_ep(dst->d_slabs, dst->bdst), n, b.j0, b.nj, false, 0,
-                             inl ? &sinl : nullptr));
+                             pool_ep(dst->d_slabs, dinl ? nullptr : dst->bdst), n, b.j0, b.nj,
+                             false, 0, inl ? &sinl : nullptr, /*meta_dep=*/!dinl));
     CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
     dst->btab_used[b.tab] = true;
   }
@@ -449,7 +457,7 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester) {
 // ------------------------------------------------------------ migration
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a0,
                                const mpk::Endpoint& b0, int64_t n, int j0, int nj, bool peer,
-                               int64_t len, const mpk::InlineIds* src_inline) {
+                               int64_t len, const mpk::InlineIds* src_inline, bool meta_dep) {
   if (n <= 0) return MP_OK;
   if (len <= 0) len = p->chunk;
   mpk::Endpoint a = a0, b = b0;
@@ -459,7 +467,7 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   const bool timed = p->profiling && s == p->stream;
   if (s == p->stream) {
     TRY(remote_apply_waits(p));  // blocks other processes stored into p
-    TRY(meta_fence(p));          // ids uploaded / allocated on meta
+    if (meta_dep) TRY(meta_fence(p));  // ids uploaded / allocated on meta
   }
   int pair = -1;
   if (timed) {

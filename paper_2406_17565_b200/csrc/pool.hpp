@@ -275,7 +275,8 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
                                const mpk::Endpoint& b, int64_t n, int j0, int nj,
                                bool peer = false, int64_t len = 0,
-                               const mpk::InlineIds* src_inline = nullptr);
+                               const mpk::InlineIds* src_inline = nullptr,
+                               bool meta_dep = true);
 
 // Launch coalescing (same-device fused transfers).
 mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,

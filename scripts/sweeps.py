@@ -271,20 +271,23 @@ def api_latency():
     out = {"workload": "Llama-2-7B pool of 8192 blocks on one B200; per-call host time",
            "alloc_free": [], "index": []}
     P = pool(0, 8192)
-    for n in (16, 64, 256, 1024, 4096):
-        reps = 20
-        ta = tf = 0.0
-        for _ in range(reps):
-            t0 = _t.perf_counter()
-            a = P.alloc_mem(n)
-            t1 = _t.perf_counter()
-            P.free_mem(a)
-            t2 = _t.perf_counter()
-            ta += t1 - t0
-            tf += t2 - t1
-        out["alloc_free"].append({"blocks": n, "alloc_us": round(ta / reps * 1e6, 2),
-                                  "free_us": round(tf / reps * 1e6, 2),
-                                  "alloc_ns_per_block": round(ta / reps / n * 1e9, 1)})
+    for so in (False, True):            # drained (default) / MP_ALLOC_STREAM_ORDERED
+        for n in (1, 16, 64, 256, 1024, 4096):
+            reps, warm = 20, 3
+            ta = tf = 0.0
+            for r in range(warm + reps):
+                t0 = _t.perf_counter()
+                a = P.alloc_mem(n, stream_ordered=so)
+                t1 = _t.perf_counter()
+                P.free_mem(a)
+                t2 = _t.perf_counter()
+                if r >= warm:
+                    ta += t1 - t0
+                    tf += t2 - t1
+            out["alloc_free"].append({"blocks": n, "stream_ordered": so,
+                                      "alloc_us": round(ta / reps * 1e6, 2),
+                                      "free_us": round(tf / reps * 1e6, 2),
+                                      "alloc_ns_per_block": round(ta / reps / n * 1e9, 1)})
     rng = np.random.default_rng(0)
     B = SHAPE.block_tokens
     base = rng.integers(3, 32000, size=4096, dtype=np.int32)       # 256 blocks
