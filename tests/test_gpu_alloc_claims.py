@@ -1,0 +1,68 @@
+"""The device bitmap allocator under deferred claims (include/mempool.h,
+mp_alloc_mem): a caller's alloc_mem is decided by the host shadow and its
+claim reaches the device bitmap only with the next stream-ordered update,
+while a transfer's receiver allocates on the device (lowest-first scan, R2).
+Seeded sequences drive every case of that bookkeeping -- claims and frees
+that cancel before they are applied, more pending updates than fit in a
+launch's parameters (the id-arena upload), the bounded pending list's early
+flush -- and every receiver allocation is compared with the oracle's
+lowest-first choice, then the device bitmap with the oracle's free set."""
+import numpy as np
+import pytest
+
+from tests.twin import Twin, connect, transfer
+from workloads.configs import TINY
+
+pytestmark = pytest.mark.gpu
+
+N = 8192          # blocks per pool (tiny shape: 16 KiB each)
+
+
+def test_claims_cancel_and_overflow_against_device_scan():
+    rng = np.random.default_rng(2406)
+    P, D = Twin(0, TINY, 512), Twin(1, TINY, N)
+    connect(P, D)
+    src = P.alloc(64)
+    P.fill(src)
+    held = []                                   # D's caller-owned blocks (oracle addrs)
+    for step in range(40):
+        op = rng.integers(0, 4)
+        if op == 0 or not held:                 # big caller allocation: deferred claims
+            k = int(rng.integers(1, 2600))
+            if k <= D.o.free_count(0):
+                held += D.alloc(k, stream_ordered=bool(rng.integers(0, 2)))
+        elif op == 1:                           # free a random part (cancels unapplied claims)
+            take = rng.random(len(held)) < rng.uniform(0.1, 0.9)
+            D.free([a for a, t in zip(held, take) if t])
+            held = [a for a, t in zip(held, take) if not t]
+        elif op == 2:                           # reuse just-freed ids (cancels unapplied frees)
+            k = int(rng.integers(1, 300))
+            if held:
+                back = held[-k:]
+                held = held[:-k]
+                D.free(back)
+                held += D.alloc(len(back), stream_ordered=True)
+        else:                                   # receiver allocation on the device
+            n = int(rng.integers(1, 64))
+            if n <= D.o.free_count(0):
+                held += transfer(P, D, src[:n])
+        if step % 10 == 9:
+            D.check_state(check_bytes=False)
+    D.check_state(check_bytes=False)
+    D.check_bytes(sample=64, rng=rng)
+
+
+def test_pending_list_bound_flushes():
+    """More than 4 x kInlineIds claims pending: flushed early through the id
+    arena; the device scan afterwards still sees every claim."""
+    P, D = Twin(0, TINY, 64), Twin(1, TINY, N)
+    connect(P, D)
+    src = P.alloc(32)
+    P.fill(src)
+    a = D.alloc(2500, stream_ordered=True)
+    b = D.alloc(2500, stream_ordered=True)      # 5000 pending > 4000: early flush
+    D.free(a[::3])                              # frees of applied claims
+    got = transfer(P, D, src)                   # device scan: lowest free ids
+    assert sorted(x[2] for x in got) == sorted(x[2] for x in a[::3])[:32]
+    D.free(b)
+    D.check_state(check_bytes=False)
