@@ -54,15 +54,13 @@ def ncu_traffic_ratio(engine):
     longest captured launch).  None when no capture exists."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_traffic_r*.json")))
-    if not files:
-        return None, None
-    with open(files[-1]) as f:
-        cap = json.load(f)
-    launches = cap.get(engine) or []
-    if not launches:
-        return None, None
-    big = max(launches, key=lambda l: l["duration_us"])
-    return big["traffic_over_algorithmic"], os.path.relpath(files[-1], ROOT)
+    for path in reversed(files):    # the latest capture of this engine
+        with open(path) as f:
+            launches = json.load(f).get(engine) or []
+        if launches:
+            big = max(launches, key=lambda l: l["duration_us"])
+            return big["traffic_over_algorithmic"], os.path.relpath(path, ROOT)
+    return None, None
 
 
 def load_peaks():
@@ -326,17 +324,18 @@ def run_ours(args, rank, world, dist):
     kernel_ms = st["kernel_ms"] / max(st["timed_launches"], 1)
     payload_per_launch = st["timed_bytes"] / max(st["timed_launches"], 1)
     same_gpu = role.kind == "PD" or args.device >= 0   # --device: every rank on one GPU
+    kname = "migrate_kernel" if args.copy_kernel == 1 else "migrate_bulk_kernel"
     if same_gpu:
         # loopback: the kernel reads Pb and writes Pb of HBM per block
         alg = 2.0 * payload_per_launch
-        roof = {"kernel": "migrate_kernel<pool,pool> (fused gather->store, A6f), "
+        roof = {"kernel": f"{kname}<pool,pool> (fused gather->store, A6f), "
                           + ("loopback" if role.kind == "PD" else
                              "two processes on one GPU (IPC-mapped receiver pool)"),
                 "bound": "hbm", "peak": peak, "peak_source": peak_src}
     else:
         # across GPUs the bound is the NVLink direction P -> D: Pb per block
         alg = payload_per_launch
-        roof = {"kernel": "migrate_kernel<pool,pool> (fused gather->peer store over NVLink)",
+        roof = {"kernel": f"{kname}<pool,pool> (fused gather->peer store over NVLink)",
                 "bound": "nvlink", "peak": NVLINK_MEASURED_GBS,
                 "peak_source": "B200_PROFILING.md measured peer copy per direction "
                                f"(nominal {NVLINK_GBS} GB/s)"}

@@ -30,6 +30,9 @@
  *    blocks to the caller (unless MP_ALLOC_STREAM_ORDERED, see there).  Frees
  *    of HBM blocks (and mp_alloc_mem's claims) are applied to the device
  *    bitmap lazily, stream-ordered before the pool's next device allocation.
+ *  - The pools of one process on one device share one data stream (migrations
+ *    between them need no cross-stream wait; MP_SHARED_STREAM=0 gives each
+ *    pool its own), so mp_sync on one of them also waits for the others' work.
  *  - Layout: the HBM pool of an instance is 2*L "slabs" (K_0, V_0, K_1, V_1,
  *    ...), each hbm_blocks chunks of c = B*H*D*elem bytes (vLLM's per-layer
  *    paged layout: "two blocks per LLM layer").  Block id b is chunk b

@@ -162,6 +162,7 @@ struct mp_pool {
   // metadata, and a block handed out again is only written by later kernels
   // of the data stream, which run after every earlier reader of it.
   cudaStream_t stream = nullptr, meta = nullptr, copy_stream = nullptr;
+  bool shared_stream = false;  // stream is the device's shared data stream (not owned)
   cudaEvent_t ev_order = nullptr, ev_meta = nullptr;
   std::vector<cudaEvent_t> slot_ev;
   // swap through device staging, double-buffered: [0,1] the halves' fill done
