@@ -137,6 +137,8 @@ def main():
     ap.add_argument("--retain", action="store_true",
                     help="keep finished sessions cached (pools fill up and evict LRU leaves)")
     ap.add_argument("--prof", action="store_true", help="cProfile the timed loop (stderr)")
+    ap.add_argument("--coalesce-mib", type=int, default=0,
+                    help="launch coalescing limit (0: library default 1 GiB, <0: off)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     global STREAM_ORDERED
@@ -151,8 +153,8 @@ def main():
     else:
         sessions = traces.react_like(seed, n_sessions=args.sessions or 32)
         fn = react_session
-    P = make_pool(M, torch, 0, 0, S, args.pool_blocks)
-    D = make_pool(M, torch, 1, 0, S, args.pool_blocks)
+    P = make_pool(M, torch, 0, 0, S, args.pool_blocks, coalesce_mib=args.coalesce_mib)
+    D = make_pool(M, torch, 1, 0, S, args.pool_blocks, coalesce_mib=args.coalesce_mib)
     M.connect(P, D)
     clocks = Clocks("/tmp/clocks_wl.csv", 0)
     with clocks:
