@@ -291,8 +291,19 @@ def run_ours(args, rank, world, dist):
         torch.cuda.profiler.start()     # ncu --profile-from-start off sees the timed region only
         st0.record()
         t0 = time.perf_counter()
+        # per-step device boundaries: an event after each step's work on the
+        # stream the copies run on (the sender's; at N=1 both pools share it)
+        mark_pool = P if role.kind in ("PD", "P") else None
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        step_moved = []
+        if mark_pool is not None:
+            mark_pool.record_event(step_ev[0])
         for k in range(args.steps):
-            moved += step(args.warmup + k, io)
+            mk = step(args.warmup + k, io)
+            moved += mk
+            step_moved.append(mk)
+            if mark_pool is not None:
+                mark_pool.record_event(step_ev[k + 1])
         for pl in (P, D):      # every block of every step has landed
             if pl is not None:
                 pl.sync()
@@ -302,6 +313,15 @@ def run_ours(args, rank, world, dist):
         torch.cuda.profiler.stop()
     ms = st0.elapsed_time(st1)
     wall_ms = (t1 - t0) * 1e3
+    step_stats = None
+    if mark_pool is not None and args.steps >= 2:
+        sms = np.array([step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps)])
+        sgb = np.array(step_moved, dtype=np.float64) * Pb / (sms * 1e-3) / 1e9
+        step_stats = {"what": "device time between consecutive end-of-step events on the "
+                              "copy stream (this rank), and that step's payload rate",
+                      "ms_p10_p50_p90": [round(float(np.percentile(sms, q)), 4) for q in (10, 50, 90)],
+                      "GBps_p10_p50_p90": [round(float(np.percentile(sgb, q)), 1)
+                                           for q in (10, 50, 90)]}
     timed_pool.profile(False)
     st = timed_pool.stats()
     launches = sum(pl.stats()["kernel_launches"] + pl.stats()["aux_launches"]
@@ -373,6 +393,7 @@ def run_ours(args, rank, world, dist):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms / args.steps, 4),
+        "per_step": step_stats,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
