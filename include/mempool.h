@@ -151,7 +151,10 @@ typedef struct {
   uint64_t timed_bytes;       /* payload bytes of those launches */
   uint64_t aux_launches;      /* allocator / free / fill kernels launched */
   double gap_ms;              /* data-stream idle time between consecutive timed launches
-                                 issued between two syncs (profiling on) */
+                                 issued between two syncs (profiling every launch) */
+  uint64_t profiled_launches; /* data-stream migration launches while profiling was on
+                                 (timed or not): kernel_ms * profiled / timed estimates
+                                 their total time when sampling */
 } mp_stats;
 
 typedef struct {
@@ -370,9 +373,13 @@ mp_status mp_unpack(mp_pool* pool, const void* staging, const mp_addr* addrs, in
                     int32_t l0, int32_t l1);
 
 /* ------------------------- measurement / debug --------------------------- */
-/* Profiling on: every migration kernel is bracketed by CUDA events on its
- * launching stream; mp_stats accumulates their durations. */
-mp_status mp_profile(mp_pool* pool, int32_t enable);
+/* Profiling: every `every`-th migration kernel on the pool's data stream
+ * (every = 1: all of them; 0: off) is bracketed by CUDA events on that
+ * stream; mp_stats accumulates their durations.  Completed events are
+ * harvested without blocking, so profiling adds no host synchronisation;
+ * sampling (every > 1) keeps the events' own cost (a few us per launch)
+ * out of short-launch workloads. */
+mp_status mp_profile(mp_pool* pool, int32_t every);
 mp_status mp_stats_get(const mp_pool* pool, mp_stats* out);
 mp_status mp_stats_reset(mp_pool* pool);
 /* Synthetic KV write (stand-in for the engine's prefill; content model of

@@ -125,25 +125,40 @@ static mp_status apply_pending(mp_pool* p, mpk::InlineIds* f) {
 
 mp_status flush_frees(mp_pool* p) { return apply_pending(p, nullptr); }
 
+// Accumulates the timed launches whose end event has completed, oldest first
+// (all of them after a sync).  Never blocks.
+static mp_status harvest_timed(mp_pool* p) {
+  size_t k = 0;
+  for (; k < p->timed.size(); ++k) {
+    const TimedLaunch& t = p->timed[k];
+    const cudaEvent_t end = p->tev[2 * (size_t)t.pair + 1];
+    const cudaError_t q = cudaEventQuery(end);
+    if (q == cudaErrorNotReady) break;
+    CK(q);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p->tev[2 * (size_t)t.pair], end));
+    p->stats.kernel_ms += ms;
+    p->stats.timed_launches += 1;
+    p->stats.timed_bytes += t.bytes;
+    if (p->profile_every == 1 && p->last_timed_pair >= 0) {
+      // idle time of the data stream between consecutive migrations
+      float gap = 0.f;
+      CK(cudaEventElapsedTime(&gap, p->tev[2 * (size_t)p->last_timed_pair + 1],
+                              p->tev[2 * (size_t)t.pair]));
+      p->stats.gap_ms += gap;
+    }
+    p->last_timed_pair = t.pair;
+  }
+  p->timed.erase(p->timed.begin(), p->timed.begin() + (std::ptrdiff_t)k);
+  return MP_OK;
+}
+
 mp_status drain(mp_pool* p) {
   TRY(remote_apply_waits(p));  // blocks stored by other processes have landed too
   CK(cudaStreamSynchronize(p->meta));
   CK(cudaStreamSynchronize(p->stream));
-  for (size_t i = 0; i < p->timed.size(); ++i) {
-    const TimedLaunch& t = p->timed[i];
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, p->tev[2 * (size_t)t.pair], p->tev[2 * (size_t)t.pair + 1]));
-    p->stats.kernel_ms += ms;
-    p->stats.timed_launches += 1;
-    p->stats.timed_bytes += t.bytes;
-    if (i > 0) {  // idle time of the data stream between consecutive migrations
-      float gap = 0.f;
-      CK(cudaEventElapsedTime(&gap, p->tev[2 * (size_t)p->timed[i - 1].pair + 1],
-                              p->tev[2 * (size_t)t.pair]));
-      p->stats.gap_ms += gap;
-    }
-  }
-  p->timed.clear();
+  TRY(harvest_timed(p));
+  p->last_timed_pair = -1;  // no gap across a sync
   if (!p->pending_verify.empty()) {
     int err = 0;
     CK(cudaMemcpy(&err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -466,14 +481,22 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   if (!a.cstride) a.cstride = p->chunk;
   if (!b.cstride) b.cstride = p->chunk;
   const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)len;
-  const bool timed = p->profiling && s == p->stream;
+  const bool cand = p->profile_every > 0 && s == p->stream;
+  const bool timed = cand && (p->profile_seen++ % (uint64_t)p->profile_every) == 0;
+  if (cand) p->stats.profiled_launches += 1;
   if (s == p->stream) {
     TRY(remote_apply_waits(p));  // blocks other processes stored into p
     if (meta_dep) TRY(meta_fence(p));  // ids uploaded / allocated on meta
   }
   int pair = -1;
   if (timed) {
-    if ((int)p->timed.size() >= kTimedPairs) TRY(drain(p));
+    if ((int)p->timed.size() >= kTimedPairs) {
+      TRY(harvest_timed(p));
+      if ((int)p->timed.size() >= kTimedPairs) {  // 512 timed launches still queued
+        CK(cudaEventSynchronize(p->tev[2 * (size_t)p->timed.front().pair + 1]));
+        TRY(harvest_timed(p));
+      }
+    }
     pair = p->tev_next;
     p->tev_next = (p->tev_next + 1) % kTimedPairs;
     CK(cudaEventRecord(p->tev[2 * (size_t)pair], s));
@@ -848,11 +871,12 @@ mp_status mp_record_event(mp_pool* p, void* ev) {
   return MP_OK;
 }
 
-mp_status mp_profile(mp_pool* p, int32_t enable) {
-  if (!p) return MP_ERR_CONFIG;
+mp_status mp_profile(mp_pool* p, int32_t every) {
+  if (!p || every < 0) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
-  if (!enable && p->profiling) TRY(drain(p));
-  p->profiling = enable != 0;
+  if (!every && p->profile_every) TRY(drain(p));
+  p->profile_every = every;
+  p->profile_seen = 0;
   return MP_OK;
 }
 

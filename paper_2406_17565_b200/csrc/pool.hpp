@@ -169,7 +169,9 @@ struct mp_pool {
   // (pack / H2D), [2,3] their drain done (D2H / unpack)
   cudaEvent_t swap_ev[4] = {};
   // profiling: a ring of (start, end) event pairs per migration launch
-  bool profiling = false;
+  int profile_every = 0;        // 0: off; k: time every k-th data-stream migration
+  uint64_t profile_seen = 0;
+  int last_timed_pair = -1;     // end event of the previous harvested launch (gaps)
   std::vector<cudaEvent_t> tev;
   std::vector<mp::TimedLaunch> timed;
   int tev_next = 0;

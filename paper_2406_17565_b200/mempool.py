@@ -100,6 +100,7 @@ class Stats(C.Structure):
         ("blocks_moved", C.c_uint64), ("kernel_ms", C.c_double),
         ("timed_launches", C.c_uint64), ("timed_bytes", C.c_uint64),
         ("aux_launches", C.c_uint64), ("gap_ms", C.c_double),
+        ("profiled_launches", C.c_uint64),
     ]
 
 
@@ -423,8 +424,9 @@ class Pool:
                               layer_end), "unpack")
 
     # ---------------------------------------------------- measurement / debug
-    def profile(self, enable: bool = True):
-        _check(_lib.mp_profile(self._h, int(enable)), "profile")
+    def profile(self, enable: bool = True, every: int = 1):
+        """Time every `every`-th migration launch with CUDA events (mp_profile)."""
+        _check(_lib.mp_profile(self._h, int(every) if enable else 0), "profile")
 
     def stats(self) -> dict:
         s = Stats()

@@ -137,6 +137,10 @@ def main():
     ap.add_argument("--retain", action="store_true",
                     help="keep finished sessions cached (pools fill up and evict LRU leaves)")
     ap.add_argument("--prof", action="store_true", help="cProfile the timed loop (stderr)")
+    ap.add_argument("--profile-every", type=int, default=4,
+                    help="time every k-th migration launch (1: all; events cost a few us each)")
+    ap.add_argument("--no-profile", action="store_true",
+                    help="no per-launch timing events (kernel shares are then unavailable)")
     ap.add_argument("--coalesce-mib", type=int, default=0,
                     help="launch coalescing limit (0: library default 1 GiB, <0: off)")
     args = ap.parse_args()
@@ -164,7 +168,7 @@ def main():
         for x in (P, D):
             x.sync()
             x.stats_reset()
-            x.profile(True)
+            x.profile(not args.no_profile, every=args.profile_every)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -191,9 +195,12 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     st = [x.stats() for x in (P, D)]
-    kms = sum(s["kernel_ms"] for s in st)
-    kl = sum(s["timed_launches"] for s in st)
-    kb = sum(s["timed_bytes"] for s in st)
+    # sampled launches stand for every profiled one (per pool)
+    kms = sum(s["kernel_ms"] * s["profiled_launches"] / s["timed_launches"]
+              for s in st if s["timed_launches"])
+    kl = sum(s["profiled_launches"] for s in st)
+    kb = sum(s["timed_bytes"] * s["profiled_launches"] / s["timed_launches"]
+             for s in st if s["timed_launches"])
     peak, src = load_peaks()
     ach = 2 * kb / (kms * 1e-3) / 1e9 if kms else None
     print(json.dumps({
@@ -206,7 +213,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
                      "peak_source": src, "frac": round(ach / peak, 4) if ach else None,
                      "launches": kl, "share_of_time": round(kms / ms, 4),
-                     "idle_between_launches_share": round(sum(s["gap_ms"] for s in st) / ms, 4),
+                     "timed_every": args.profile_every,
                      "host_ms": round(host_ms, 3)},
         "engine_alloc": "drain" if args.drain_alloc else "stream_ordered",
         "sessions_retained": RETAIN,
