@@ -17,6 +17,7 @@
 //    frees ride in the allocation kernel's parameters.
 //  * fill_kernel : test/bench-only synthetic KV writer (content model).
 #include <cstdlib>
+#include <utility>
 
 #include "kernels.cuh"
 
@@ -66,6 +67,18 @@ __device__ __forceinline__ long long dst_id(const Endpoint& dst, const InlineIds
   return dst.ids ? __ldg(dst.ids + i) : (long long)i;
 }
 
+// Programmatic dependent launch (PDL): a migration launched right behind
+// another on the same stream is scheduled while that one drains its tail;
+// griddepcontrol.wait holds it until the previous grid has completed and its
+// stores are visible (a no-op without a programmatic dependency), and each CTA
+// of the running grid releases its dependents once it has claimed its last
+// unit.  Nothing global is touched before the wait: the dynamic-claiming
+// counter is shared by consecutive launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Copies `len` bytes per chunk (the whole chunk, or a head range of it).
 constexpr unsigned kGroup = 8;  // units per dynamic claim (32 KiB per warp)
 
@@ -81,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
   const unsigned warp = (blockIdx.x * (unsigned)kThreads + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * (unsigned)kThreads) >> 5;
   const bool full_units = (len % kUnitBytes) == 0;
+  pdl_wait();
   const long long chunk = len;
   auto copy_unit = [&](unsigned u) {
     const unsigned ch = u / units_per_chunk;
@@ -109,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
   };
   if (!ctr) {  // static grid-stride split
     for (unsigned u = warp; u < total_units; u += nwarps) copy_unit(u);
+    pdl_release();
     return;
   }
   // dynamic: warp w starts on group w; later groups (nwarps + claim) come
@@ -129,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
     g = __shfl_sync(0xffffffffu, next, 0);
     if (g >= ngroups) break;
   }
+  pdl_release();
 }
 
 // ---------------------------------------------------------------------------
@@ -245,6 +261,7 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
   if (threadIdx.x != 0) return;
   for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  pdl_wait();
   UnitSource units{ctr, base, total_units, blockIdx.x, gridDim.x};
   const char* sp;
   char* dp;
@@ -265,6 +282,11 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     bulk_load(smem + (size_t)k * kPiece, sp, bytes, &bars[k]);
     u = units.claim();  // in flight while the loads are
   }
+  bool released = false;
+  if (u == 0xFFFFFFFFu) {  // nothing left to claim: only the ring's tail remains
+    pdl_release();
+    released = true;
+  }
   // consume stage k % kStages; refill the stage the previous store read from
   for (unsigned k = 0;; ++k) {
     const unsigned s = k % kStages;
@@ -283,10 +305,39 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
         mbar_expect_tx(&bars[r], bytes);
         bulk_load(smem + (size_t)r * kPiece, sp, bytes, &bars[r]);
         u = units.claim();
+        if (u == 0xFFFFFFFFu && !released) {
+          pdl_release();
+          released = true;
+        }
       }
     }
   }
   bulk_wait_all();
+}
+
+// Migration launches carry the PDL attribute (MP_PDL=0 turns it off).
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... Exp, typename... Act>
+static cudaError_t launch_pdl(void (*kern)(Exp...), int grid, int block, size_t smem,
+                              cudaStream_t stream, Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
 // Single CTA of 1024 threads: popcount per thread-range of words, block-wide
@@ -434,10 +485,9 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
   }
   const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
   const bool dyn = sched && sched->ctr && bulk_dynamic();
-  kern<<<grid, kBulkThreads, smem, stream>>>(src, dst, j0, nj, chunk, pieces, (unsigned)total,
-                                             dyn ? sched->ctr : nullptr, dyn ? *sched->base : 0,
-                                             sinl);
-  const cudaError_t e = cudaGetLastError();
+  const cudaError_t e = launch_pdl(kern, grid, kBulkThreads, smem, stream, src, dst, j0, nj, chunk,
+                                   pieces, (unsigned)total, dyn ? sched->ctr : nullptr,
+                                   dyn ? *sched->base : 0ull, sinl);
   if (dyn && e == cudaSuccess) *sched->base += total + (unsigned long long)grid;
   return e;
 }
@@ -523,19 +573,10 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   const bool dyn = sched && sched->ctr && bulk_dynamic();
   unsigned long long* ctr = dyn ? sched->ctr : nullptr;
   const unsigned long long sbase = dyn ? *sched->base : 0;
-  if (sp && dp)
-    migrate_kernel<true, true><<<grid, kThreads, 0, stream>>>(
-        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
-  else if (sp)
-    migrate_kernel<true, false><<<grid, kThreads, 0, stream>>>(
-        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
-  else if (dp)
-    migrate_kernel<false, true><<<grid, kThreads, 0, stream>>>(
-        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
-  else
-    migrate_kernel<false, false><<<grid, kThreads, 0, stream>>>(
-        src, dst, j0, nj, chunk, units_per_chunk, (unsigned)total, si, ctr, sbase);
-  const cudaError_t e = cudaGetLastError();
+  auto kern = sp ? (dp ? migrate_kernel<true, true> : migrate_kernel<true, false>)
+                 : (dp ? migrate_kernel<false, true> : migrate_kernel<false, false>);
+  const cudaError_t e = launch_pdl(kern, grid, kThreads, 0, stream, src, dst, j0, nj, chunk,
+                                   units_per_chunk, (unsigned)total, si, ctr, sbase);
   if (dyn && e == cudaSuccess) {
     const unsigned long long groups = (total + kGroup - 1) / kGroup;
     const unsigned long long warps = (unsigned long long)grid * (kThreads / 32);
