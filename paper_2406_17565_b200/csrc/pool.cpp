@@ -305,8 +305,10 @@ mp_status flush_batch(mp_pool* dst) {
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, inl ? nullptr : dst->bsrc),
                              pool_ep(dst->d_slabs, dinl ? nullptr : dst->bdst), n, b.j0, b.nj,
                              false, 0, inl ? &sinl : nullptr, /*meta_dep=*/!dinl));
-    CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
-    dst->btab_used[b.tab] = true;
+    if (!inl || !dinl) {  // the launch reads this batch's id tables: guard their reuse
+      CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
+      dst->btab_used[b.tab] = true;
+    }  // (no stream op between back-to-back inline launches: PDL overlaps them)
   }
   TRY(link(dst, src));
   for (int32_t id : b.sids) src->pend_r[(size_t)id] = 0;

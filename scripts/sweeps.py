@@ -320,7 +320,55 @@ def api_latency():
     return out
 
 
+def chain_sweep():
+    """Back-to-back ASYNC transfers of n scattered blocks (no sync between
+    them): device time per transfer from CUDA events around the whole chain.
+    Run once with MP_PDL=1 and once with MP_PDL=0 to see what programmatic
+    dependent launch hides between consecutive migration kernels."""
+    import torch
+    out = {"workload": "chains of up to 400 back-to-back ASYNC mp_transfer calls of n scattered "
+                       "Llama-2-7B blocks, loopback, one B200",
+           "pdl": os.environ.get("MP_PDL", "1") != "0", "rows": []}
+    # one launch per transfer (no coalescing); the pools' stream is gated
+    # behind a sleeping kernel while the host issues the whole chain, so the
+    # events time the device back to back, not the host's issue rate
+    P, D = pool(0, 4096, coalesce_mib=-1), pool(1, 4096, coalesce_mib=-1)
+    M.connect(P, D)
+    rng = np.random.default_rng(3)
+    src = P.alloc_mem(2048)
+    P.debug_fill(src, 1)
+    P.sync()
+    side = torch.cuda.Stream()
+    for n in (1, 2, 4, 8, 16, 64):
+        reps = min(400, 3800 // n)       # every destination stays allocated until the end
+        sels = [src[rng.choice(len(src), n, replace=False)] for _ in range(reps)]
+        for warm in (True, False):
+            P.sync()
+            D.sync()
+            gate = torch.cuda.Event()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(side):
+                torch.cuda._sleep(200_000_000)       # ~0.1 s: longer than issuing the chain
+                gate.record()
+            P.wait_event(gate)
+            P.record_event(e0)
+            got = []
+            for s in sels[: 20 if warm else reps]:
+                got.append(P.transfer(1, s, flags=M.XFER_ASYNC))
+            D.record_event(e1)
+            torch.cuda.synchronize()
+            if not warm:
+                ms = e0.elapsed_time(e1)
+            for g in got:
+                D.free_mem(g)
+        out["rows"].append({"n_blocks": n, "us_per_transfer": round(ms * 1e3 / reps, 2),
+                            "GBps": round(n * Pb * reps / (ms * 1e-3) / 1e9, 1)})
+    P.close()
+    D.close()
+    return out
+
+
 if __name__ == "__main__":
     fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency,
-          "dram_source": dram_source_sweep, "gs": gs_latency}[sys.argv[1]]
+          "dram_source": dram_source_sweep, "gs": gs_latency, "chain": chain_sweep}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))

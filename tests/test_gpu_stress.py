@@ -169,3 +169,44 @@ def test_three_pools_crossing_transfers_bytes():
             pools[y][0].free_mem(d)
     for p, _r in pools:
         p.close()
+
+
+@pytest.mark.parametrize("k", [1, 40, 700])   # ids inline in the launch / through id tables
+def test_relay_chain_reads_what_the_previous_hop_wrote(k):
+    """k blocks hop A -> B -> C -> A -> ... eleven times, every hop ASYNC and
+    issued before the previous one has run, in reverse order: each migration
+    starts on exactly the blocks the previous migration writes last, so it
+    must not start before that grid has completed (stream order on the shared
+    data stream, and griddepcontrol.wait under programmatic dependent launch;
+    a blocked next grid only gets SMs as the previous one's CTAs exit, so the
+    window this guards is a unit or two wide).  The last hop's blocks must
+    equal the first hop's sources byte for byte."""
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    from workloads.configs import KVShape
+    S = KVShape("relay", 8, 8, 128, 16)             # 32 KiB chunks, 512 KiB blocks
+    n = 4 * k
+    pools = [_pool(M, torch, i, S, n) for i in range(3)]
+    for i in range(3):
+        for j in range(i + 1, 3):
+            M.connect(pools[i][0], pools[j][0])
+    first = pools[0][0].alloc_mem(k)
+    pools[0][0].debug_fill(first, 4242)
+    cur, at = first, 0
+    order = np.arange(k)             # cur[i] holds the content of first[order[i]]
+    for hop in range(11):
+        nxt = (at + 1) % 3
+        # reversed: the hop's first units read the blocks the previous hop wrote last
+        got = pools[at][0].transfer(nxt, cur[::-1], flags=M.XFER_ASYNC)
+        if hop:      # forwarded: free it while the copy may still read it (stream order)
+            pools[at][0].free_mem(cur)
+        cur, at, order = got, nxt, order[::-1]
+    for p, _r in pools:
+        p.sync()
+    s_ids = torch.as_tensor(M.addr_indices(first)[order], device="cuda:0")
+    d_ids = torch.as_tensor(M.addr_indices(cur), device="cuda:0")
+    for j in range(2 * S.layers):
+        bad = (pools[at][1][j, d_ids] != pools[0][1][j, s_ids]).any(dim=1)
+        assert not bool(bad.any()), f"chunk {j}: {int(bad.sum())} blocks differ"
+    for p, _r in pools:
+        p.close()
