@@ -85,3 +85,23 @@ def test_fast_binding_loads_and_reports_status():
         assert e.value.name == "CONFIG"
     with pytest.raises((TypeError, ValueError)):
         F.free_mem(0, "not an addr list")
+
+
+def test_fast_binding_converts_inputs():
+    """Lists, other integer dtypes, non-contiguous and 2-D arrays are
+    converted (flattened, cast) before the C call -- the NULL handle then
+    yields CONFIG, not a conversion error."""
+    import numpy as np
+    from paper_2406_17565_b200 import mempool as M
+    F = M._F
+    toks64 = np.arange(0, 96, dtype=np.int64)
+    strided = np.arange(0, 192, dtype=np.int32)[::2]
+    addrs = np.arange(12, dtype=np.uint64).reshape(3, 4)
+    for toks in (list(range(48)), toks64, strided, toks64.reshape(6, 16)):
+        for a in (addrs, addrs.T, [1, 2, 3], np.arange(3, dtype=np.int64)):
+            with pytest.raises(M.MempoolError) as e:
+                F.insert(0, toks, a, 0)
+            assert e.value.name == "CONFIG"
+    with pytest.raises(M.MempoolError) as e:
+        F.transfer_with_insert(0, 1, strided, addrs.T, [5, 6], 0, bytearray(b"pv"), 16)
+    assert e.value.name == "CONFIG"
