@@ -358,7 +358,9 @@ def run_ours(args, rank, world, dist):
     kernel_ms_total = kernel_ms * st["profiled_launches"]
     payload_per_launch = st["timed_bytes"] / max(st["timed_launches"], 1)
     same_gpu = role.kind == "PD" or args.device >= 0   # --device: every rank on one GPU
-    kname = "migrate_kernel" if args.copy_kernel == 1 else "migrate_bulk_kernel"
+    # engine: auto = the bulk ring within one pool's GPU, vector LD/ST for peer stores
+    bulk = args.copy_kernel == 2 or (args.copy_kernel == 0 and role.kind == "PD")
+    kname = "migrate_bulk_kernel" if bulk else "migrate_kernel"
     if same_gpu:
         # loopback: the kernel reads Pb and writes Pb of HBM per block
         alg = 2.0 * payload_per_launch
@@ -374,7 +376,7 @@ def run_ours(args, rank, world, dist):
                 "peak_source": "B200_PROFILING.md measured peer copy per direction "
                                f"(nominal {NVLINK_GBS} GB/s)"}
     achieved = alg / (kernel_ms * 1e-3) / 1e9 if kernel_ms > 0 else None
-    ratio, ratio_src = (ncu_traffic_ratio("vector" if args.copy_kernel == 1 else "bulk")
+    ratio, ratio_src = (ncu_traffic_ratio("bulk" if bulk else "vector")
                         if role.kind == "PD" else (None, None))
     roof.update({
         "achieved": round(achieved, 1) if achieved else None, "unit": "GB/s",
