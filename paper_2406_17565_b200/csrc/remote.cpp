@@ -474,9 +474,11 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
         }
       }
       if (xs == MP_OK)
+        // a receiver process on this same GPU: its IPC-mapped pool is local
+        // HBM, so the copy takes the loopback engine (bulk ring, claiming)
         xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
                                   pool_ep(r->d_slabs, d_d), (int64_t)hs.size(), j0, nj,
-                                  /*peer=*/true, 0, si.n ? &si : nullptr);
+                                  /*peer=*/!r->same_device, 0, si.n ? &si : nullptr);
     }
     if (xs == MP_OK && !ds_.empty()) {
       int *d_s = nullptr, *d_d = nullptr;
