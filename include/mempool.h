@@ -153,8 +153,9 @@ typedef struct {
   double gap_ms;              /* data-stream idle time between consecutive timed launches
                                  issued between two syncs (profiling every launch) */
   uint64_t profiled_launches; /* data-stream migration launches while profiling was on
-                                 (timed or not): kernel_ms * profiled / timed estimates
-                                 their total time when sampling */
+                                 (timed or not) */
+  uint64_t profiled_bytes;    /* their payload bytes: kernel_ms * profiled_bytes /
+                                 timed_bytes estimates their total time when sampling */
 } mp_stats;
 
 typedef struct {

@@ -485,7 +485,10 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   const uint64_t bytes = (uint64_t)n * (uint64_t)nj * (uint64_t)len;
   const bool cand = p->profile_every > 0 && s == p->stream;
   const bool timed = cand && (p->profile_seen++ % (uint64_t)p->profile_every) == 0;
-  if (cand) p->stats.profiled_launches += 1;
+  if (cand) {
+    p->stats.profiled_launches += 1;
+    p->stats.profiled_bytes += bytes;
+  }
   if (s == p->stream) {
     TRY(remote_apply_waits(p));  // blocks other processes stored into p
     if (meta_dep) TRY(meta_fence(p));  // ids uploaded / allocated on meta

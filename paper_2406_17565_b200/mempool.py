@@ -100,7 +100,7 @@ class Stats(C.Structure):
         ("blocks_moved", C.c_uint64), ("kernel_ms", C.c_double),
         ("timed_launches", C.c_uint64), ("timed_bytes", C.c_uint64),
         ("aux_launches", C.c_uint64), ("gap_ms", C.c_double),
-        ("profiled_launches", C.c_uint64),
+        ("profiled_launches", C.c_uint64), ("profiled_bytes", C.c_uint64),
     ]
 
 

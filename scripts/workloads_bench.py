@@ -195,12 +195,12 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     st = [x.stats() for x in (P, D)]
-    # sampled launches stand for every profiled one (per pool)
-    kms = sum(s["kernel_ms"] * s["profiled_launches"] / s["timed_launches"]
-              for s in st if s["timed_launches"])
+    # sampled launches stand for every profiled one (per pool; ratio
+    # estimator: kernel time per byte of the sampled launches x all bytes)
+    kms = sum(s["kernel_ms"] * s["profiled_bytes"] / s["timed_bytes"]
+              for s in st if s["timed_bytes"])
     kl = sum(s["profiled_launches"] for s in st)
-    kb = sum(s["timed_bytes"] * s["profiled_launches"] / s["timed_launches"]
-             for s in st if s["timed_launches"])
+    kb = sum(s["profiled_bytes"] for s in st)
     peak, src = load_peaks()
     ach = 2 * kb / (kms * 1e-3) / 1e9 if kms else None
     print(json.dumps({
