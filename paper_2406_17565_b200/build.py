@@ -19,7 +19,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 SOURCES = ["pool.cpp", "api_memory_index.cpp", "api_transfer.cpp", "api_swap.cpp",
            "remote.cpp", "gs.cpp", "kernels.cu"]
-HEADERS = ["kernels.cuh", "index.hpp", "pool.hpp"]
+HEADERS = ["kernels.cuh", "index.hpp", "pool.hpp", "bitmap_updates.hpp"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -87,25 +87,14 @@ mp_status src_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d, mpk::Inl
 // small sets by value in a kernel's parameters (folded into the next
 // allocation when there is one), large ones through the id arena.
 // Deferred claims (mp_alloc_mem) travel the same way, encoded -(id+1).
-static void take_pending(mp_pool* p, std::vector<int32_t>* out) {
-  out->clear();
-  for (int32_t id : p->pending_free) {
-    uint8_t& d = p->dev_pend[(size_t)id];
-    if (d == DEV_FREE) out->push_back(id);
-    else if (d == DEV_CLAIM) out->push_back(-id - 1);
-    d = DEV_NONE;  // later duplicates of this id are stale
-  }
-  p->pending_free.clear();
-}
-
 // Applies every pending update before the next device-bitmap scan: a short
 // list is returned in *f for the caller's allocation kernel (f nullable:
 // launched here), a long one goes through the id arena now.
 static mp_status apply_pending(mp_pool* p, mpk::InlineIds* f) {
   if (f) f->n = 0;
-  if (p->pending_free.empty()) return MP_OK;
+  if (p->dev_upd.empty()) return MP_OK;
   std::vector<int32_t> v;
-  take_pending(p, &v);
+  p->dev_upd.take(&v);
   if (v.empty()) return MP_OK;  // everything cancelled out
   if ((int)v.size() <= mpk::kInlineIds) {
     mpk::InlineIds local;
@@ -363,13 +352,7 @@ void free_block(mp_pool* p, int med, int32_t idx) {
   ++p->nfree[med];
   if (med == MP_HBM) {
     p->hfree[(size_t)idx >> 6] |= 1ull << (idx & 63);
-    uint8_t& d = p->dev_pend[(size_t)idx];
-    if (d == DEV_CLAIM) {  // claimed on the host only: the device bit is still 1
-      d = DEV_NONE;
-    } else {
-      d = DEV_FREE;
-      p->pending_free.push_back(idx);  // device bitmap: stream-ordered, lazily
-    }
+    p->dev_upd.on_free(idx);  // device bitmap: stream-ordered, lazily
   } else {
     p->dram_free.insert(idx);
   }
@@ -422,17 +405,9 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
   for (int32_t id : *ids) hazard = hazard || p->pend_w[(size_t)id] || p->pend_r[(size_t)id];
   if (hazard) TRY(flush_involving(p));
   if (defer) {
-    for (int32_t id : *ids) {
-      uint8_t& dp = p->dev_pend[(size_t)id];
-      if (dp == DEV_FREE) {  // freed on the host only: the device bit is still 0
-        dp = DEV_NONE;
-      } else {
-        dp = DEV_CLAIM;
-        p->pending_free.push_back(id);
-      }
-    }
-    // keep the pending list bounded (stale entries and long claim runs)
-    if (p->pending_free.size() > (size_t)4 * mpk::kInlineIds) TRY(flush_frees(p));
+    for (int32_t id : *ids) p->dev_upd.on_claim(id);
+    // keep the queue bounded (stale entries and long claim runs)
+    if (p->dev_upd.queued() > (size_t)4 * mpk::kInlineIds) TRY(flush_frees(p));
     *d_ids = nullptr;
     return MP_OK;
   }
@@ -758,7 +733,7 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->batch_limit = (uint64_t)(cfg->coalesce_mib > 0 ? cfg->coalesce_mib : 1024) << 20;
   p->batch_cap = p->n_hbm;
   p->pend_w.assign((size_t)p->n_hbm, 0);
-  p->dev_pend.assign((size_t)p->n_hbm, 0);
+  p->dev_upd.reset((size_t)p->n_hbm);
   p->pend_r.assign((size_t)p->n_hbm, 0);
   for (int k = 0; k < mp_pool::kBatchTabs; ++k) {
     CKC(cudaMalloc(&p->bsrc_ring[k], sizeof(int) * (size_t)p->batch_cap));

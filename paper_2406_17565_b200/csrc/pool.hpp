@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/mempool.h"
+#include "bitmap_updates.hpp"
 #include "index.hpp"
 #include "kernels.cuh"
 
@@ -35,7 +36,6 @@ void set_err(const std::string& s);
 const std::string& get_err();
 
 enum : uint8_t { ST_FREE = 0, ST_ACTIVE = 1, ST_INDEXED = 2, ST_ORPHAN = 3 };
-enum : uint8_t { DEV_NONE = 0, DEV_FREE = 1, DEV_CLAIM = 2 };  // mp_pool::dev_pend
 
 struct DevGuard {
   int prev = -1, want;
@@ -183,13 +183,9 @@ struct mp_pool {
   std::vector<uint64_t> hfree;             // HBM shadow bitmap (bit = 1: free)
   std::set<int32_t> dram_free;             // host-managed pinned DRAM allocator
   std::map<int32_t, int32_t> orphan_ref[2];
-  // Device-bitmap updates not applied yet (stream-ordered, lazily): ids whose
-  // dev_pend is DEV_FREE (host freed, device bit still 0) or DEV_CLAIM (taken
-  // by mp_alloc_mem on the host, device bit still 1).  A free and a claim of
-  // the same id cancel, so the pending set is order-free; entries whose
-  // dev_pend no longer matches are stale and skipped.
-  std::vector<int32_t> pending_free;
-  std::vector<uint8_t> dev_pend;
+  // Device-bitmap updates not applied yet (frees, mp_alloc_mem's claims):
+  // stream-ordered, lazily, before the next device scan (bitmap_updates.hpp).
+  mp::BitmapUpdates dev_upd;
   std::vector<uint32_t> mark[2];           // scratch duplicate marks (next_mark)
   uint32_t mark_gen = 0;
   std::vector<mp::PendingVerify> pending_verify;
