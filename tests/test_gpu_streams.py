@@ -9,12 +9,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _pool(M, torch, inst, shape, n):
+def _pool(M, torch, inst, shape, n, **kw):
     c = shape.chunk_bytes
     region = torch.zeros(2 * shape.layers * n * c, dtype=torch.uint8, device="cuda:0")
     slabs = [region.data_ptr() + j * n * c for j in range(2 * shape.layers)]
     p = M.Pool(inst, 0, shape.layers, shape.kv_heads, shape.head_dim, shape.block_tokens, n,
-               slabs=slabs, verify=True)
+               slabs=slabs, verify=True, **kw)
     return p, region.view(2 * shape.layers, n, c)
 
 
@@ -89,5 +89,43 @@ def test_stream_ordered_alloc_reuses_block_still_being_read():
     did = torch.as_tensor(M.addr_indices(dst), device="cuda:0")
     assert (dr[:, did] == 7).all(), "receiver copied the new owner's bytes"
     assert (pr[:, sid] == 99).all()
+    P.close()
+    D.close()
+
+
+def test_sampled_profiling_counts():
+    """mp_profile(every=k): every k-th data-stream migration is timed with
+    CUDA events; profiled_launches / profiled_bytes count all of them, and the
+    harvest never blocks (ASYNC transfers stay queued until the sync)."""
+    import torch
+    from paper_2406_17565_b200 import mempool as M
+    from workloads.configs import KVShape
+    shape = KVShape("s", 4, 4, 64, 16)
+    P, _ = _pool(M, torch, 0, shape, 64, coalesce_mib=-1)   # one launch per transfer
+    D, _ = _pool(M, torch, 1, shape, 256, coalesce_mib=-1)
+    M.connect(P, D)
+    src = P.alloc_mem(8)
+    P.debug_fill(src, 5)
+    P.sync()
+    per = 8 * 2 * shape.layers * shape.chunk_bytes
+    for every, n in ((3, 10), (1, 5)):
+        D.stats_reset()
+        P.stats_reset()
+        D.profile(True, every=every)
+        P.profile(True, every=every)
+        got = [P.transfer(1, src, flags=M.XFER_ASYNC | M.PATH_FUSED) for _ in range(n)]
+        P.sync()
+        D.sync()
+        st = [D.stats(), P.stats()]
+        prof = sum(s["profiled_launches"] for s in st)
+        assert prof == n                                   # one launch per transfer
+        assert sum(s["profiled_bytes"] for s in st) == n * per
+        assert sum(s["timed_launches"] for s in st) == -(-n // every)
+        assert sum(s["timed_bytes"] for s in st) == -(-n // every) * per
+        assert sum(s["kernel_ms"] for s in st) > 0
+        for p in (P, D):
+            p.profile(False)
+        for g in got:
+            D.free_mem(g)
     P.close()
     D.close()
