@@ -368,7 +368,66 @@ def chain_sweep():
     return out
 
 
+def tiny_latency():
+    """BASELINE configs[0] (tiny pool: L2 H2 D64 fp16, B16, 64 blocks per
+    instance) is latency-bound, not roofline-graded: host
+    µs per call of the golden run's operations, p10 / p50 / p90 over 300
+    rounds of the three prompts (each round deletes them again)."""
+    from workloads.configs import TINY as T
+    from workloads.traces import golden_prompts
+    import time as _t
+    P = M.Pool(0, 0, T.layers, T.kv_heads, T.head_dim, T.block_tokens, 64)
+    D = M.Pool(1, 0, T.layers, T.kv_heads, T.head_dim, T.block_tokens, 64)
+    M.connect(P, D)
+    _, p1, p2, p3 = golden_prompts()
+    B = T.block_tokens
+    acc = {k: [] for k in ("match", "alloc_mem", "insert", "twi_dedup_sync", "twi_dedup_async",
+                           "free_mem", "delete")}
+    for rnd in range(320):
+        keep = rnd >= 20
+        flags = M.XFER_DEDUP | (M.XFER_ASYNC if rnd % 2 else 0)
+        parts = []
+        for p in (p1, p2, p3):
+            t0 = _t.perf_counter()
+            _, m = P.match(p)
+            t1 = _t.perf_counter()
+            new = P.alloc_mem(-(-len(p) // B) - len(m), stream_ordered=True)
+            t2 = _t.perf_counter()
+            full = np.concatenate([m, new])
+            t3 = _t.perf_counter()
+            P.insert(p, full[: len(p) // B])
+            t4 = _t.perf_counter()
+            fin, _ = P.transfer_with_insert(1, p, full, flags=flags)
+            t5 = _t.perf_counter()
+            if keep:
+                acc["match"].append(t1 - t0)
+                acc["alloc_mem"].append(t2 - t1)
+                acc["insert"].append(t4 - t3)
+                acc["twi_dedup_async" if flags & M.XFER_ASYNC else "twi_dedup_sync"].append(t5 - t4)
+            parts.append((p, full[len(p) // B:], fin[len(p) // B:]))
+        for p, pp, dp in parts:
+            t0 = _t.perf_counter()
+            P.free_mem(pp)
+            t1 = _t.perf_counter()
+            P.delete(p)
+            t2 = _t.perf_counter()
+            D.free_mem(dp)
+            D.delete(p)
+            if keep:
+                acc["free_mem"].append(t1 - t0)
+                acc["delete"].append(t2 - t1)
+    P.sync()
+    D.sync()
+    P.close()
+    D.close()
+    return {"workload": "configs[0] tiny pools (16 KiB blocks), golden prompts p1-p3, P->D DEDUP "
+                        "transfer_with_insert, host clock per call through the Python binding",
+            "us_p10_p50_p90": {k: [round(float(np.percentile(v, q)) * 1e6, 2) for q in (10, 50, 90)]
+                               for k, v in acc.items()}}
+
+
 if __name__ == "__main__":
     fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency,
-          "dram_source": dram_source_sweep, "gs": gs_latency, "chain": chain_sweep}[sys.argv[1]]
+          "dram_source": dram_source_sweep, "gs": gs_latency, "chain": chain_sweep,
+          "tiny": tiny_latency}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))
