@@ -45,7 +45,8 @@ NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per directi
 METRIC = "KV migration GB/s (P->D transfer_with_insert payload)"
 WORKLOAD = ("configs[1]: Llama-2-7B-shaped KV (L32 H32 D128 fp16 B16, Pb=8 MiB) ShareGPT-like "
             "1P1D per pair, PD-Caching-2 P->D with DEDUP")
-DTYPE = "u16 (fp16 KV copied as opaque 16-bit words)"
+DTYPE = "u16"          # the path computes nothing: fp16 KV is copied as opaque 16-bit words
+KV_DTYPE = "fp16 KV copied as opaque 16-bit words (bit-exact, NaN payloads preserved)"
 
 
 def ncu_traffic_ratio(engine):
@@ -427,6 +428,7 @@ def run_ours(args, rank, world, dist):
         "data": "synthetic (seeded ShareGPT-like token traces; counter-based KV fill)",
         "config": {
             "workload": WORKLOAD,
+            "kv_dtype": KV_DTYPE,
             "placement": placement,
             "wire_bound": ("HBM read+write of one GPU (loopback; N=1 has no wire)" if world == 1
                            else f"NVLink per direction, {world // 2} independent pair(s): "
@@ -619,7 +621,7 @@ def run_reference(args, world):
         "ms_per_step": round(secs * 1e3 / max(args.steps, 1), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": DTYPE, "data": "synthetic",
-        "config": {"workload": WORKLOAD,
+        "config": {"workload": WORKLOAD, "kv_dtype": KV_DTYPE,
                    "sample": "bounded sample of the workload per step (CPU oracle)"},
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": arm.cores,
                          "kind": "oracle", "sample": arm.sample(n_req, args.steps)},
