@@ -6,7 +6,7 @@ Checked against the oracle as it goes (tests/twin.py)."""
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # tests/ -> repo root
 sys.path.insert(0, ROOT)
 
 from paper_2406_17565_b200 import mempool as M  # noqa: E402
