@@ -366,14 +366,20 @@ void hint_slot(mp_pool* src, mp_pool* dst, uint32_t flags, const std::vector<uin
   dst->slot_hint.nj = nj;
 }
 
+// A synchronous transfer returns once the work it issued has completed: its
+// launches (flushed here if still batched) and the receiver's allocation.
+// Bitmap updates still queued from earlier frees are not part of it and
+// stay queued (applying them here cost a kernel and a wait per call).
 mp_status finish(mp_pool* src, mp_pool* dst, uint32_t flags) {
   if (flags & MP_XFER_ASYNC) return MP_OK;
+  TRY(flush_involving(dst));
+  TRY(flush_involving(src));
   {
     DevGuard g(dst->dev);
-    TRY(sync(dst));
+    TRY(drain(dst));
   }
   DevGuard g(src->dev);
-  return sync(src);
+  return drain(src);
 }
 
 void stash_priv(DstPrep* st, const void* priv, int64_t priv_len) {
