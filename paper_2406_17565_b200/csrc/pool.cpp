@@ -488,6 +488,19 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
   int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyBulk : p->copy_kernel;
   if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
+  // Knobs for the first multi-GPU box (untested on NVLink so far):
+  // MP_PEER_ENGINE=bulk stores into peer memory with the bulk (TMA) ring,
+  // MP_PEER_SCHED=dynamic lets peer copies claim units dynamically.
+  static const bool peer_bulk = [] {
+    const char* e = getenv("MP_PEER_ENGINE");
+    return e && e[0] == 'b';
+  }();
+  static const bool peer_dyn = [] {
+    const char* e = getenv("MP_PEER_SCHED");
+    return e && e[0] == 'd';
+  }();
+  if (peer && !host_side && peer_bulk && p->copy_kernel == mpk::kCopyAuto)
+    variant = mpk::kCopyBulk;
   // dynamic unit claiming on the pool's data stream (launches serialised);
   // stores into a peer's memory keep the static split: on the one-GPU
   // two-process run (IPC-mapped pool) it was 4% ahead of claiming
@@ -495,7 +508,8 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   // rebalancing SMs
   const mpk::Sched sched{p->d_sched, &p->sched_base};
   CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant,
-                         (s == p->stream && !peer) ? &sched : nullptr, src_inline));
+                         (s == p->stream && (!peer || peer_dyn)) ? &sched : nullptr,
+                         src_inline));
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});
