@@ -36,6 +36,47 @@ PYEXT_SRC = os.path.join(CSRC, "pyfast.c")
 PYEXT = os.path.join(LIBDIR, "_mpfast" + sysconfig.get_config_var("EXT_SUFFIX"))
 
 
+# The paper's NCCL send/recv transport as a comparison arm (csrc/nccl_arm.cpp,
+# include/mempool_nccl.h), in its own library: libmempool.so stays NCCL-free.
+# Linked against the NCCL that torch loads (same soname, one copy per process).
+NCCL_SRC = os.path.join(CSRC, "nccl_arm.cpp")
+NCCL_LIB = os.path.join(LIBDIR, "libmempool_nccl.so")
+
+
+def _nccl_dirs():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec else []):
+        inc, lib = os.path.join(base, "nccl", "include"), os.path.join(base, "nccl", "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.isdir(lib):
+            return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+def build_nccl_arm(verbose: bool = False) -> str:
+    inc, lib = _nccl_dirs()
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    tmp = NCCL_LIB + ".tmp"
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall", "-I", inc,
+           "-I", os.path.join(cuda, "include"), "-I", INCLUDE, NCCL_SRC, "-o", tmp,
+           "-L", lib, "-l:libnccl.so.2", "-Wl,-rpath," + lib,
+           "-L", os.path.join(cuda, "lib64"), "-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError("g++ failed building libmempool_nccl.so")
+    os.replace(tmp, NCCL_LIB)
+    return NCCL_LIB
+
+
+def nccl_stale() -> bool:
+    if not os.path.exists(NCCL_LIB):
+        return True
+    t = os.path.getmtime(NCCL_LIB)
+    return any(os.path.getmtime(d) > t for d in (NCCL_SRC, os.path.join(INCLUDE, "mempool_nccl.h")))
+
+
 def _nvcc():
     cand = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
     return cand if os.path.exists(cand) else "nvcc"
@@ -76,6 +117,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         if pyext_stale():
             build_pyext(verbose)
+        if nccl_stale():
+            build_nccl_arm(verbose)
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
@@ -90,6 +133,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
         f.write(res.stderr)
     build_pyext(verbose)
+    build_nccl_arm(verbose)
     return LIB
 
 

@@ -368,6 +368,96 @@ def chain_sweep():
     return out
 
 
+def nccl_sweep():
+    """The paper's transport (NCCL send/recv) beside the
+    fused one-sided kernel, on one B200 through a one-rank communicator (NCCL's
+    self send/recv = its local copy path), n scattered Llama-2-7B blocks:
+      nccl_discrete_per_block  one NCCL group per block of 2L chunk sends (the
+                               paper's discrete layout, one call per block)
+      nccl_discrete_grouped    all n * 2L chunk sends in one group
+      nccl_aggregated          mp_pack -> one send of n * Pb -> mp_unpack
+                               (the paper's aggregation)
+      fused                    mp_transfer (the product path)
+    Host clock per synchronous transfer; destination bytes checked against
+    the source on the device after every mode."""
+    import time as _t
+    import torch
+    from bench import make_pool
+    from paper_2406_17565_b200 import nccl_arm as N
+    S = SHAPE
+    nb = 1024
+    P = make_pool(M, torch, 0, 0, S, nb)
+    D = make_pool(M, torch, 1, 0, S, nb)
+    M.connect(P, D)
+    c, L = S.chunk_bytes, S.layers
+    pv = P._region.view(2 * L, nb, c)
+    dv = D._region.view(2 * L, nb, c)
+    comm = N.NcclComm.create_single(0)
+    stream = torch.cuda.current_stream()
+    rng = np.random.default_rng(7)
+    src_all = P.alloc_mem(512)
+    P.debug_fill(src_all, 11)
+    P.sync()
+    stg = torch.empty(2, 256 * Pb, dtype=torch.uint8, device="cuda:0")
+    out = {"workload": "n scattered Llama-2-7B blocks (Pb = 8 MiB) P -> D on one B200; NCCL "
+                       f"{N.version()} one-rank communicator (self send/recv)", "rows": []}
+
+    def chunk_ptrs(view, ids):
+        base = view.data_ptr()
+        return [base + (j * nb + int(b)) * c for b in ids for j in range(2 * L)]
+
+    def check(src, dst):
+        s = torch.as_tensor(M.addr_indices(src), device="cuda:0")
+        d = torch.as_tensor(M.addr_indices(dst), device="cuda:0")
+        for j in (0, 2 * L - 1):
+            assert bool((pv[j, s] == dv[j, d]).all()), "bytes differ"
+
+    for n in (1, 16, 128, 256):
+        row = {"n_blocks": n}
+        for mode in ("nccl_discrete_per_block", "nccl_discrete_grouped", "nccl_aggregated",
+                     "fused"):
+            reps = 5 if n >= 128 or mode != "nccl_discrete_per_block" else 3
+            ts = []
+            for r in range(reps + 1):
+                src = src_all[rng.choice(len(src_all), n, replace=False)]
+                dst = D.alloc_mem(n)
+                dv[:, torch.as_tensor(M.addr_indices(dst), device="cuda:0")] = 0
+                torch.cuda.synchronize()
+                t0 = _t.perf_counter()
+                if mode == "fused":      # the receiver allocates inside the call
+                    D.free_mem(dst)
+                    dst = P.transfer(1, src)
+                elif mode == "nccl_aggregated":
+                    P.pack(src, 0, L, stg[0].data_ptr())
+                    P.sync()
+                    comm.exchange(0, [stg[0].data_ptr()], [n * Pb], 0, [stg[1].data_ptr()],
+                                  [n * Pb], stream.cuda_stream)
+                    stream.synchronize()
+                    D.unpack(stg[1].data_ptr(), dst, 0, L)
+                    D.sync()
+                else:
+                    sp, dp = chunk_ptrs(pv, M.addr_indices(src)), chunk_ptrs(dv, M.addr_indices(dst))
+                    step = 2 * L if mode == "nccl_discrete_per_block" else len(sp)
+                    for k in range(0, len(sp), step):
+                        comm.exchange(0, sp[k:k + step], [c] * step, 0, dp[k:k + step],
+                                      [c] * step, stream.cuda_stream)
+                    stream.synchronize()
+                dt = _t.perf_counter() - t0
+                check(src, dst)
+                D.free_mem(dst)
+                if r:
+                    ts.append(dt)
+            ms = float(np.median(ts)) * 1e3
+            row[mode] = {"ms": round(ms, 3), "GBps": round(n * Pb / (ms * 1e-3) / 1e9, 1),
+                         "calls": (n if mode == "nccl_discrete_per_block" else 1)}
+        out["rows"].append(row)
+        print(row, file=sys.stderr)
+    comm.close()
+    P.close()
+    D.close()
+    return out
+
+
 def tiny_latency():
     """BASELINE configs[0] (tiny pool: L2 H2 D64 fp16, B16, 64 blocks per
     instance) is latency-bound, not roofline-graded: host
@@ -429,5 +519,5 @@ def tiny_latency():
 if __name__ == "__main__":
     fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency,
           "dram_source": dram_source_sweep, "gs": gs_latency, "chain": chain_sweep,
-          "tiny": tiny_latency}[sys.argv[1]]
+          "tiny": tiny_latency, "nccl": nccl_sweep}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))

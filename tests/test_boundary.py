@@ -105,3 +105,17 @@ def test_fast_binding_converts_inputs():
     with pytest.raises(M.MempoolError) as e:
         F.transfer_with_insert(0, 1, strided, addrs.T, [5, 6], 0, bytearray(b"pv"), 16)
     assert e.value.name == "CONFIG"
+
+
+def test_nccl_arm_exports_every_declared_symbol():
+    """libmempool_nccl.so (the paper's NCCL transport, comparison arm) loads
+    without a GPU and exports what include/mempool_nccl.h declares."""
+    src = open(os.path.join(ROOT, "include", "mempool_nccl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = sorted(set(re.findall(r"\b(mp_nccl_[a-z0-9_]+)\s*\(", src)))
+    from paper_2406_17565_b200 import nccl_arm as N
+    lib = N.lib()
+    for name in names:
+        assert hasattr(lib, name), name
+    assert sorted(N.SIGNATURES) == names
+    assert N.version() >= 22000
