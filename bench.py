@@ -499,7 +499,80 @@ def side_measurements(M, torch, shape, seed, peak, args):
             out["swap"] = swap_point(M, torch, shape, seed)
         except Exception as e:  # report, never hide
             out["swap"] = {"error": str(e)}
+    try:
+        out["paper_transport_nccl"] = nccl_point(M, torch, shape, seed)
+    except Exception as e:      # report, never hide
+        out["paper_transport_nccl"] = {"error": str(e)}
     return out
+
+
+def nccl_point(M, torch, shape, seed, n=128):
+    """The paper's transport beside ours on the same 128 scattered blocks (a
+    2048-token prompt): NCCL send/recv of every (layer, K/V) chunk, one
+    group per block (the discrete layout), and of the aggregated
+    staging (mp_pack -> one send -> mp_unpack), through a one-rank
+    communicator (NCCL's self send/recv: the wire is this GPU's HBM), vs the
+    fused mp_transfer.  Host clock per synchronous transfer, median of 3."""
+    from paper_2406_17565_b200 import nccl_arm as N
+    dev = torch.cuda.current_device()
+    nb, c, L, Pb = 2 * n + 8, shape.chunk_bytes, shape.layers, shape.block_bytes
+    P = make_pool(M, torch, 210, dev, shape, nb)
+    D = make_pool(M, torch, 211, dev, shape, nb)
+    M.connect(P, D)
+    pv = P._region.view(2 * L, nb, c)
+    dv = D._region.view(2 * L, nb, c)
+    comm = N.NcclComm.create_single(dev)
+    st = torch.cuda.current_stream()
+    src = P.alloc_mem(n)
+    P.debug_fill(src, seed)
+    src = src[np.random.default_rng(seed).permutation(n)]
+    P.sync()
+    stg = torch.empty(2, n * Pb, dtype=torch.uint8, device=f"cuda:{dev}")
+    res = {"blocks": n, "nccl_version": N.version()}
+
+    def discrete(dst):
+        for s, d in zip(M.addr_indices(src), M.addr_indices(dst)):
+            sp = [pv.data_ptr() + (j * nb + int(s)) * c for j in range(2 * L)]
+            dp = [dv.data_ptr() + (j * nb + int(d)) * c for j in range(2 * L)]
+            comm.exchange(0, sp, [c] * (2 * L), 0, dp, [c] * (2 * L), st.cuda_stream)
+        st.synchronize()
+        return dst
+
+    def aggregated(dst):
+        P.pack(src, 0, L, stg[0].data_ptr())
+        P.sync()
+        comm.exchange(0, [stg[0].data_ptr()], [n * Pb], 0, [stg[1].data_ptr()], [n * Pb],
+                      st.cuda_stream)
+        st.synchronize()
+        D.unpack(stg[1].data_ptr(), dst, 0, L)
+        D.sync()
+        return dst
+
+    def fused(dst):
+        D.free_mem(dst)
+        return P.transfer(D.inst, src)
+
+    for name, fn in (("nccl_discrete_per_block", discrete), ("nccl_aggregated", aggregated),
+                     ("fused", fused)):
+        ts = []
+        for r in range(4):
+            dst = D.alloc_mem(n)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dst = fn(dst)
+            dt = time.perf_counter() - t0
+            s_ids = torch.as_tensor(M.addr_indices(src), device=f"cuda:{dev}")
+            d_ids = torch.as_tensor(M.addr_indices(dst), device=f"cuda:{dev}")
+            if not bool((pv[0, s_ids] == dv[0, d_ids]).all()):
+                raise RuntimeError(f"{name}: destination bytes differ")
+            D.free_mem(dst)
+            if r:
+                ts.append(dt)
+        res[f"{name}_GBps"] = round(n * Pb / float(np.median(ts)) / 1e9, 1)
+    comm.close()
+    P.close()
+    D.close()
+    return res
 
 
 def swap_point(M, torch, shape, seed):

@@ -6,8 +6,10 @@ fused one-sided path.  Argument marshalling only.
     comm = NcclComm.create(world, rank, device, uid)  # uid from rank 0, any bootstrap
     comm.exchange(peer, send_ptrs, send_bytes, peer, recv_ptrs, recv_bytes, stream)
 """
+import contextlib
 import ctypes as C
 import os
+import sys
 
 import numpy as np
 
@@ -67,11 +69,29 @@ def version() -> int:
     return int(lib().mp_nccl_version())
 
 
+@contextlib.contextmanager
+def _stdout_to_stderr():
+    """NCCL may print its version banner on stdout at communicator init;
+    bench.py's stdout must carry exactly one JSON line."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    try:
+        os.dup2(2, 1)
+        yield
+    finally:
+        libc = C.CDLL(None)
+        libc.fflush(None)
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 class NcclComm:
     def __init__(self, world: int, rank: int, device: int, uid: bytes):
         h = C.c_void_p()
         b = C.create_string_buffer(bytes(uid), 128)
-        _check(lib().mp_nccl_comm_init(world, rank, b, device, C.byref(h)), "comm_init")
+        with _stdout_to_stderr():
+            r = lib().mp_nccl_comm_init(world, rank, b, device, C.byref(h))
+        _check(r, "comm_init")
         self._h = h
         self.rank = rank
         self.world = world
