@@ -10,11 +10,15 @@
 //    cp.async.bulk (TMA) ring through shared memory (64 KiB units, one
 //    elected lane per CTA, the default inside one GPU's HBM).  Units are
 //    claimed dynamically from a per-pool device counter (the fast SMs take
-//    more), source ids of short lists come by value in the launch
-//    parameters, destination ids from the device allocator's table.
+//    more); short id lists (source, and destination when both fit) come by
+//    value in the launch parameters, longer ones from id tables (the
+//    destination table is the device allocator's output).  Launched with
+//    programmatic dependent launch: the next migration's CTAs start as this
+//    one drains and wait at griddepcontrol.wait.
 //  * alloc_kernel / free_kernel : the device-resident block allocator
 //    (BASELINE.json north_star item 1) over a bitmap, lowest-first; pending
-//    frees ride in the allocation kernel's parameters.
+//    updates (frees, and claims the host made for mp_alloc_mem) ride in the
+//    allocation kernel's parameters.
 //  * fill_kernel : test/bench-only synthetic KV writer (content model).
 #include <cstdlib>
 #include <utility>
