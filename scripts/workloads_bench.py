@@ -85,12 +85,21 @@ def prefill(P, prompt):
     return full
 
 
+TURN_EV = None   # list collecting (turn, start_event, end_event) when set
+
+
 def loogle_session(P, D, sess):
     moved = 0
     prompts = []
-    for t in sess.turns:
+    for ti, t in enumerate(sess.turns):
         src = prefill(P, t.prompt)
+        if TURN_EV is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            P.record_event(ev[0])
         final, nm = P.transfer_with_insert(D.inst, t.prompt, src, flags=FLAGS)
+        if TURN_EV is not None:
+            D.record_event(ev[1])
+            TURN_EV.append((ti, nm, ev))
         moved += nm
         prompts.append((t.prompt, src[len(t.prompt) // B:], final[len(t.prompt) // B:]))
     for prompt, p_part, d_part in prompts:       # the session ends: both sides retire it
@@ -195,6 +204,26 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     st = [x.stats() for x in (P, D)]
+    turn_lat = None
+    if args.workload == "loogle":
+        # device time of each turn's transfer (untimed pass after the region,
+        # events on the shared copy stream): turn 1 moves the document,
+        # turns 2-5 only their new blocks (DEDUP)
+        global TURN_EV
+        TURN_EV = []
+        for s in sessions[:4]:
+            fn(P, D, s)
+        for x in (P, D):
+            x.sync()
+        first = [a.elapsed_time(b) for ti, _, (a, b) in TURN_EV if ti == 0]
+        rest = [a.elapsed_time(b) for ti, _, (a, b) in TURN_EV if ti > 0]
+        nrest = [nm for ti, nm, _ in TURN_EV if ti > 0]
+        turn_lat = {"turn1_document_ms_p50": round(float(np.median(first)), 3),
+                    "turns2to5_incremental_ms_p10_p50_p90":
+                        [round(float(np.percentile(rest, q)), 4) for q in (10, 50, 90)],
+                    "turns2to5_blocks_moved_p50": float(np.median(nrest)),
+                    "sessions": 4}
+        TURN_EV = None
     # sampled launches stand for every profiled one (per pool; ratio
     # estimator: kernel time per byte of the sampled launches x all bytes)
     kms = sum(s["kernel_ms"] * s["profiled_bytes"] / s["timed_bytes"]
@@ -215,6 +244,7 @@ def main():
                      "launches": kl, "share_of_time": round(kms / ms, 4),
                      "timed_every": args.profile_every,
                      "host_ms": round(host_ms, 3)},
+        "turn_latency": turn_lat,
         "engine_alloc": "drain" if args.drain_alloc else "stream_ordered",
         "sessions_retained": RETAIN,
         "clocks": clocks.summary()}))
