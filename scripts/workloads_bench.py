@@ -112,9 +112,15 @@ def loogle_session(P, D, sess):
 
 
 def react_session(P, D, sess):
-    moved = 0
+    return sum(react_steps(P, D, sess))
+
+
+def react_steps(P, D, sess):
+    """One ReAct session as a generator: yields the blocks moved per turn, so
+    several sessions can be interleaved turn by turn (--concurrent)."""
     retire = []
     for t in sess.turns:
+        moved = 0
         src = prefill(P, t.prompt)
         fin_d, nm = P.transfer_with_insert(D.inst, t.prompt, src, flags=FLAGS)
         moved += nm
@@ -127,9 +133,30 @@ def react_session(P, D, sess):
         D.free_mem(d_addrs[len(whole) // B:])
         P.free_mem(src[k:])
         retire.append(whole)
+        yield moved
     for whole in retire if not RETAIN else ():
         P.delete(whole)
         D.delete(whole)
+
+
+def interleaved(P, D, sessions, k):
+    """k ReAct sessions in flight, advanced one turn each in round robin (a
+    serving loop with k concurrent agents); a finished one is replaced by
+    the next session."""
+    moved = 0
+    pending = list(sessions)
+    live = []
+    while pending or live:
+        while pending and len(live) < k:
+            live.append(react_steps(P, D, pending.pop(0)))
+        nxt = []
+        for g in live:
+            try:
+                moved += next(g)
+                nxt.append(g)
+            except StopIteration:
+                pass
+        live = nxt
     return moved
 
 
@@ -150,6 +177,8 @@ def main():
                     help="time every k-th migration launch (1: all; events cost a few us each)")
     ap.add_argument("--no-profile", action="store_true",
                     help="no per-launch timing events (kernel shares are then unavailable)")
+    ap.add_argument("--concurrent", type=int, default=1,
+                    help="react: sessions in flight, interleaved turn by turn")
     ap.add_argument("--coalesce-mib", type=int, default=0,
                     help="launch coalescing limit (0: library default 1 GiB, <0: off)")
     args = ap.parse_args()
@@ -193,7 +222,10 @@ def main():
                 print(f"{k:24s} calls {n:5d}  total {t * 1e3:8.3f} ms  per call {t / n * 1e6:7.1f} us",
                       file=sys.stderr)
         else:
-            moved = sum(fn(P, D, s) for s in sessions)
+            if args.workload == "react" and args.concurrent > 1:
+                moved = interleaved(P, D, sessions, args.concurrent)
+            else:
+                moved = sum(fn(P, D, s) for s in sessions)
         if args.prof:
             pr.disable()
             pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(15)
