@@ -49,7 +49,12 @@ static PyArrayObject* new_u64(npy_intp n) {
   return (PyArrayObject*)PyArray_SimpleNew(1, &n, NPY_UINT64);
 }
 
-static mp_pool* handle(PyObject* o) { return (mp_pool*)PyLong_AsVoidPtr(o); }
+/* Not an int: NULL, which every entry point rejects with MP_ERR_CONFIG. */
+static mp_pool* handle(PyObject* o) {
+  void* p = PyLong_AsVoidPtr(o);
+  if (!p && PyErr_Occurred()) PyErr_Clear();
+  return (mp_pool*)p;
+}
 
 static PyObject* py_set_error_factory(PyObject* self, PyObject* f) {
   Py_XINCREF(f);
@@ -66,8 +71,9 @@ static PyObject* py_alloc_mem(PyObject* self, PyObject* args) {
   PyArrayObject* out = new_u64(n > 0 ? (npy_intp)n : 0);
   if (!out) return NULL;
   int st;
+  mp_pool* p = handle(h);  /* with the GIL held */
   Py_BEGIN_ALLOW_THREADS
-  st = mp_alloc_mem(handle(h), n, type, req, (mp_addr*)PyArray_DATA(out));
+  st = mp_alloc_mem(p, n, type, req, (mp_addr*)PyArray_DATA(out));
   Py_END_ALLOW_THREADS
   if (st != MP_OK) {
     Py_DECREF(out);

@@ -85,6 +85,9 @@ def test_fast_binding_loads_and_reports_status():
         assert e.value.name == "CONFIG"
     with pytest.raises((TypeError, ValueError)):
         F.free_mem(0, "not an addr list")
+    with pytest.raises(M.MempoolError) as e:       # a handle that is not an int
+        F.free_mem("not a pool", [1])
+    assert e.value.name == "CONFIG"
 
 
 def test_fast_binding_converts_inputs():
