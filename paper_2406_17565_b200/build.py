@@ -70,6 +70,14 @@ def build_nccl_arm(verbose: bool = False) -> str:
     return NCCL_LIB
 
 
+def _build_nccl_arm_soft(verbose: bool = False):
+    """The comparison arm must not fail the product's build."""
+    try:
+        build_nccl_arm(verbose)
+    except Exception as e:  # reported, not fatal
+        sys.stderr.write(f"warning: libmempool_nccl.so (NCCL comparison arm) not built: {e}\n")
+
+
 def nccl_stale() -> bool:
     if not os.path.exists(NCCL_LIB):
         return True
@@ -118,7 +126,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if pyext_stale():
             build_pyext(verbose)
         if nccl_stale():
-            build_nccl_arm(verbose)
+            _build_nccl_arm_soft(verbose)
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
@@ -133,7 +141,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
         f.write(res.stderr)
     build_pyext(verbose)
-    build_nccl_arm(verbose)
+    _build_nccl_arm_soft(verbose)
     return LIB
 
 
