@@ -522,13 +522,19 @@ static cudaError_t launch_bulk_any(const Endpoint& src, const Endpoint& dst, int
 //   0 = 64 KiB x 3 (1 CTA / SM)     1 = 32 KiB x 3 (2 CTAs / SM)
 //   2 = 8 KiB x 6 (4 CTAs / SM)     3 = 16 KiB x 4 (3 CTAs / SM)
 //   4 = 32 KiB x 6 (1 CTA / SM)     5 = 48 KiB x 4 (1 CTA / SM)
-static int bulk_cfg() {
-  static int cfg = -1;
-  if (cfg < 0) {
+// Without the knob the geometry follows the launch's size: below 128 MiB
+// (under ~14 units of 64 KiB per SM) 16 KiB x 4 stages spread the copy over
+// more, shorter units (back-to-back 1-8-block transfers 2-5% faster), above
+// it 64 KiB x 3 (the 2 GiB sweep's and the bench's best; 16 KiB x 4 loses
+// 4% there).
+static int bulk_cfg(unsigned long long bytes) {
+  static int cfg = -2;
+  if (cfg == -2) {
     const char* e = getenv("MP_BULK_CFG");
-    cfg = (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : 0;
+    cfg = (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : -1;
   }
-  return cfg;
+  if (cfg >= 0) return cfg;
+  return bytes < (128ull << 20) ? 3 : 0;
 }
 
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
@@ -541,7 +547,7 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
     return cudaErrorInvalidValue;
   const InlineIds& si = src_inline ? *src_inline : no_ids;
   if (variant == kCopyBulk) {
-    switch (bulk_cfg()) {
+    switch (bulk_cfg((unsigned long long)n * (unsigned long long)nj * (unsigned long long)chunk)) {
       case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
       case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
       case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
