@@ -115,6 +115,9 @@ def react_session(P, D, sess):
     return sum(react_steps(P, D, sess))
 
 
+DIR = {"p2d_sent": 0, "p2d_moved": 0, "d2p_moved": 0}   # ReAct per-direction block counts
+
+
 def react_steps(P, D, sess):
     """One ReAct session as a generator: yields the blocks moved per turn, so
     several sessions can be interleaved turn by turn (--concurrent)."""
@@ -124,12 +127,15 @@ def react_steps(P, D, sess):
         src = prefill(P, t.prompt)
         fin_d, nm = P.transfer_with_insert(D.inst, t.prompt, src, flags=FLAGS)
         moved += nm
+        DIR["p2d_sent"] += len(src)
+        DIR["p2d_moved"] += nm
         whole = np.concatenate([t.prompt, t.gen])
         k = len(t.prompt) // B
         D.free_mem(fin_d[k:])                                 # the prompt's partial block
         d_addrs = prefill(D, whole)                           # decode appends blocks
         _, nm2 = D.transfer_with_insert(P.inst, whole, d_addrs[k:], flags=M.XFER_ASYNC)
         moved += nm2
+        DIR["d2p_moved"] += nm2
         D.free_mem(d_addrs[len(whole) // B:])
         P.free_mem(src[k:])
         retire.append(whole)
@@ -209,6 +215,8 @@ def main():
             x.profile(not args.no_profile, every=args.profile_every)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for key in DIR:
+            DIR[key] = 0
         e0.record()
         h0 = time.perf_counter()
         if args.prof:
@@ -277,6 +285,11 @@ def main():
                      "timed_every": args.profile_every,
                      "host_ms": round(host_ms, 3)},
         "turn_latency": turn_lat,
+        "directions": ({"p_to_d_blocks_sent": DIR["p2d_sent"],
+                        "p_to_d_blocks_moved": DIR["p2d_moved"],
+                        "p_to_d_blocks_avoided_by_dedup": DIR["p2d_sent"] - DIR["p2d_moved"],
+                        "d_to_p_blocks_moved": DIR["d2p_moved"]}
+                       if args.workload == "react" else None),
         "engine_alloc": "drain" if args.drain_alloc else "stream_ordered",
         "sessions_retained": RETAIN,
         "clocks": clocks.summary()}))
