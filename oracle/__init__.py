@@ -19,7 +19,12 @@ dst[d_j] == src[s_j], np.take cross-check), golden worked example; and by
 independent models in tests/test_oracle_pins.py: LRU eviction and swap-out
 victims (R7-R9, recency recomputed from the op history), evict-before-OOM
 feasibility (R2, subset brute force), DEDUP reuse of the receiver's cached
-prefix (R3, bytes + reuse + conservation).  Tie-breaks between equally recent
+prefix (R3, bytes + reuse + conservation); the block aggregation (pack's
+layout and the network-call counts of P:546-552: 10,240 discrete vs 128
+aggregated calls for the paper's 2048-token / L=40 instance, block i at
+i*Pb; tests/test_oracle_aggregation.py); the global scheduler's routing
+(gs_oracle.py) by hand-derived cases of P:641-649 incl. the TTL boundary
+(tests/test_gs.py).  Tie-breaks between equally recent
 blocks (lowest block index) are a reading no model can pin: a single op
 never leaves two leaves equally recent, so it only orders the initial state.
 """
@@ -27,4 +32,5 @@ from .mempool_oracle import (  # noqa: F401
     HBM, DRAM, MIXED, FREE, ACTIVE, INDEXED, ORPHAN,
     FLAG_DST_GIVEN, FLAG_DEDUP, FLAG_INS_ERR_ON_CONFLICT, FLAG_MATCH_PIN,
     MPError, OraclePool, transfer, transfer_with_insert, transfer_heads, tp_plan,
+    pack, network_calls,
 )

@@ -227,7 +227,8 @@ class OraclePool:
 
     # ------------------------------------------------------------------- index
     def _prefix(self, tokens, k):
-        return tuple(int(t) for t in tokens[: k * self.B])
+        # the key is the tuple of Python ints tokens[:k*B] (R1)
+        return tuple(np.asarray(tokens[: k * self.B], dtype=np.int64).tolist())
 
     def _peek_match(self, tokens):
         """Longest k <= floor(n/B) with prefix_k in the map (no side effects)."""
@@ -643,3 +644,55 @@ def transfer_with_insert(src, dst, tokens, src_addrs, dst_addrs=None, flags=0,
         final.append(full[floor_b])
     dst.inbox.append(("transfer_with_insert", src.inst, bytes(priv), list(final)))
     return final, nm, dup
+
+
+# ------------------------------------------------------------- aggregation
+def pack(pool, addrs, layer_begin=0, layer_end=None):
+    """A4, the block aggregation of P:549-550 ("instead of having two blocks
+    per layer, we aggregate them into one block; the new block size equals
+    2*L smaller blocks").  Returns the staging buffer as uint64 words of shape
+    [n][l1-l0][2][W]: block i, layer l, K (kv=0) then V (kv=1) -- reading R11
+    (layer-major, K before V).  Block i therefore starts at word offset
+    i*(l1-l0)*2*W, i.e. byte i*Pb for a whole-request (all-layer) staging."""
+    layer_end = pool.L if layer_end is None else layer_end
+    if not (0 <= layer_begin < layer_end <= pool.L):
+        raise MPError("CONFIG")
+    for a in addrs:
+        pool._check_addr(a)
+    out = np.zeros((len(addrs), layer_end - layer_begin, 2, pool.W), np.uint64)
+    for i, a in enumerate(addrs):
+        words = pool.block_bytes(a)                 # [2L][W], aggregated order
+        for l in range(layer_begin, layer_end):
+            for kv in (0, 1):
+                out[i, l - layer_begin, kv] = words[2 * l + kv]
+    return out
+
+
+def network_calls(n_tokens, B, L, chunk_bytes, mode):
+    """The network API calls one request's KV needs, as a list of
+    (staging byte offset, bytes) -- one entry per call.
+
+    * "by_request" / "by_layer" with the discrete layout: "each call only
+      transmits a single block" and "the number of network API calls equals
+      the number of discrete memory blocks, regardless of whether the
+      by-layer or by-request approach is used": one call per
+      (token block, layer, K/V) chunk of c bytes.  Offsets are those of the
+      chunk in an aggregated image (block-major), for comparison only.
+    * "by_request_agg": the 2*L chunks of a token block are one aggregated
+      block of Pb = 2*L*c bytes: one call per token block,
+      block i at offset i*Pb.
+    * "by_layer_agg": "the by-layer approach inevitably needs to call the
+      network APIs at least L times": one call per layer carrying
+      that layer's K and V of every block ([n][1][2][c] staging).
+    ceil(n_tokens/B) token blocks (R1: the trailing partial block moves too)."""
+    nb = _ceil_div(n_tokens, B)
+    c = chunk_bytes
+    Pb = 2 * L * c
+    if mode in ("by_request", "by_layer"):
+        return [(i * Pb + (2 * l + kv) * c, c)
+                for i in range(nb) for l in range(L) for kv in (0, 1)]
+    if mode == "by_request_agg":
+        return [(i * Pb, Pb) for i in range(nb)]
+    if mode == "by_layer_agg":
+        return [(l * nb * 2 * c, nb * 2 * c) for l in range(L)] if nb else []
+    raise MPError("CONFIG")

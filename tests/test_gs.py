@@ -10,8 +10,43 @@ import pytest
 from oracle.gs_oracle import OracleGS
 
 
-def test_paper_cases():
-    from paper_2406_17565_b200.mempool import GlobalScheduler as GS
+class _OracleGSAdapter:
+    """OracleGS behind the product's GlobalScheduler interface (route raises
+    when no instance of the kind is registered)."""
+    PREFILL, DECODE, COLOCATED = 0, 1, 2
+
+    def __init__(self, B, ttl_seconds):
+        self.o = OracleGS(B, ttl_seconds)
+
+    def register(self, inst, kind):
+        self.o.register(inst, kind)
+
+    def set_load(self, inst, load):
+        self.o.set_load(inst, load)
+
+    def update(self, inst, toks, now):
+        self.o.update(inst, toks, now)
+
+    def route(self, kind, toks, now):
+        r = self.o.route(kind, toks, now)
+        if r is None:
+            raise LookupError("no instance of this kind")
+        return r
+
+
+def _impl(which):
+    if which == "oracle":
+        return _OracleGSAdapter
+    from paper_2406_17565_b200.mempool import GlobalScheduler
+    return GlobalScheduler
+
+
+@pytest.mark.parametrize("which", ["oracle", "product"])
+def test_paper_cases(which):
+    """Hand-derived values of the paper's routing rules, checked on the
+    oracle (its pin: nothing here comes from running either implementation)
+    and on the product."""
+    GS = _impl(which)
     g = GS(16, ttl_seconds=60.0)
     for inst, kind in ((0, GS.PREFILL), (1, GS.PREFILL), (2, GS.DECODE)):
         g.register(inst, kind)
@@ -32,6 +67,40 @@ def test_paper_cases():
     assert g.route(GS.PREFILL, q1, 61.5) == (0, 0, [(2, 192)])
     assert g.route(GS.PREFILL, q1, 63.5) == (0, 0, [])
 
+
+
+@pytest.mark.parametrize("which", ["oracle", "product"])
+def test_ttl_boundary_and_ties(which):
+    """R17 boundaries, hand-derived: an update at t is held while now < t + ttl
+    (P:648-649 "expire ... after a TTL"), so at exactly t + ttl it is gone;
+    a partial last block is not cached (block-granular trees); equal
+    prefixes tie to the least load, then the lowest id; extra holders are
+    listed longest first, ties by id."""
+    GS = _impl(which)
+    B = 4
+    g = GS(B, ttl_seconds=10.0)
+    for inst, kind in ((5, 0), (3, 0), (9, 1), (7, 2)):
+        g.register(inst, kind)
+    p = np.arange(100, 100 + 3 * B + 2, dtype=np.int32)     # 3 full blocks + 2 tokens
+    g.update(5, p, 1.0)
+    assert g.route(0, p, 10.999) == (5, 3 * B, [])
+    assert g.route(0, p, 11.0) == (3, 0, [])                 # expired at exactly t + ttl
+    g.update(5, p, 20.0)
+    g.update(3, p[: 2 * B + 1], 20.0)                        # 2 full blocks
+    assert g.route(0, p, 21.0) == (5, 3 * B, [])
+    g.update(3, p, 21.0)                                     # both hold 3 blocks: tie
+    assert g.route(0, p, 22.0) == (3, 3 * B, [])             # equal load -> lowest id
+    g.set_load(3, 1.0)
+    assert g.route(0, p, 22.0) == (5, 3 * B, [])             # least load wins the tie
+    # extra holders of any kind, longest first, ties by id
+    longer = np.concatenate([p, np.arange(7, 7 + 2 * B, dtype=np.int32)])
+    g.update(9, longer, 23.0)                                # decode: 5 full blocks
+    g.update(7, longer[: 4 * B + 3], 23.0)                   # colocated: 4 blocks
+    assert g.route(0, longer, 24.0) == (5, 3 * B, [(9, 5 * B), (7, 4 * B)])
+    # a query shorter than a cached prompt matches only its own full blocks
+    assert g.route(1, p[: B + 3], 24.0) == (9, B, [])
+    with pytest.raises(Exception):
+        GS(B, 10.0).route(0, p, 0.0)                         # no instance of the kind
 
 def test_random_vs_oracle():
     from paper_2406_17565_b200.mempool import GlobalScheduler as GS, MempoolError
