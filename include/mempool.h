@@ -32,7 +32,10 @@
  *    bitmap lazily, stream-ordered before the pool's next device allocation.
  *  - The pools of one process on one device share one data stream (migrations
  *    between them need no cross-stream wait; MP_SHARED_STREAM=0 gives each
- *    pool its own), so mp_sync on one of them also waits for the others' work.
+ *    pool its own), so mp_sync on one of them also waits for the others' work,
+ *    and pools of one device driven by different threads serialise their
+ *    data movement on that stream (it is HBM-bound either way).  The stream
+ *    is created with the device's first pool and destroyed with its last.
  *  - Layout: the HBM pool of an instance is 2*L "slabs" (K_0, V_0, K_1, V_1,
  *    ...), each hbm_blocks chunks of c = B*H*D*elem bytes (vLLM's per-layer
  *    paged layout: "two blocks per LLM layer").  Block id b is chunk b
@@ -156,6 +159,8 @@ typedef struct {
                                  (timed or not) */
   uint64_t profiled_bytes;    /* their payload bytes: kernel_ms * profiled_bytes /
                                  timed_bytes estimates their total time when sampling */
+  uint64_t overlapped_launches; /* migrations that started without waiting for the previous
+                                   grid on the stream (independent blocks) */
 } mp_stats;
 
 typedef struct {

@@ -251,6 +251,7 @@ mp_status mp_debug_fill(mp_pool* p, const mp_addr* a, int64_t n, uint64_t seed) 
   TRY(meta_fence(p));
   CK(mpk::launch_fill(p->d_slabs, d, (int)n, p->nch, p->chunk, seed, (uint64_t)p->inst, p->epoch,
                       p->stream));
+  track_fence(p->track);
   p->stats.aux_launches += 1;
   return sync(p);
 }

@@ -174,9 +174,10 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
       TRY(upload_ids(dst, dids, &t));
       dd = t;
     }
+    const LaunchBlocks lb{&src->bmarks, sids.data(), &dst->bmarks, dids.data(), n};
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, ds),
                              pool_ep(dst->d_slabs, both ? nullptr : dd), n, j0, nj, false, 0,
-                             si.n ? &si : nullptr, /*meta_dep=*/!both));
+                             si.n ? &si : nullptr, /*meta_dep=*/!both, &lb));
     dst->stats.blocks_moved += (uint64_t)n;
     return link(dst, src);
   }
@@ -194,9 +195,10 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
       TRY(src_ids(src, sids, &ds, &si));
       TRY(upload_ids(src, dids, &dd));
     }
+    const LaunchBlocks lb{&src->bmarks, sids.data(), &dst->bmarks, dids.data(), n};
     TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds),
                              pool_ep(it->second, dd), n, j0, nj, /*peer=*/true, 0,
-                             si.n ? &si : nullptr, /*meta_dep=*/!both));
+                             si.n ? &si : nullptr, /*meta_dep=*/!both, &lb));
     src->stats.blocks_moved += (uint64_t)n;
     return link(src, dst);
   }
@@ -226,6 +228,7 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
       CK(cudaMemcpyBatchAsync(ds.data(), ss.data(), sz.data(), sz.size(), &attr, &attr_idx, 1,
                               &fail, src->stream));
     }
+    track_fence(src->track);  // copies the launch window knows nothing about
     src->stats.bytes_moved += (uint64_t)(n * nj * src->chunk);
     src->stats.blocks_moved += (uint64_t)n;
     return link(src, dst);
@@ -463,6 +466,40 @@ mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, 
   return MP_OK;
 }
 
+mp_status transmit_precheck(mp_pool* src, mp_pool* dst, uint32_t path, int nj,
+                            const std::vector<uint8_t>& smeds) {
+  switch (path) {
+    case MP_XFER_PATH_AUTO:
+    case MP_XFER_PATH_FUSED:
+    case MP_XFER_PATH_CE:
+    case MP_XFER_PATH_CE_BATCH:
+      return MP_OK;
+    case MP_XFER_PATH_STAGED: {
+      bool any_hbm = false;  // DRAM sources take the direct DRAM kernel, not the ring
+      for (uint8_t m : smeds) any_hbm = any_hbm || m == MP_HBM;
+      if (!any_hbm) return MP_OK;
+      const int S = std::max(1, std::min(src->staging_slots, dst->staging_slots));
+      const int64_t slot_bytes = std::min(src->staging_bytes, dst->staging_bytes) / S;
+      if (slot_bytes < (int64_t)nj * src->chunk) {
+        set_err("staging slot smaller than one block");
+        return MP_ERR_CONFIG;
+      }
+      return MP_OK;
+    }
+    default:
+      set_err("unknown transfer path");
+      return MP_ERR_CONFIG;
+  }
+}
+
+void dst_abort(mp_pool* dst, DstPrep& st) {
+  unpin_nodes(dst, st.matched);
+  st.matched.clear();
+  if (!(st.flags & MP_XFER_DST_GIVEN))
+    for (int32_t id : st.dids) free_block(dst, MP_HBM, id);
+  st.dids.clear();
+}
+
 // ------------------------------------------------- receiver: insertion step
 mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out) {
   Msg msg{st.kind, st.src_inst, {}, {}};
@@ -513,6 +550,7 @@ mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t
   if (rp)
     return remote_transfer(src, rp, 0, nullptr, 0, sids, smeds, n, da, flags, l0, l1, priv,
                            priv_len, nullptr);
+  TRY(transmit_precheck(src, dst, flags & MP_XFER_PATH_MASK, 2 * (l1 - l0), smeds));
   // ---- (1) allocation at the receiver ----
   DstPrep st;
   hint_slot(src, dst, flags, smeds, 2 * l0, 2 * (l1 - l0));
@@ -520,8 +558,12 @@ mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t
   dst->slot_hint.src = nullptr;
   TRY(ps);
   // ---- (2) transmission ----
-  TRY(transmit(src, dst, sids, smeds, st.dids, st.d_dst, 2 * l0, 2 * (l1 - l0),
-               flags & MP_XFER_PATH_MASK));
+  const mp_status xs = transmit(src, dst, sids, smeds, st.dids, st.d_dst, 2 * l0,
+                                2 * (l1 - l0), flags & MP_XFER_PATH_MASK);
+  if (xs != MP_OK) {
+    dst_abort(dst, st);
+    return xs;
+  }
   // ---- (3) completion ----
   TRY(dst_commit(dst, st, da));
   return finish(src, dst, flags);
@@ -555,6 +597,7 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
   if (rp)
     return remote_transfer(src, rp, 1, toks, n_tok, sids, smeds, m, da, flags, 0, src->L, priv,
                            priv_len, n_moved);
+  TRY(transmit_precheck(src, dst, flags & MP_XFER_PATH_MASK, src->nch, smeds));
   lap(0);
   // ---- (1) allocation at the receiver, with its DEDUP match ----
   DstPrep st;
@@ -567,8 +610,12 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
   // ---- (2) transmission of all layers ----
   std::vector<int32_t> moved_src(sids.begin() + st.skip, sids.end());
   std::vector<uint8_t> moved_med(smeds.begin() + st.skip, smeds.end());
-  TRY(transmit(src, dst, moved_src, moved_med, st.dids, st.d_dst, 0, src->nch,
-               flags & MP_XFER_PATH_MASK));
+  const mp_status xs = transmit(src, dst, moved_src, moved_med, st.dids, st.d_dst, 0, src->nch,
+                                flags & MP_XFER_PATH_MASK);
+  if (xs != MP_OK) {
+    dst_abort(dst, st);
+    return xs;
+  }
   lap(2);
   // ---- (3) insertion at the receiver, ok ----
   TRY(dst_commit(dst, st, da));
@@ -625,11 +672,12 @@ mp_status mp_transfer_heads(mp_pool* src, int32_t dst_inst, const mp_addr* sa, i
     mpk::InlineIds si;
     TRY(src_ids(ex, sids, &ds, &si));
     TRY(upload_ids(ex, dids, &dd));
+    const LaunchBlocks lb{&src->bmarks, sids.data(), &dst->bmarks, dids.data(), n};
     TRY(launch_migrate_timed(ex, ex->stream,
                              pool_ep(src->d_slabs, ds, src->chunk, src_head0 * head_bytes),
                              pool_ep(dslabs, dd, dst->chunk, dst_head0 * head_bytes), n, 2 * l0,
                              2 * (l1 - l0), /*peer=*/!same_dev, n_heads * head_bytes,
-                             si.n ? &si : nullptr));
+                             si.n ? &si : nullptr, true, &lb));
     ex->stats.blocks_moved += (uint64_t)n;
   }
   TRY(same_dev ? link(dst, src) : link(src, dst));

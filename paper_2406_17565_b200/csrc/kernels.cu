@@ -20,6 +20,7 @@
 //    updates (frees, and claims the host made for mp_alloc_mem) ride in the
 //    allocation kernel's parameters.
 //  * fill_kernel : test/bench-only synthetic KV writer (content model).
+#include <atomic>
 #include <cstdlib>
 #include <utility>
 
@@ -78,6 +79,12 @@ __device__ __forceinline__ long long dst_id(const Endpoint& dst, const InlineIds
 // of the running grid releases its dependents once it has claimed its last
 // unit.  Nothing global is touched before the wait: the dynamic-claiming
 // counter is shared by consecutive launches.
+// Independent launches (the host found no block the previous launches of its
+// window write and this one reads or writes, or the other way round) skip the
+// wait at the start and overlap the previous grid's tail.  Every grid still
+// waits before its CTAs exit, so a grid completes only after its predecessor
+// has: completion stays ordered along the stream, and a later launch that
+// does wait at its start sees every earlier grid complete.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_release() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -86,19 +93,23 @@ __device__ __forceinline__ void pdl_release() {
 // Copies `len` bytes per chunk (the whole chunk, or a head range of it).
 constexpr unsigned kGroup = 8;  // units per dynamic claim (32 KiB per warp)
 
+// 3 CTAs x 256 threads per SM (85 registers): 96 KiB of loads in flight per
+// SM, more than HBM or NVLink needs, and no register spills (at 4 CTAs the
+// 64-register cap spilled 20 bytes per thread).
 template <bool kSrcPool, bool kDstPool>
-__global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endpoint dst, int j0,
+__global__ void __launch_bounds__(kThreads, 3) migrate_kernel(Endpoint src, Endpoint dst, int j0,
                                                            int nj, long long len,
                                                            unsigned units_per_chunk,
                                                            unsigned total_units,
                                                            const __grid_constant__ InlineIds sinl,
                                                            unsigned long long* ctr,
-                                                           unsigned long long base) {
+                                                           unsigned long long base,
+                                                           int wait_prev) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned warp = (blockIdx.x * (unsigned)kThreads + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * (unsigned)kThreads) >> 5;
   const bool full_units = (len % kUnitBytes) == 0;
-  pdl_wait();
+  if (wait_prev) pdl_wait();
   const long long chunk = len;
   auto copy_unit = [&](unsigned u) {
     const unsigned ch = u / units_per_chunk;
@@ -128,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
   if (!ctr) {  // static grid-stride split
     for (unsigned u = warp; u < total_units; u += nwarps) copy_unit(u);
     pdl_release();
+    if (threadIdx.x == 0) pdl_wait();  // complete only after the previous grid
     return;
   }
   // dynamic: warp w starts on group w; later groups (nwarps + claim) come
@@ -149,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 4) migrate_kernel(Endpoint src, Endp
     if (g >= ngroups) break;
   }
   pdl_release();
+  if (threadIdx.x == 0) pdl_wait();  // complete only after the previous grid
 }
 
 // ---------------------------------------------------------------------------
@@ -259,13 +272,13 @@ template <int kPiece, int kStages, bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     Endpoint src, Endpoint dst, int j0, int nj, long long chunk, unsigned pieces_per_chunk,
     unsigned total_units, unsigned long long* ctr, unsigned long long base,
-    const __grid_constant__ InlineIds sinl) {
+    const __grid_constant__ InlineIds sinl, int wait_prev) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   if (threadIdx.x != 0) return;
   for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  pdl_wait();
+  if (wait_prev) pdl_wait();
   UnitSource units{ctr, base, total_units, blockIdx.x, gridDim.x};
   const char* sp;
   char* dp;
@@ -317,6 +330,7 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     }
   }
   bulk_wait_all();
+  pdl_wait();  // complete only after the previous grid
 }
 
 // Migration launches carry the PDL attribute (MP_PDL=0 turns it off).
@@ -456,18 +470,21 @@ int sm_count(int device) {
 
 // MP_BULK_SCHED=static turns the dynamic unit claiming off (comparison knob).
 static bool bulk_dynamic() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = getenv("MP_BULK_SCHED");
-    v = (e && e[0] == 's') ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && e[0] == 's');
+  }();
+  return v;
 }
+
+// Per-device caches of the launch caps (resident CTAs x SMs); pools on other
+// threads may launch concurrently, so the slots are atomics.
+using CapCache = std::atomic<int>[64];
 
 template <int kPieceT, int kStagesT, bool kSrcPool, bool kDstPool>
 static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                                long long chunk, int max_ctas, cudaStream_t stream,
-                               const Sched* sched, const InlineIds& sinl) {
+                               const Sched* sched, const InlineIds& sinl, bool wait_prev) {
   auto kern = migrate_bulk_kernel<kPieceT, kStagesT, kSrcPool, kDstPool>;
   const unsigned pieces = (unsigned)((chunk + kPieceT - 1) / kPieceT);
   const unsigned long long total = (unsigned long long)n * nj * pieces;
@@ -475,23 +492,25 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
   const size_t smem = (size_t)kStagesT * kPieceT;
   int dev = 0;
   cudaGetDevice(&dev);
-  static int cached_cap[64] = {0};  // per device (the smem attribute is per device too)
+  static CapCache cached_cap{};  // per device (the smem attribute is per device too)
   int cap = max_ctas;
-  if (dev >= 64 || cached_cap[dev] <= 0) {
+  const int cached = dev < 64 ? cached_cap[dev].load(std::memory_order_acquire) : 0;
+  if (cached <= 0) {
+    // idempotent: two threads may both get here the first time
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkThreads, smem);
     if (per_sm <= 0) per_sm = 1;
-    if (dev < 64) cached_cap[dev] = per_sm * sm_count(dev);
+    if (dev < 64) cached_cap[dev].store(per_sm * sm_count(dev), std::memory_order_release);
     if (cap <= 0) cap = per_sm * sm_count(dev);
   } else if (cap <= 0) {
-    cap = cached_cap[dev];
+    cap = cached;
   }
   const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
   const bool dyn = sched && sched->ctr && bulk_dynamic();
   const cudaError_t e = launch_pdl(kern, grid, kBulkThreads, smem, stream, src, dst, j0, nj, chunk,
                                    pieces, (unsigned)total, dyn ? sched->ctr : nullptr,
-                                   dyn ? *sched->base : 0ull, sinl);
+                                   dyn ? *sched->base : 0ull, sinl, wait_prev ? 1 : 0);
   if (dyn && e == cudaSuccess) *sched->base += total + (unsigned long long)grid;
   return e;
 }
@@ -499,19 +518,19 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
 template <int kPieceT, int kStagesT>
 static cudaError_t launch_bulk_any(const Endpoint& src, const Endpoint& dst, int n, int j0,
                                    int nj, long long chunk, int max_ctas, cudaStream_t stream,
-                                   const Sched* sc, const InlineIds& si) {
+                                   const Sched* sc, const InlineIds& si, bool w) {
   const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
   if (sp && dp)
     return launch_bulk<kPieceT, kStagesT, true, true>(src, dst, n, j0, nj, chunk, max_ctas, stream,
-                                                      sc, si);
+                                                      sc, si, w);
   if (sp)
     return launch_bulk<kPieceT, kStagesT, true, false>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                       stream, sc, si);
+                                                       stream, sc, si, w);
   if (dp)
     return launch_bulk<kPieceT, kStagesT, false, true>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                       stream, sc, si);
+                                                       stream, sc, si, w);
   return launch_bulk<kPieceT, kStagesT, false, false>(src, dst, n, j0, nj, chunk, max_ctas,
-                                                      stream, sc, si);
+                                                      stream, sc, si, w);
 }
 
 
@@ -528,18 +547,17 @@ static cudaError_t launch_bulk_any(const Endpoint& src, const Endpoint& dst, int
 // it 64 KiB x 3 (the 2 GiB sweep's and the bench's best; 16 KiB x 4 loses
 // 4% there).
 static int bulk_cfg(unsigned long long bytes) {
-  static int cfg = -2;
-  if (cfg == -2) {
+  static const int cfg = [] {
     const char* e = getenv("MP_BULK_CFG");
-    cfg = (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : -1;
-  }
+    return (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : -1;
+  }();
   if (cfg >= 0) return cfg;
   return bytes < (128ull << 20) ? 3 : 0;
 }
 
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                            long long chunk, int max_ctas, cudaStream_t stream, int variant,
-                           const Sched* sched, const InlineIds* src_inline) {
+                           const Sched* sched, const InlineIds* src_inline, bool wait_prev) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
   static const InlineIds no_ids{};
   if (src_inline && (src_inline->n != n || (src_inline->nd && (src_inline->nd != n ||
@@ -548,12 +566,12 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   const InlineIds& si = src_inline ? *src_inline : no_ids;
   if (variant == kCopyBulk) {
     switch (bulk_cfg((unsigned long long)n * (unsigned long long)nj * (unsigned long long)chunk)) {
-      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
-      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
-      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
-      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
-      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
-      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si);
+      case 1: return launch_bulk_any<32768, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si, wait_prev);
+      case 2: return launch_bulk_any<8192, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si, wait_prev);
+      case 3: return launch_bulk_any<16384, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si, wait_prev);
+      case 4: return launch_bulk_any<32768, 6>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si, wait_prev);
+      case 5: return launch_bulk_any<49152, 4>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si, wait_prev);
+      default: return launch_bulk_any<65536, 3>(src, dst, n, j0, nj, chunk, max_ctas, stream, sched, si, wait_prev);
     }
   }
   const unsigned units_per_chunk = (unsigned)((chunk + kUnitBytes - 1) / kUnitBytes);
@@ -564,18 +582,19 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   const bool sp = src.slabs != nullptr, dp = dst.slabs != nullptr;
   // One full wave: resident CTAs per SM x SM count (148 on B200), so no CTA
   // waits for a second wave; the grid-stride loop spreads the units.
-  static int cached_cap[64] = {0};  // per device: resident CTAs x SMs
+  static CapCache cached_cap{};  // per device: resident CTAs x SMs
   int cap = max_ctas;
   if (cap <= 0) {
-    if (dev < 64 && cached_cap[dev] > 0) {
-      cap = cached_cap[dev];
+    const int cached = dev < 64 ? cached_cap[dev].load(std::memory_order_acquire) : 0;
+    if (cached > 0) {
+      cap = cached;
     } else {
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, migrate_kernel<true, true>,
                                                     kThreads, 0);
       if (per_sm <= 0) per_sm = 1;
       cap = per_sm * sm_count(dev);
-      if (dev < 64) cached_cap[dev] = cap;
+      if (dev < 64) cached_cap[dev].store(cap, std::memory_order_release);
     }
   }
   const unsigned long long want = (total + (kThreads / 32) - 1) / (kThreads / 32);
@@ -586,7 +605,8 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
   auto kern = sp ? (dp ? migrate_kernel<true, true> : migrate_kernel<true, false>)
                  : (dp ? migrate_kernel<false, true> : migrate_kernel<false, false>);
   const cudaError_t e = launch_pdl(kern, grid, kThreads, 0, stream, src, dst, j0, nj, chunk,
-                                   units_per_chunk, (unsigned)total, si, ctr, sbase);
+                                   units_per_chunk, (unsigned)total, si, ctr, sbase,
+                                   wait_prev ? 1 : 0);
   if (dyn && e == cudaSuccess) {
     const unsigned long long groups = (total + kGroup - 1) / kGroup;
     const unsigned long long warps = (unsigned long long)grid * (kThreads / 32);

@@ -57,9 +57,13 @@ enum CopyVariant { kCopyAuto = 0, kCopyVector = 1, kCopyBulk = 2 };
 // sched (nullable, bulk only): claim units dynamically instead of statically.
 // src_inline (nullable): the n source ids by value in the launch parameters
 // (n <= kInlineIds); src.ids is then ignored.
+// wait_prev: the launch waits at its start for the previous grid on the
+// stream (programmatic dependent launch); false only when the host knows it
+// touches no block the grids still running may touch (pool.cpp LaunchTrack).
 cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int j0, int nj,
                            long long len, int max_ctas, cudaStream_t stream, int variant,
-                           const Sched* sched = nullptr, const InlineIds* src_inline = nullptr);
+                           const Sched* sched = nullptr, const InlineIds* src_inline = nullptr,
+                           bool wait_prev = true);
 
 
 // Lowest-first allocation of n blocks from a bitmap (bit = 1: free), after

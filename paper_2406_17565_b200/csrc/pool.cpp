@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 
@@ -82,6 +83,53 @@ mp_status src_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d, mpk::Inl
   return upload_ids(p, ids, d);
 }
 
+// ------------------------------------------------- shared data streams
+// The pools of one process on one device share their data stream (see
+// mp_pool_create): reference-counted, created with the first pool of the
+// device and destroyed with the last one (so a cudaDeviceReset after all
+// pools are gone leaves no stale handle behind).
+namespace {
+std::mutex g_stream_mu;
+struct DevStream {
+  cudaStream_t s = nullptr;
+  int refs = 0;
+  LaunchTrack track;
+} g_dev_stream[kMaxDevStreams];
+std::atomic<uint32_t> g_track_gen{0};
+}  // namespace
+
+uint32_t new_track_gen() {
+  uint32_t g = g_track_gen.fetch_add(1, std::memory_order_relaxed) + 1;
+  if (g == 0) g = g_track_gen.fetch_add(1, std::memory_order_relaxed) + 1;  // 0 = never marked
+  return g;
+}
+
+cudaError_t shared_stream_acquire(int dev, cudaStream_t* out, LaunchTrack** track) {
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  DevStream& d = g_dev_stream[dev];
+  if (!d.s) {
+    const cudaError_t e = cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      d.s = nullptr;
+      return e;
+    }
+  }
+  ++d.refs;
+  *out = d.s;
+  *track = &d.track;
+  return cudaSuccess;
+}
+
+void shared_stream_release(int dev) {
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  DevStream& d = g_dev_stream[dev];
+  if (d.refs > 0 && --d.refs == 0 && d.s) {
+    cudaStreamSynchronize(d.s);
+    cudaStreamDestroy(d.s);
+    d.s = nullptr;
+  }
+}
+
 // ------------------------------------------------------- sync / ordering
 // Frees of HBM blocks reach the device bitmap lazily, on the meta stream:
 // small sets by value in a kernel's parameters (folded into the next
@@ -146,6 +194,7 @@ mp_status drain(mp_pool* p) {
   TRY(remote_apply_waits(p));  // blocks stored by other processes have landed too
   CK(cudaStreamSynchronize(p->meta));
   CK(cudaStreamSynchronize(p->stream));
+  track_fence(p->track);  // idle: the window is empty (the next launch opens one)
   TRY(harvest_timed(p));
   p->last_timed_pair = -1;  // no gap across a sync
   if (!p->pending_verify.empty()) {
@@ -291,9 +340,10 @@ mp_status flush_batch(mp_pool* dst) {
       CK(cudaMemcpyAsync(dst->bsrc, b.sids.data(), (size_t)n * sizeof(int32_t),
                          cudaMemcpyHostToDevice, dst->meta));
     }
+    const LaunchBlocks lb{&src->bmarks, b.sids.data(), &dst->bmarks, b.dids.data(), n};
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, inl ? nullptr : dst->bsrc),
                              pool_ep(dst->d_slabs, dinl ? nullptr : dst->bdst), n, b.j0, b.nj,
-                             false, 0, inl ? &sinl : nullptr, /*meta_dep=*/!dinl));
+                             false, 0, inl ? &sinl : nullptr, /*meta_dep=*/!dinl, &lb));
     if (!inl || !dinl) {  // the launch reads this batch's id tables: guard their reuse
       CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
       dst->btab_used[b.tab] = true;
@@ -449,9 +499,43 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester) {
 }
 
 // ------------------------------------------------------------ migration
+// Whether the next launch on p's data stream must wait for the grids before
+// it (see LaunchTrack), and its blocks joined to the window.
+static bool window_admit(LaunchTrack* t, const LaunchBlocks* lb) {
+  static const bool overlap = [] {  // MP_PDL_OVERLAP=0: every launch waits (comparison)
+    const char* e = getenv("MP_PDL_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  constexpr int kMaxWindow = 8;  // bounds how many grids may overlap
+  bool wait = !overlap || !lb || t->unknown || t->launches >= kMaxWindow || t->gen == 0;
+  if (!wait) {
+    const uint32_t g = t->gen;
+    for (int64_t i = 0; i < lb->n && !wait; ++i) wait = lb->rm->w[(size_t)lb->sids[i]] == g;
+    for (int64_t i = 0; i < lb->n && !wait; ++i) {
+      const size_t d = (size_t)lb->dids[i];
+      wait = lb->wm->w[d] == g || lb->wm->r[d] == g;
+    }
+  }
+  if (wait) {  // a new window starts with this launch
+    t->gen = new_track_gen();
+    t->launches = 0;
+    t->unknown = false;
+  }
+  if (lb) {
+    const uint32_t g = t->gen;
+    for (int64_t i = 0; i < lb->n; ++i) lb->rm->r[(size_t)lb->sids[i]] = g;
+    for (int64_t i = 0; i < lb->n; ++i) lb->wm->w[(size_t)lb->dids[i]] = g;
+  } else {
+    t->unknown = true;
+  }
+  ++t->launches;
+  return wait;
+}
+
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a0,
                                const mpk::Endpoint& b0, int64_t n, int j0, int nj, bool peer,
-                               int64_t len, const mpk::InlineIds* src_inline, bool meta_dep) {
+                               int64_t len, const mpk::InlineIds* src_inline, bool meta_dep,
+                               const LaunchBlocks* blocks) {
   if (n <= 0) return MP_OK;
   if (len <= 0) len = p->chunk;
   mpk::Endpoint a = a0, b = b0;
@@ -507,9 +591,14 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   // (profiles/sched_r01.txt), and an NVLink-bound copy gains nothing from
   // rebalancing SMs
   const mpk::Sched sched{p->d_sched, &p->sched_base};
+  // only launches on the data stream join its window; a timed launch is
+  // bracketed by events (stream operations between kernels), so it waits
+  const bool wait = s != p->stream || timed || window_admit(p->track, blocks);
+  if (timed && s == p->stream) track_fence(p->track);
   CK(mpk::launch_migrate(a, b, (int)n, j0, nj, len, p->max_ctas, s, variant,
                          (s == p->stream && (!peer || peer_dyn)) ? &sched : nullptr,
-                         src_inline));
+                         src_inline, wait));
+  if (!wait) p->stats.overlapped_launches += 1;
   if (timed) {
     CK(cudaEventRecord(p->tev[2 * (size_t)pair + 1], s));
     p->timed.push_back({pair, bytes});
@@ -592,6 +681,7 @@ void mp_pool_destroy(mp_pool* p) {
       if (e) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
     if (p->stream && !p->shared_stream) cudaStreamDestroy(p->stream);
+    if (p->stream && p->shared_stream) shared_stream_release(p->dev);
     if (p->meta) cudaStreamDestroy(p->meta);
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   }
@@ -681,15 +771,12 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
       const char* e = getenv("MP_SHARED_STREAM");
       return !(e && e[0] == '0');
     }();
-    static std::mutex mu;
-    static cudaStream_t dev_stream[64] = {};
-    if (shared && p->dev < 64) {
-      std::lock_guard<std::mutex> lk(mu);
-      if (!dev_stream[p->dev]) CKC(cudaStreamCreateWithFlags(&dev_stream[p->dev], cudaStreamNonBlocking));
-      p->stream = dev_stream[p->dev];
+    if (shared && p->dev < kMaxDevStreams) {
+      CKC(shared_stream_acquire(p->dev, &p->stream, &p->track));
       p->shared_stream = true;
     } else {
       CKC(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      p->track = &p->own_track;
     }
   }
   CKC(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
@@ -726,6 +813,7 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
     for (int j = 0; j < p->nch; ++j)
       p->slabs[(size_t)j] = (char*)p->own_slab_region + (size_t)j * p->n_hbm * chunk;
   }
+  p->bmarks.reset((size_t)p->n_hbm);
   CKC(cudaMalloc(&p->d_slabs, sizeof(char*) * p->nch));
   CKC(cudaMemcpy(p->d_slabs, p->slabs.data(), sizeof(char*) * p->nch, cudaMemcpyHostToDevice));
   p->nwords = (int)((p->n_hbm + 31) / 32);

@@ -103,6 +103,45 @@ struct DstPrep {
   std::vector<uint8_t> priv;
 };
 
+// ---- overlap of independent migration launches (programmatic dependent
+// launch without the start wait; kernels.cu pdl_wait).  The "window" of a
+// data stream is the set of migration grids that may still run when the next
+// launch's CTAs start: every launch since the last one that waited at its
+// start (that one included -- it may itself still run).  A launch may skip
+// its start wait iff it reads no block a window grid writes and writes no
+// block a window grid reads or writes; otherwise it waits and opens a new
+// window.  A launch whose blocks the host does not know (staging, DRAM,
+// caller buffers) always waits and makes the next launch wait too.
+// Marks hold the generation of the window that last touched a block;
+// generations are unique across all streams, so a stale mark never matches.
+struct BlockMarks {
+  std::vector<uint32_t> r, w;  // per block: window generation of its last read / write
+  void reset(size_t n) {
+    r.assign(n, 0u);
+    w.assign(n, 0u);
+  }
+};
+struct LaunchTrack {
+  uint32_t gen = 0;
+  bool unknown = true;  // the window holds a launch with unknown blocks
+  int launches = 0;
+};
+// The blocks of one pool -> pool launch (host copies of its id lists).
+struct LaunchBlocks {
+  BlockMarks* rm;       // source pool's marks
+  const int32_t* sids;
+  BlockMarks* wm;       // destination pool's marks (a peer's, for remote stores)
+  const int32_t* dids;
+  int64_t n;
+};
+uint32_t new_track_gen();
+// The stream is idle (synchronised) or something outside the window's
+// knowledge was enqueued on it: the next launch waits.
+inline void track_fence(LaunchTrack* t) {
+  t->unknown = true;
+  t->launches = 0;
+}
+
 struct Channel;  // shared-memory mailbox (remote.cpp)
 
 // A pool living in another process (one process per GPU), imported with
@@ -121,6 +160,7 @@ struct RemotePeer {
   Channel* in = nullptr;          // peer -> me requests
   bool has_pending = false;       // peer's transfer between prepare and commit
   DstPrep pending;
+  BlockMarks bmarks;              // the peer's HBM blocks in my launch window
   // the peer has stored into this pool since this pool's data stream last
   // waited for the peer's event: the wait is applied lazily, before this
   // pool's next data-stream work (remote_apply_waits), so consecutive inbound
@@ -163,6 +203,9 @@ struct mp_pool {
   // of the data stream, which run after every earlier reader of it.
   cudaStream_t stream = nullptr, meta = nullptr, copy_stream = nullptr;
   bool shared_stream = false;  // stream is the device's shared data stream (not owned)
+  mp::LaunchTrack* track = nullptr;  // launch window of `stream` (shared with it)
+  mp::LaunchTrack own_track;
+  mp::BlockMarks bmarks;             // this pool's HBM blocks in launch windows
   cudaEvent_t ev_order = nullptr, ev_meta = nullptr;
   std::vector<cudaEvent_t> slot_ev;
   // swap through device staging, double-buffered: [0,1] the halves' fill done
@@ -242,6 +285,9 @@ struct mp_pool {
 namespace mp {
 
 constexpr int kTimedPairs = 512;
+constexpr int kMaxDevStreams = 64;
+cudaError_t shared_stream_acquire(int dev, cudaStream_t* out, LaunchTrack** track);
+void shared_stream_release(int dev);
 
 int* arena_take(mp_pool* p, int64_t n, int** host);
 mp_status upload_ids(mp_pool* p, const std::vector<int32_t>& ids, int** d_out);
@@ -271,11 +317,13 @@ std::vector<int32_t> alloc_dram(mp_pool* p, int64_t n, int32_t requester);
 // the copy engine choice then stays on the vector path.
 // len: bytes copied per chunk (0: the whole chunk, p->chunk); an endpoint
 // with cstride == 0 uses p->chunk as its chunk stride.
+// blocks (nullable): the launch's pool -> pool blocks, so it may overlap the
+// previous grids of the stream (LaunchTrack); nullptr: it waits for them.
 mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& a,
                                const mpk::Endpoint& b, int64_t n, int j0, int nj,
                                bool peer = false, int64_t len = 0,
                                const mpk::InlineIds* src_inline = nullptr,
-                               bool meta_dep = true);
+                               bool meta_dep = true, const LaunchBlocks* blocks = nullptr);
 
 // Launch coalescing (same-device fused transfers).
 mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
@@ -313,6 +361,14 @@ mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, 
 // (3) insertion + completion: insert (twi), unpin, final addrs, `private`
 // delivery.  final_out: st.ceil_b entries (twi) or st.nm entries (transfer).
 mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out);
+// The transmission failed after (1): release what the allocation step took
+// (the pinned matched prefix, the fresh blocks unless caller-given), so the
+// failed call leaves no state change behind.
+void dst_abort(mp_pool* dst, DstPrep& st);
+// What the transmission step could reject (unknown path, a STAGED slot that
+// cannot hold one block), checked before the receiver changes any state.
+mp_status transmit_precheck(mp_pool* src, mp_pool* dst, uint32_t path, int nj,
+                            const std::vector<uint8_t>& smeds);
 
 // remote.cpp
 uint64_t new_uid();

@@ -202,11 +202,18 @@ static PyObject* py_transfer(PyObject* self, PyObject* args) {
       Py_DECREF(out);
       return NULL;
     }
-    const npy_intp nd = PyArray_SIZE(da) < n ? PyArray_SIZE(da) : n;
-    memset(PyArray_DATA(out), 0, (size_t)n * sizeof(mp_addr));
-    memcpy(PyArray_DATA(out), PyArray_DATA(da), (size_t)nd * sizeof(mp_addr));
+    /* a given list must name exactly one destination per source block */
+    if (PyArray_SIZE(da) != n) {
+      Py_DECREF(da);
+      Py_DECREF(sa);
+      Py_DECREF(out);
+      return raise_status(MP_ERR_ADDR_COUNT, "transfer");
+    }
+    memcpy(PyArray_DATA(out), PyArray_DATA(da), (size_t)n * sizeof(mp_addr));
     Py_DECREF(da);
     flags |= MP_XFER_DST_GIVEN;
+  } else {
+    flags &= ~MP_XFER_DST_GIVEN; /* no list given: the receiver allocates */
   }
   Py_buffer pv;
   if (get_priv(priv, &pv) < 0) {
@@ -252,8 +259,16 @@ static PyObject* py_transfer_with_insert(PyObject* self, PyObject* args) {
       Py_DECREF(sa);
       return NULL;
     }
+    if (PyArray_SIZE(da) != PyArray_SIZE(sa)) { /* one given destination per source block */
+      Py_DECREF(ta);
+      Py_DECREF(sa);
+      Py_DECREF(da);
+      return raise_status(MP_ERR_ADDR_COUNT, "transfer_with_insert");
+    }
     if (PyArray_SIZE(da) > cap) cap = PyArray_SIZE(da);
     flags |= MP_XFER_DST_GIVEN;
+  } else {
+    flags &= ~MP_XFER_DST_GIVEN; /* no list given: the receiver allocates */
   }
   PyArrayObject* out = new_u64(cap);
   if (!out) {

@@ -285,9 +285,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       r->has_pending = false;
       if (sender_status != MP_OK) {  // the transmission failed on the sender:
         // release what the allocation step took (pins, fresh blocks)
-        unpin_nodes(p, r->pending.matched);
-        if (!(r->pending.flags & MP_XFER_DST_GIVEN))
-          for (int32_t id : r->pending.dids) free_block(p, MP_HBM, id);
+        dst_abort(p, r->pending);
         rstatus = sender_status;
         break;
       }
@@ -476,9 +474,12 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
       if (xs == MP_OK)
         // a receiver process on this same GPU: its IPC-mapped pool is local
         // HBM, so the copy takes the loopback engine (bulk ring, claiming)
+      {
+        const LaunchBlocks lb{&src->bmarks, hs.data(), &r->bmarks, hd.data(), (int64_t)hs.size()};
         xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
                                   pool_ep(r->d_slabs, d_d), (int64_t)hs.size(), j0, nj,
-                                  /*peer=*/!r->same_device, 0, si.n ? &si : nullptr);
+                                  /*peer=*/!r->same_device, 0, si.n ? &si : nullptr, true, &lb);
+      }
     }
     if (xs == MP_OK && !ds_.empty()) {
       int *d_s = nullptr, *d_d = nullptr;
@@ -691,6 +692,7 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
   char mine[32] = {0};
   cudaDeviceGetPCIBusId(mine, sizeof(mine), p->dev);
   r->same_device = std::strncmp(mine, h->bus_id, sizeof(mine)) == 0;
+  r->bmarks.reset((size_t)h->n_hbm);
   bool ok = true;
   for (int k = 0; k < h->n_allocs && ok; ++k) {
     void* m = nullptr;

@@ -101,6 +101,7 @@ class Stats(C.Structure):
         ("timed_launches", C.c_uint64), ("timed_bytes", C.c_uint64),
         ("aux_launches", C.c_uint64), ("gap_ms", C.c_double),
         ("profiled_launches", C.c_uint64), ("profiled_bytes", C.c_uint64),
+        ("overlapped_launches", C.c_uint64),
     ]
 
 

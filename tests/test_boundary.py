@@ -106,8 +106,22 @@ def test_fast_binding_converts_inputs():
                 F.insert(0, toks, a, 0)
             assert e.value.name == "CONFIG"
     with pytest.raises(M.MempoolError) as e:
-        F.transfer_with_insert(0, 1, strided, addrs.T, [5, 6], 0, bytearray(b"pv"), 16)
+        F.transfer_with_insert(0, 1, strided, addrs.T, list(range(5, 17)), 0,
+                               bytearray(b"pv"), 16)
     assert e.value.name == "CONFIG"
+    # a given destination list names exactly one block per source block
+    # (ADDR_COUNT, before the handle is looked at); no list: DST_GIVEN is
+    # cleared, not read from an uninitialised buffer
+    with pytest.raises(M.MempoolError) as e:
+        F.transfer_with_insert(0, 1, strided, addrs.T, [5, 6], 0, None, 16)
+    assert e.value.name == "ADDR_COUNT"
+    with pytest.raises(M.MempoolError) as e:
+        F.transfer(0, 1, [1, 2, 3], [7], 0, 0, 1, None)
+    assert e.value.name == "ADDR_COUNT"
+    for d in (None,):
+        with pytest.raises(M.MempoolError) as e:
+            F.transfer(0, 1, [1, 2, 3], d, M.XFER_DST_GIVEN, 0, 1, None)
+        assert e.value.name == "CONFIG"
 
 
 def test_nccl_arm_exports_every_declared_symbol():
