@@ -126,7 +126,7 @@ typedef struct {
    * bytes, caller-owned; NULL: the library cudaHostAllocs it. */
   void* dram_base;
   int64_t staging_bytes; /* device staging for the STAGED path (0: 256 MiB) */
-  int32_t staging_slots; /* ring depth (0: 4) */
+  int32_t staging_slots; /* ring depth (0: 4, at most 64) */
   int32_t max_ctas;      /* cap on migration kernel CTAs (0: auto = one full wave) */
   int32_t copy_kernel;   /* copy engine: 0 auto (bulk cp.async ring within this GPU's HBM,
                             vector LD/ST for pinned DRAM and peer memory), 1 vector, 2 bulk */
@@ -134,6 +134,15 @@ typedef struct {
                             one launch per batch, flushed when the data stream is idle, at
                             this many MiB, or when anything else touches either pool;
                             0: 1024 MiB, < 0: off (one launch per transfer) */
+  int32_t peer_engine;   /* copy engine of stores into a peer's memory (another GPU over
+                            NVLink, or another process's IPC-mapped pool): 0 auto (vector
+                            LD/ST, or MP_PEER_ENGINE=bulk), 1 vector, 2 bulk cp.async ring */
+  int32_t peer_sched;    /* work split of those stores: 0 auto (static, or
+                            MP_PEER_SCHED=dynamic), 1 static, 2 dynamic unit claiming */
+  int32_t force_peer;    /* test knob: treat a peer on the same GPU (in-process pool or
+                            IPC-imported process) as one on another GPU, so the peer
+                            dispatch (peer_engine / peer_sched, one-sided stores from the
+                            sender's stream) runs -- and is parity-tested -- on one GPU */
 } mp_pool_config;
 
 typedef struct {

@@ -75,6 +75,7 @@ mp_status mp_swap_out(mp_pool* p, int64_t n, uint32_t flags, mp_addr* out_old, m
     const int halves = per >= 2 ? 2 : 1;
     const int64_t k = per / halves;
     TRY(meta_fence(p));
+    TRY(staging_acquire(p, p->stream));  // STAGED transfers may still use the staging
     for (size_t b0 = 0, r = 0; b0 < hs.size(); b0 += (size_t)k, ++r) {
       const size_t nb = std::min(hs.size() - b0, (size_t)k);
       const int h = (int)(r % (size_t)halves);
@@ -150,6 +151,7 @@ mp_status mp_swap_in(mp_pool* p, const mp_addr* a, int64_t n, uint32_t flags, mp
     const int halves = per >= 2 ? 2 : 1;
     const int64_t k = per / halves;
     TRY(meta_fence(p));   // the allocation above (dh) is on the meta stream
+    TRY(staging_acquire(p, p->copy_stream));  // STAGED transfers may still use the staging
     CK(cudaEventRecord(p->swap_ev[0], p->stream));         // everything earlier on
     CK(cudaStreamWaitEvent(p->copy_stream, p->swap_ev[0], 0));  // the pool goes first
     for (int64_t b0 = 0, r = 0; b0 < n; b0 += k, ++r) {

@@ -134,17 +134,6 @@ RemotePeer* remote_of(mp_pool* src, int32_t inst) {
 // dst's device) or nullptr.  Enqueued after all earlier work of both pools and
 // before their later work; STAGED completes before returning, the others are
 // stream-ordered.
-// Both id lists by value in the launch parameters when they fit (the host
-// shadow's dids equal what the allocation kernel wrote on the device).
-bool pair_inline(const std::vector<int32_t>& sids, const std::vector<int32_t>& dids,
-                 mpk::InlineIds* si) {
-  const size_t n = sids.size();
-  if (n == 0 || dids.size() != n || 2 * n > (size_t)mpk::kInlineIds) return false;
-  si->n = si->nd = (int)n;
-  std::memcpy(si->ids, sids.data(), n * sizeof(int32_t));
-  std::memcpy(si->ids + n, dids.data(), n * sizeof(int32_t));
-  return true;
-}
 
 mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
                        const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj,
@@ -152,7 +141,7 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
   const int64_t n = (int64_t)sids.size();
   if (n == 0) return MP_OK;
   if (path == MP_XFER_PATH_AUTO) path = MP_XFER_PATH_FUSED;
-  const bool same_dev = src->dev == dst->dev;
+  const bool same_dev = same_gpu(src, dst);
   if (path == MP_XFER_PATH_FUSED && same_dev && dst->coalesce) {
     DevGuard g(dst->dev);
     return batch_append(src, dst, sids, dids, d_dst, j0, nj);
@@ -256,6 +245,17 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
         TRY(upload_ids(dst, dids, &dd));
       }
     }
+    // Stream-ordered, no host wait: the pack of slot r on the source's data
+    // stream, the copy-engine copy on its copy stream, the unpack on the
+    // destination's data stream, chained by events; a slot is refilled once
+    // the copy out of it (source side) and the unpack out of it
+    // (destination side) are done, and every earlier user of either staging
+    // buffer (other transfers, swap) goes first (staging_acquire).
+    {
+      DevGuard g(src->dev);
+      TRY(staging_acquire(src, src->stream));
+      TRY(staging_acquire(dst, src->copy_stream));
+    }
     const int64_t nslots = (n + k - 1) / k;
     for (int64_t s = 0; s < nslots; ++s) {
       const int r = (int)(s % S);
@@ -264,11 +264,12 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
       char* dslot = dst->staging + r * slot_bytes;
       {
         DevGuard g(src->dev);
-        if (s >= S) CK(cudaStreamWaitEvent(src->stream, dst->slot_ev[(size_t)r], 0));
+        if (s >= S) CK(cudaStreamWaitEvent(src->stream, src->slot_ev[(size_t)r], 0));
         TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, ds + b0),
                                  agg_ep(sslot, per_block, nullptr), nb, j0, nj));
-        CK(cudaEventRecord(src->slot_ev[(size_t)r], src->stream));
-        CK(cudaStreamWaitEvent(src->copy_stream, src->slot_ev[(size_t)r], 0));
+        CK(cudaEventRecord(src->pack_ev[(size_t)r], src->stream));
+        CK(cudaStreamWaitEvent(src->copy_stream, src->pack_ev[(size_t)r], 0));
+        if (s >= S) CK(cudaStreamWaitEvent(src->copy_stream, dst->slot_ev[(size_t)r], 0));
         CK(cudaMemcpyAsync(dslot, sslot, (size_t)(nb * per_block), cudaMemcpyDefault,
                            src->copy_stream));
         CK(cudaEventRecord(src->slot_ev[(size_t)r], src->copy_stream));
@@ -280,14 +281,6 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
                                  pool_ep(dst->d_slabs, dd + b0), nb, j0, nj));
         CK(cudaEventRecord(dst->slot_ev[(size_t)r], dst->stream));
       }
-    }
-    {
-      DevGuard g(dst->dev);
-      TRY(sync(dst));
-    }
-    {
-      DevGuard g(src->dev);
-      TRY(sync(src));
     }
     src->stats.blocks_moved += (uint64_t)n;
     return MP_OK;
@@ -310,7 +303,7 @@ mp_status transmit_dram(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& 
   TRY(flush_involving(dst));
   // aggregated block layout [2L][c]: shift the base to chunk j0
   char* base = src->dram_dev + (int64_t)j0 * src->chunk;
-  const bool same_dev = src->dev == dst->dev;
+  const bool same_dev = same_gpu(src, dst);
   mp_pool* ex = same_dev ? dst : src;
   if (same_dev)
     TRY(link(src, dst));
@@ -359,7 +352,7 @@ mp_status transmit(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
 void hint_slot(mp_pool* src, mp_pool* dst, uint32_t flags, const std::vector<uint8_t>& smeds,
                int j0, int nj) {
   const uint32_t path = flags & MP_XFER_PATH_MASK;
-  if (!(path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED) || src->dev != dst->dev ||
+  if (!(path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED) || !same_gpu(src, dst) ||
       !dst->coalesce || (flags & MP_XFER_DST_GIVEN))
     return;
   for (uint8_t m : smeds)
@@ -410,8 +403,6 @@ mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t f
     DevGuard g(dst->dev);
     if (dst->nfree[MP_HBM] < n) evict_internal(dst, n - dst->nfree[MP_HBM], MP_HBM, nullptr);
     TRY(alloc_hbm(dst, n, src_inst, &st->dids, &st->d_dst));
-    if (st->d_dst && st->d_dst >= dst->ar.d && st->d_dst < dst->ar.d + dst->ar.cap)
-      st->d_dst_off = st->d_dst - dst->ar.d;
   }
   return MP_OK;
 }
@@ -460,8 +451,6 @@ mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, 
     if (dst->nfree[MP_HBM] < st->nm)
       evict_internal(dst, st->nm - dst->nfree[MP_HBM], MP_HBM, nullptr);
     TRY(alloc_hbm(dst, st->nm, src_inst, &st->dids, &st->d_dst));
-    if (st->d_dst && st->d_dst >= dst->ar.d && st->d_dst < dst->ar.d + dst->ar.cap)
-      st->d_dst_off = st->d_dst - dst->ar.d;
   }
   return MP_OK;
 }
@@ -657,7 +646,7 @@ mp_status mp_transfer_heads(mp_pool* src, int32_t dst_inst, const mp_addr* sa, i
   if (n == 0) return MP_OK;
   TRY(flush_involving(src));
   TRY(flush_involving(dst));
-  const bool same_dev = src->dev == dst->dev;
+  const bool same_dev = same_gpu(src, dst);
   mp_pool* ex = same_dev ? dst : src;
   char** dslabs = dst->d_slabs;
   if (!same_dev) {

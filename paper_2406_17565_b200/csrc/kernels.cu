@@ -560,9 +560,11 @@ cudaError_t launch_migrate(const Endpoint& src, const Endpoint& dst, int n, int 
                            const Sched* sched, const InlineIds* src_inline, bool wait_prev) {
   if (n <= 0 || nj <= 0) return cudaSuccess;
   static const InlineIds no_ids{};
-  if (src_inline && (src_inline->n != n || (src_inline->nd && (src_inline->nd != n ||
-                                                                2 * n > kInlineIds))))
-    return cudaErrorInvalidValue;
+  if (src_inline) {  // source ids, destination ids, or both (ids[0, n) then ids[n', n'+n))
+    const int ns = src_inline->n, nd = src_inline->nd;
+    if (!((ns == 0 || ns == n) && (nd == 0 || nd == n) && (ns || nd) && ns + nd <= kInlineIds))
+      return cudaErrorInvalidValue;
+  }
   const InlineIds& si = src_inline ? *src_inline : no_ids;
   if (variant == kCopyBulk) {
     switch (bulk_cfg((unsigned long long)n * (unsigned long long)nj * (unsigned long long)chunk)) {

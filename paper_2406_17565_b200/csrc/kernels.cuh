@@ -28,8 +28,9 @@ struct Endpoint {
 
 // Up to kInlineIds block ids passed by value in the kernel parameters (no
 // host-to-device copy call: 3.7 us of host time each on B200).
-// A migration launch may also carry its n destination ids, at ids[n, 2n)
-// (nd == n; needs 2n <= kInlineIds), so it reads no id table at all.
+// A migration launch may also carry its n destination ids, at ids[n', n'+n)
+// where n' = this->n (nd == n; n' + n <= kInlineIds), so it reads no id
+// table at all; n == 0 with nd == n: destination ids only.
 constexpr int kInlineIds = 1000;
 struct InlineIds {
   int n = 0;

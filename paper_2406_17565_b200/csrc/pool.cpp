@@ -18,35 +18,15 @@ void set_err(const std::string& s) { g_err = s; }
 const std::string& get_err() { return g_err; }
 
 // ----------------------------------------------------------------- arena
-// Arena ranges a peer process may still read: the device-allocated block
-// table of a remote transfer between its allocation reply and its completion
-// (the sender's copy reads it over IPC; a drain here cannot wait for it).
-static int64_t skip_live(const mp_pool* p, int64_t start, int64_t n) {
-  for (bool moved = true; moved;) {
-    moved = false;
-    for (const auto& kv : p->remotes) {
-      const RemotePeer* r = kv.second;
-      if (!r->has_pending || r->pending.d_dst_off < 0) continue;
-      const int64_t o = r->pending.d_dst_off, e = o + std::max<int64_t>(r->pending.nm, 1);
-      if (start < e && o < start + n) {
-        start = e;
-        moved = true;
-      }
-    }
-  }
-  return start;
-}
-
 int* arena_take(mp_pool* p, int64_t n, int** host) {
   n = std::max<int64_t>(n, 1);
   if (n > p->ar.cap) return nullptr;
-  int64_t at = p->remotes.empty() ? p->ar.used : skip_live(p, p->ar.used, n);
+  int64_t at = p->ar.used;
   if (at + n > p->ar.cap) {
-    // wrap: everything this process issued (and every completed inbound
-    // copy) is done after the drain; in-flight remote ranges are skipped
+    // wrap: everything this process issued is done after the drain (peers
+    // never read this arena: their copies take ids from their own side)
     if (drain(p) != MP_OK) return nullptr;
-    at = p->remotes.empty() ? 0 : skip_live(p, 0, n);
-    if (at + n > p->ar.cap) return nullptr;
+    at = 0;
   }
   p->ar.used = at;
   int* d = p->ar.d + p->ar.used;
@@ -130,6 +110,56 @@ void shared_stream_release(int dev) {
   }
 }
 
+// ------------------------------------------- stream memory operations
+namespace {
+typedef int (*StreamValue32Fn)(cudaStream_t, unsigned long long, uint32_t, unsigned);
+StreamValue32Fn driver_value_fn(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return (StreamValue32Fn)f;
+}
+}  // namespace
+
+mp_status stream_wait_geq(cudaStream_t s, const uint32_t* dptr, uint32_t v) {
+  static const StreamValue32Fn fn = driver_value_fn("cuStreamWaitValue32");
+  if (!fn) {
+    set_err("cuStreamWaitValue32 unavailable");
+    return MP_ERR_CUDA;
+  }
+  // flags 0 = CU_STREAM_WAIT_VALUE_GEQ: (int32_t)(*addr - value) >= 0
+  if (fn(s, (unsigned long long)(uintptr_t)dptr, v, 0) != 0) {
+    set_err("cuStreamWaitValue32 failed");
+    return MP_ERR_CUDA;
+  }
+  return MP_OK;
+}
+
+mp_status stream_write_u32(cudaStream_t s, uint32_t* dptr, uint32_t v) {
+  static const StreamValue32Fn fn = driver_value_fn("cuStreamWriteValue32");
+  if (!fn) {
+    set_err("cuStreamWriteValue32 unavailable");
+    return MP_ERR_CUDA;
+  }
+  // flags 0 = CU_STREAM_WRITE_VALUE_DEFAULT: ordered after (and fenced
+  // behind) the stream's earlier work
+  if (fn(s, (unsigned long long)(uintptr_t)dptr, v, 0) != 0) {
+    set_err("cuStreamWriteValue32 failed");
+    return MP_ERR_CUDA;
+  }
+  return MP_OK;
+}
+
+mp_status staging_acquire(mp_pool* p, cudaStream_t s) {
+  // an event never recorded is complete, so every slot's event can be waited on
+  for (cudaEvent_t e : p->slot_ev) CK(cudaStreamWaitEvent(s, e, 0));
+  for (cudaEvent_t e : p->pack_ev) CK(cudaStreamWaitEvent(s, e, 0));
+  for (cudaEvent_t e : p->swap_ev) CK(cudaStreamWaitEvent(s, e, 0));
+  return MP_OK;
+}
+
 // ------------------------------------------------------- sync / ordering
 // Frees of HBM blocks reach the device bitmap lazily, on the meta stream:
 // small sets by value in a kernel's parameters (folded into the next
@@ -194,6 +224,7 @@ mp_status drain(mp_pool* p) {
   TRY(remote_apply_waits(p));  // blocks stored by other processes have landed too
   CK(cudaStreamSynchronize(p->meta));
   CK(cudaStreamSynchronize(p->stream));
+  CK(cudaStreamSynchronize(p->copy_stream));  // STAGED copy-engine copies issued by p
   track_fence(p->track);  // idle: the window is empty (the next launch opens one)
   TRY(harvest_timed(p));
   p->last_timed_pair = -1;  // no gap across a sync
@@ -567,29 +598,32 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
   }
   // Copy engine: auto = the bulk (TMA) ring for copies within this GPU's HBM
   // (measured ~1% ahead of the vector kernel, with a third of the issued
-  // instructions); mapped pinned DRAM (swap) and peer memory (NVLink / IPC)
-  // stay on the vector LD/ST path.
+  // instructions); mapped pinned DRAM (swap) stays on the vector LD/ST path;
+  // stores into peer memory (NVLink / IPC) take the pool's peer_engine.
   const bool host_side = (a.base && a.base == p->dram_dev) || (b.base && b.base == p->dram_dev);
   int variant = p->copy_kernel == mpk::kCopyAuto ? mpk::kCopyBulk : p->copy_kernel;
-  if (host_side || (peer && p->copy_kernel == mpk::kCopyAuto)) variant = mpk::kCopyVector;
-  // Knobs for the first multi-GPU box (untested on NVLink so far):
-  // MP_PEER_ENGINE=bulk stores into peer memory with the bulk (TMA) ring,
-  // MP_PEER_SCHED=dynamic lets peer copies claim units dynamically.
-  static const bool peer_bulk = [] {
+  // environment defaults of the auto peer choices (measurement knobs):
+  // MP_PEER_ENGINE=bulk, MP_PEER_SCHED=dynamic
+  static const int env_peer_engine = [] {
     const char* e = getenv("MP_PEER_ENGINE");
-    return e && e[0] == 'b';
+    return (e && e[0] == 'b') ? mpk::kCopyBulk : mpk::kCopyVector;
   }();
-  static const bool peer_dyn = [] {
+  static const bool env_peer_dyn = [] {
     const char* e = getenv("MP_PEER_SCHED");
     return e && e[0] == 'd';
   }();
-  if (peer && !host_side && peer_bulk && p->copy_kernel == mpk::kCopyAuto)
-    variant = mpk::kCopyBulk;
+  if (host_side) {
+    variant = mpk::kCopyVector;
+  } else if (peer) {
+    variant = p->peer_engine ? p->peer_engine
+                             : (p->copy_kernel ? p->copy_kernel : env_peer_engine);
+  }
   // dynamic unit claiming on the pool's data stream (launches serialised);
-  // stores into a peer's memory keep the static split: on the one-GPU
+  // stores into a peer's memory default to the static split: on the one-GPU
   // two-process run (IPC-mapped pool) it was 4% ahead of claiming
-  // (profiles/sched_r01.txt), and an NVLink-bound copy gains nothing from
+  // (profiles/sched_r01.txt), and an NVLink-bound copy gains less from
   // rebalancing SMs
+  const bool peer_dyn = p->peer_sched ? p->peer_sched == 2 : env_peer_dyn;
   const mpk::Sched sched{p->d_sched, &p->sched_base};
   // only launches on the data stream join its window; a timed launch is
   // bracketed by events (stream operations between kernels), so it waits
@@ -677,6 +711,7 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->ev_meta) cudaEventDestroy(p->ev_meta);
     if (p->ev_ipc) cudaEventDestroy(p->ev_ipc);
     for (auto e : p->slot_ev) cudaEventDestroy(e);
+    for (auto e : p->pack_ev) cudaEventDestroy(e);
     for (auto e : p->swap_ev)
       if (e) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
@@ -720,13 +755,18 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->n_dram = cfg->dram_blocks;
   p->max_ctas = cfg->max_ctas;
   p->copy_kernel = cfg->copy_kernel;
-  if (p->copy_kernel < 0 || p->copy_kernel > 2) {
-    set_err("copy_kernel must be 0 (auto), 1 (vector) or 2 (bulk)");
+  p->peer_engine = cfg->peer_engine;
+  p->peer_sched = cfg->peer_sched;
+  p->force_peer = cfg->force_peer != 0;
+  if (p->copy_kernel < 0 || p->copy_kernel > 2 || p->peer_engine < 0 || p->peer_engine > 2 ||
+      p->peer_sched < 0 || p->peer_sched > 2) {
+    set_err("copy_kernel / peer_engine must be 0 (auto), 1 (vector) or 2 (bulk); "
+            "peer_sched 0 (auto), 1 (static) or 2 (dynamic)");
     delete p->index;
     delete p;
     return MP_ERR_CONFIG;
   }
-  p->staging_slots = cfg->staging_slots > 0 ? cfg->staging_slots : 4;
+  p->staging_slots = std::min(cfg->staging_slots > 0 ? cfg->staging_slots : 4, kMaxSyncSlots);
   p->staging_bytes = cfg->staging_bytes > 0 ? cfg->staging_bytes : (256ll << 20);
   p->index = new mpi::Index(p->B, p->n_hbm, p->n_dram);
   for (int m = 0; m < 2; ++m) {
@@ -795,6 +835,8 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   p->uid = new_uid();
   p->slot_ev.resize((size_t)p->staging_slots);
   for (auto& e : p->slot_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  p->pack_ev.resize((size_t)p->staging_slots);
+  for (auto& e : p->pack_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : p->swap_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   p->tev.resize(2 * (size_t)kTimedPairs);
   for (auto& e : p->tev) CKC(cudaEventCreate(&e));

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
 #include <deque>
 #include <map>
 #include <set>
@@ -99,7 +100,6 @@ struct DstPrep {
   std::vector<mpi::Node*> matched;  // pinned receiver prefix (R3, R12)
   std::vector<int32_t> dids;        // receiver block ids of the moved blocks
   int* d_dst = nullptr;             // allocator output on the receiver's device
-  int64_t d_dst_off = -1;           // its offset in the receiver's id arena
   std::vector<uint8_t> priv;
 };
 
@@ -144,6 +144,31 @@ inline void track_fence(LaunchTrack* t) {
 
 struct Channel;  // shared-memory mailbox (remote.cpp)
 
+// A page of host shared memory, pinned and mapped for the GPUs, holding the
+// device-side flags of one ordered pair of pools (remote.cpp): GPU streams
+// write them with stream memory operations and wait on them with
+// cuStreamWaitValue32, so the two processes' streams synchronise without a
+// host round trip.  Layout (uint32 words): [0] done sequence of one-round-
+// trip (ASYNC) transfers, [kSyncReady + s] STAGED slot s filled, [kSyncFree
+// + s] slot s drained.
+constexpr int kMaxSyncSlots = 64;
+constexpr int kSyncDone = 0, kSyncReady = 16, kSyncFree = 16 + kMaxSyncSlots;
+struct SyncPage {
+  std::string name;
+  int fd = -1;
+  uint32_t* h = nullptr;  // host view
+  uint32_t* d = nullptr;  // device view
+  bool registered = false;
+};
+// Stream memory operations (driver API through the runtime's entry points):
+// s waits until (int32)(*dptr - v) >= 0; s writes v to *dptr after its
+// earlier work (with a memory fence).
+mp_status stream_wait_geq(cudaStream_t s, const uint32_t* dptr, uint32_t v);
+mp_status stream_write_u32(cudaStream_t s, uint32_t* dptr, uint32_t v);
+// Make `s` wait for every earlier user of p's staging buffer (STAGED slots,
+// swap halves).
+mp_status staging_acquire(mp_pool* p, cudaStream_t s);
+
 // A pool living in another process (one process per GPU), imported with
 // mp_import_peer: its slabs and id arena are CUDA-IPC mapped into this
 // process, its interprocess event orders the two processes' streams, and two
@@ -154,13 +179,37 @@ struct RemotePeer {
   bool same_device = false;
   std::vector<void*> mapped;      // IPC-opened allocation bases
   char** d_slabs = nullptr;       // the peer's slab pointers, valid on my device
-  int* arena = nullptr;           // the peer's id arena (device), mapped
   cudaEvent_t ev = nullptr;       // the peer's interprocess event
   Channel* out = nullptr;         // me -> peer requests
   Channel* in = nullptr;          // peer -> me requests
   bool has_pending = false;       // peer's transfer between prepare and commit
   DstPrep pending;
   BlockMarks bmarks;              // the peer's HBM blocks in my launch window
+  std::vector<char*> slabs_h;     // the peer's slab pointers, valid here (copy-engine paths)
+  int64_t staging_bytes = 0;      // the peer's staging configuration (STAGED ring geometry)
+  int32_t staging_slots = 0;
+  // device-side synchronisation with the peer (host shared memory, mapped)
+  SyncPage* out_sync = nullptr;   // my transfers to the peer
+  SyncPage* in_sync = nullptr;    // the peer's transfers to me
+  // STAGED transport: the receiver keeps one inbound ring per sending peer
+  // (device memory, IPC-exported in its first allocation reply); the sender
+  // packs a slot, copies it into the peer's ring with the copy engine and
+  // raises the slot's ready flag; the receiver's recv_stream waits for the
+  // flag, unpacks into the fresh blocks and raises the slot's free flag.
+  char* ring = nullptr;           // receiver side: my inbound ring for this peer
+  int64_t ring_bytes = 0;
+  uint64_t ring_id = 0;
+  char* peer_ring = nullptr;      // sender side: the peer's inbound ring for me
+  uint64_t peer_ring_id = 0;
+  uint32_t out_slot = 0, in_slot = 0;  // slot sequence numbers per direction
+  cudaStream_t recv_stream = nullptr;
+  cudaEvent_t recv_dep = nullptr, recv_ev = nullptr;
+  bool recv_join = false;         // recv_ev (the last staged inbound's unpacks) not yet joined
+  // one-round-trip ASYNC transfers from the peer (committed at allocation):
+  // their copies have landed once the done flag reaches seq; joined to my
+  // data stream lazily, oldest first: (prepare stamp, seq)
+  uint32_t in_seq = 0;
+  std::deque<std::pair<uint64_t, uint32_t>> async_in;
   // the peer has stored into this pool since this pool's data stream last
   // waited for the peer's event: the wait is applied lazily, before this
   // pool's next data-stream work (remote_apply_waits), so consecutive inbound
@@ -178,6 +227,9 @@ struct mp_pool {
   int nch = 0;
   int max_ctas = 0;
   int copy_kernel = 0;  // mpk::CopyVariant for device<->device copies
+  int peer_engine = 0;  // copy engine / split of stores into peer memory (mp_pool_config)
+  int peer_sched = 0;
+  bool force_peer = false;  // test knob: same-GPU peers take the peer dispatch
   // device memory
   std::vector<char*> slabs;
   void* own_slab_region = nullptr;
@@ -206,6 +258,15 @@ struct mp_pool {
   mp::LaunchTrack* track = nullptr;  // launch window of `stream` (shared with it)
   mp::LaunchTrack own_track;
   mp::BlockMarks bmarks;             // this pool's HBM blocks in launch windows
+  // cross-process ordering: every inbound one-round-trip transfer gets a
+  // prepare stamp; while this pool issues a transfer of its own it joins
+  // only inbound transfers prepared before that transfer started
+  // (join_bound), so waits always point at earlier-started transfers and no
+  // cycle of device waits can form between two processes sending to each
+  // other (remote.cpp)
+  uint64_t prep_stamp = 0;
+  uint64_t join_bound = ~0ull;
+  std::vector<cudaEvent_t> pack_ev;  // STAGED (cross-process): slot packed
   cudaEvent_t ev_order = nullptr, ev_meta = nullptr;
   std::vector<cudaEvent_t> slot_ev;
   // swap through device staging, double-buffered: [0,1] the halves' fill done
@@ -298,6 +359,10 @@ mp_status link(mp_pool* signal, mp_pool* waiter);  // waiter's stream waits for 
 mp_status meta_fence(mp_pool* p);                  // p->stream waits for p->meta
 
 bool decode(const mp_pool* p, mp_addr a, int* med, int32_t* idx);
+// Both pools on one GPU and neither asks for the peer dispatch (force_peer).
+inline bool same_gpu(const mp_pool* a, const mp_pool* b) {
+  return a->dev == b->dev && !a->force_peer && !b->force_peer;
+}
 inline mp_addr enc(const mp_pool* p, int med, int32_t idx) { return MP_ADDR(p->inst, med, idx); }
 
 void free_block(mp_pool* p, int med, int32_t idx);
@@ -324,6 +389,18 @@ mp_status launch_migrate_timed(mp_pool* p, cudaStream_t s, const mpk::Endpoint& 
                                bool peer = false, int64_t len = 0,
                                const mpk::InlineIds* src_inline = nullptr,
                                bool meta_dep = true, const LaunchBlocks* blocks = nullptr);
+
+// Both id lists by value in the launch parameters when they fit (the host
+// shadow's dids equal what the allocation kernel wrote on the device).
+inline bool pair_inline(const std::vector<int32_t>& sids, const std::vector<int32_t>& dids,
+                        mpk::InlineIds* si) {
+  const size_t n = sids.size();
+  if (n == 0 || dids.size() != n || 2 * n > (size_t)mpk::kInlineIds) return false;
+  si->n = si->nd = (int)n;
+  std::memcpy(si->ids, sids.data(), n * sizeof(int32_t));
+  std::memcpy(si->ids + n, dids.data(), n * sizeof(int32_t));
+  return true;
+}
 
 // Launch coalescing (same-device fused transfers).
 mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,

@@ -12,22 +12,37 @@
 //  * control messages travel through a POSIX shared-memory mailbox per ordered
 //    pair of pools (request slot + reply slot, sequence numbers with
 //    acquire/release ordering) -- both processes are on the same 8-GPU box;
-//  * the transmission is one-sided: the receiver's slabs and its id arena are
-//    CUDA-IPC mapped into the sender, whose fused gather->store kernel writes
-//    the scattered source chunks straight into the receiver's freshly
-//    allocated blocks over NVLink (or HBM when both processes share a GPU),
-//    reading the destination block table the receiver's device allocator
-//    wrote -- no staging, no per-block calls, no ordering thread (the paper's
-//    NCCL send/recv needs one per communicator);
-//  * the two processes' streams are ordered with interprocess CUDA events:
-//    the sender's copy waits for the receiver's allocation, the receiver's
-//    later work waits for the sender's copy.
+//  * the receiver's slabs are CUDA-IPC mapped into the sender, and the
+//    transmission is one-sided, on the sender's GPU, in one of four
+//    transports (remote_transmit): FUSED -- one gather -> peer-store kernel
+//    writing the scattered source chunks straight into the receiver's fresh
+//    blocks over NVLink (no staging, no per-block calls, no ordering thread;
+//    the paper's NCCL send/recv needs one per communicator); CE /
+//    CE_BATCH -- copy-engine memcpys per chunk; STAGED -- pack, one
+//    copy-engine copy per slot into the receiver's inbound ring, unpack by
+//    the receiver, pipelined by device-side flags;
+//  * the two processes' streams are ordered with interprocess CUDA events
+//    (the sender's copy waits for the receiver's allocation; the receiver's
+//    later work waits for a completed copy) and, where a wait must be
+//    enqueued before its producer, with flags in a pinned shared-memory page
+//    per ordered pair that GPU streams raise and wait on (SyncPage);
+//  * an MP_XFER_ASYNC transfer takes ONE round trip: the receiver allocates,
+//    inserts and delivers `private` when the request arrives (R15: host-side
+//    effects at call time) and joins the sender's copy through the pair's
+//    done flag before its next data-stream work; synchronous transfers keep
+//    the paper's two round trips (the sender completes once the receiver
+//    has the data and answered ok).
+//  Waits across processes never form a cycle: a pool issuing a transfer
+//  joins only inbound one-round-trip transfers prepared before its own
+//  transfer started (mp_pool::join_bound), so every device wait points at
+//  an earlier-started transfer or at an event already recorded.
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <time.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <random>
@@ -122,6 +137,83 @@ void chan_close(Channel* c, bool unlink) {
   delete c;
 }
 
+// Synchronisation page of one ordered pair (pool.hpp SyncPage): created by
+// whichever process opens it first (ftruncate zero-fills), pinned and mapped
+// for the GPU in both.
+constexpr size_t kSyncBytes = 4096;
+
+SyncPage* sync_open(const std::string& name) {
+  SyncPage* s = new SyncPage();
+  s->name = name;
+  s->fd = shm_open(name.c_str(), O_CREAT | O_RDWR, 0600);
+  if (s->fd < 0) {
+    set_err("shm_open(" + name + ") failed");
+    delete s;
+    return nullptr;
+  }
+  struct stat sb;
+  if (fstat(s->fd, &sb) != 0 || (size_t)sb.st_size < kSyncBytes) {
+    if (ftruncate(s->fd, (off_t)kSyncBytes) != 0) {
+      set_err("ftruncate(" + name + ") failed");
+      close(s->fd);
+      delete s;
+      return nullptr;
+    }
+  }
+  void* m = mmap(nullptr, kSyncBytes, PROT_READ | PROT_WRITE, MAP_SHARED, s->fd, 0);
+  if (m == MAP_FAILED) {
+    set_err("mmap(" + name + ") failed");
+    close(s->fd);
+    delete s;
+    return nullptr;
+  }
+  s->h = (uint32_t*)m;
+  void* d = nullptr;
+  if (cudaHostRegister(m, kSyncBytes, cudaHostRegisterMapped | cudaHostRegisterPortable) !=
+          cudaSuccess ||
+      cudaHostGetDevicePointer(&d, m, 0) != cudaSuccess) {
+    cudaGetLastError();
+    set_err("cudaHostRegister of the synchronisation page failed");
+    munmap(m, kSyncBytes);
+    close(s->fd);
+    delete s;
+    return nullptr;
+  }
+  s->registered = true;
+  s->d = (uint32_t*)d;
+  return s;
+}
+
+void sync_close(SyncPage* s) {
+  if (!s) return;
+  if (s->registered) cudaHostUnregister(s->h);
+  if (s->h) munmap(s->h, kSyncBytes);
+  if (s->fd >= 0) close(s->fd);
+  shm_unlink(s->name.c_str());  // both sides unlink; the second finds it gone
+  delete s;
+}
+
+// A flag the GPU may still be about to overwrite: set from the host (used
+// only after the writing stream has been drained, on failure paths, so a
+// waiting peer stream is released).
+void host_raise(uint32_t* h, uint32_t v) { __atomic_store_n(h, v, __ATOMIC_RELEASE); }
+
+// Slot geometry of the STAGED ring between two pools' staging buffers:
+// S slots of slot_bytes, k blocks (<= kInlineIds, their ids ride in the
+// unpack's launch parameters) of per_block bytes each.
+struct RingGeom {
+  int S = 0;
+  int64_t slot_bytes = 0, k = 0;
+};
+RingGeom ring_geom(int64_t a_bytes, int a_slots, int64_t b_bytes, int b_slots,
+                   int64_t per_block) {
+  RingGeom g;
+  g.S = std::max(1, std::min(std::min(a_slots, b_slots), kMaxSyncSlots));
+  g.slot_bytes = (std::min(a_bytes, b_bytes) / g.S) & ~(int64_t)255;
+  g.k = std::min<int64_t>(per_block > 0 ? g.slot_bytes / per_block : 0, mpk::kInlineIds);
+  return g;
+}
+
 // Little serializer for the message payloads.
 struct Writer {
   char* p;
@@ -214,6 +306,57 @@ void remote_report_timing() {
 // ---------------------------------------------------------- receiver side
 namespace {
 
+// Receiver half of a STAGED transfer, enqueued at its allocation step: the
+// moved blocks whose sources sit in the sender's HBM arrive through this
+// peer's inbound ring.  recv_stream waits for each slot's ready flag, unpacks
+// it into the fresh blocks (ids in the launch parameters) and raises the
+// slot's free flag -- all device-side, no host round trip per slot.  The
+// stream is separate from the data stream, so a data stream never blocks on
+// a flag a peer raises later.
+mp_status staged_recv(mp_pool* p, RemotePeer* r, const DstPrep& st, const uint8_t* meds, int j0,
+                      int nj) {
+  const int64_t per_block = (int64_t)nj * p->chunk;
+  const RingGeom g = ring_geom(r->staging_bytes, r->staging_slots, p->staging_bytes,
+                               p->staging_slots, per_block);
+  if (g.k < 1) {
+    set_err("staging slot smaller than one block");
+    return MP_ERR_CONFIG;
+  }
+  if (!r->ring) {  // first STAGED transfer from this peer: its inbound ring
+    r->ring_bytes = std::min(p->staging_bytes, r->staging_bytes);
+    CK(cudaMalloc(&r->ring, (size_t)r->ring_bytes));
+    r->ring_id = new_uid();
+    CK(cudaStreamCreateWithFlags(&r->recv_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&r->recv_dep, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&r->recv_ev, cudaEventDisableTiming));
+  }
+  std::vector<int32_t> ids;
+  for (int64_t i = 0; i < st.nm; ++i)
+    if (meds[st.skip + i] == MP_HBM) ids.push_back(st.dids[(size_t)i]);
+  if (ids.empty()) return MP_OK;
+  // after the allocation and every earlier data-stream use of the blocks
+  CK(cudaEventRecord(r->recv_dep, p->meta));
+  CK(cudaStreamWaitEvent(r->recv_stream, r->recv_dep, 0));
+  CK(cudaEventRecord(r->recv_dep, p->stream));
+  CK(cudaStreamWaitEvent(r->recv_stream, r->recv_dep, 0));
+  uint32_t q = r->in_slot;
+  for (size_t off = 0; off < ids.size(); off += (size_t)g.k, ++q) {
+    const int slot = (int)(q % (uint32_t)g.S);
+    const int64_t nb = std::min<int64_t>(g.k, (int64_t)(ids.size() - off));
+    TRY(stream_wait_geq(r->recv_stream, r->in_sync->d + kSyncReady + slot, q + 1));
+    mpk::InlineIds di;
+    di.n = 0;   // the source is the ring slot itself (block i at i * per_block)
+    di.nd = (int)nb;
+    std::memcpy(di.ids, ids.data() + off, (size_t)nb * sizeof(int32_t));
+    TRY(launch_migrate_timed(p, r->recv_stream,
+                             agg_ep(r->ring + (int64_t)slot * g.slot_bytes, per_block, nullptr),
+                             pool_ep(p->d_slabs, nullptr), nb, j0, nj, false, 0, &di));
+    TRY(stream_write_u32(r->recv_stream, r->in_sync->d + kSyncFree + slot, q + 1));
+  }
+  r->in_slot = q;
+  return MP_OK;
+}
+
 mp_status serve_message(mp_pool* p, RemotePeer* r) {
   Channel* c = r->in;
   SlotHdr* q = c->req();
@@ -241,6 +384,13 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       if (flags & MP_XFER_DST_GIVEN) given = (const mp_addr*)rd.bytes(m * (int64_t)sizeof(mp_addr));
       const int64_t plen = rd.get<int64_t>();
       const void* priv = rd.bytes(plen);
+      const int32_t j0 = rd.get<int32_t>(), nj = rd.get<int32_t>();
+      const uint8_t* meds = (const uint8_t*)rd.bytes(m);
+      const bool staged = (flags & MP_XFER_PATH_MASK) == MP_XFER_PATH_STAGED;
+      // one round trip: the receiver commits (insert, delivery) now and the
+      // sender's copy is joined through the pair's done flag (R15: an ASYNC
+      // transfer's host-side effects happen at call time)
+      const bool one_trip = (flags & MP_XFER_ASYNC) && !staged;
       mp_status s = flush_involving(p);
       if (s == MP_OK && !rd.ok) s = MP_ERR_CONFIG;
       if (s == MP_OK && r->has_pending) s = MP_ERR_PRECONDITION;
@@ -250,28 +400,53 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         s = dst_prepare_twi(p, r->inst, toks, n_tok, m, flags, given, priv, plen, &r->pending);
       else
         s = dst_prepare_xfer(p, r->inst, m, flags, given, priv, plen, &r->pending);
+      const uint32_t slot0 = r->in_slot;
       if (s == MP_OK) {
         r->has_pending = true;
         // the sender's copy must follow this allocation and every earlier use
         // of the blocks on this pool's streams, including other peers' copies
-        // into them (a block freed and re-allocated); its own earlier copies
-        // are ordered by its stream already
-        for (auto& kv2 : p->remotes) {
-          RemotePeer* o = kv2.second;
-          if (o == r || !o->inbound_pending) continue;
-          if (cudaStreamWaitEvent(p->stream, o->ev, 0) != cudaSuccess) s = MP_ERR_CUDA;
-          o->inbound_pending = false;
-        }
+        // into them (a block freed and re-allocated); the sender's own
+        // earlier copies are ordered by its stream already
+        s = remote_apply_waits(p);
         if (s == MP_OK) s = meta_fence(p);
         if (s == MP_OK && cudaEventRecord(p->ev_ipc, p->stream) != cudaSuccess) s = MP_ERR_CUDA;
+        if (s == MP_OK && staged) s = staged_recv(p, r, r->pending, meds, j0, nj);
+        if (s != MP_OK) {
+          dst_abort(p, r->pending);
+          r->has_pending = false;
+        }
+      }
+      std::vector<mp_addr> fin;
+      uint32_t done_seq = 0;
+      if (s == MP_OK && one_trip) {
+        r->has_pending = false;
+        const int64_t nfin = r->pending.kind == 1 ? r->pending.ceil_b : r->pending.nm;
+        fin.assign((size_t)std::max<int64_t>(nfin, 1), 0);
+        s = dst_commit(p, r->pending, fin.data());
+        fin.resize((size_t)nfin);
+        if (s == MP_OK) {
+          done_seq = ++r->in_seq;
+          r->async_in.push_back({++p->prep_stamp, done_seq});
+        }
       }
       rtype = REP_PREP;
       rstatus = s;
       if (s == MP_OK) {
         wr.put<int64_t>(r->pending.skip);
         wr.put<int64_t>(r->pending.nm);
-        wr.put<int64_t>(r->pending.d_dst_off);
         wr.bytes(r->pending.dids.data(), (int64_t)r->pending.dids.size() * 4);
+        if (staged) {
+          cudaIpcMemHandle_t hnd;
+          if (cudaIpcGetMemHandle(&hnd, r->ring) != cudaSuccess) rstatus = MP_ERR_CUDA;
+          wr.bytes(&hnd, sizeof(hnd));
+          wr.put<uint64_t>(r->ring_id);
+          wr.put<uint32_t>(slot0);
+        }
+        if (one_trip) {
+          wr.put<uint32_t>(done_seq);
+          wr.put<int64_t>((int64_t)fin.size());
+          wr.bytes(fin.data(), (int64_t)fin.size() * (int64_t)sizeof(mp_addr));
+        }
       }
       break;
     }
@@ -283,6 +458,25 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         break;
       }
       r->has_pending = false;
+      const bool staged = (r->pending.flags & MP_XFER_PATH_MASK) == MP_XFER_PATH_STAGED;
+      if (staged && r->recv_stream) {
+        // every unpack of this transfer is on recv_stream (the sender has
+        // raised every slot's ready flag, also on failure)
+        if (cudaEventRecord(r->recv_ev, r->recv_stream) != cudaSuccess) {
+          rstatus = MP_ERR_CUDA;
+          break;
+        }
+        if (sender_status != MP_OK || !(r->pending.flags & MP_XFER_ASYNC)) {
+          // data landed before the receiver says ok; a failed
+          // transfer's unpacks finish before its blocks are released
+          if (cudaEventSynchronize(r->recv_ev) != cudaSuccess) {
+            rstatus = MP_ERR_CUDA;
+            break;
+          }
+        } else {
+          r->recv_join = true;  // later data-stream work joins it lazily
+        }
+      }
       if (sender_status != MP_OK) {  // the transmission failed on the sender:
         // release what the allocation step took (pins, fresh blocks)
         dst_abort(p, r->pending);
@@ -352,10 +546,26 @@ mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
 mp_status remote_apply_waits(mp_pool* p) {
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
-    if (!r->inbound_pending) continue;
+    if (!r->inbound_pending && !r->recv_join && r->async_in.empty()) continue;
     DevGuard g(p->dev);
-    CK(cudaStreamWaitEvent(p->stream, r->ev, 0));
-    r->inbound_pending = false;
+    if (r->inbound_pending) {  // a completed two-round-trip transfer (event recorded before DONE)
+      CK(cudaStreamWaitEvent(p->stream, r->ev, 0));
+      r->inbound_pending = false;
+    }
+    if (r->recv_join) {  // the unpacks of a completed STAGED transfer
+      CK(cudaStreamWaitEvent(p->stream, r->recv_ev, 0));
+      r->recv_join = false;
+    }
+    // one-round-trip transfers: only those prepared before the transfer this
+    // pool is issuing right now (join_bound), whose senders started earlier
+    bool any = false;
+    uint32_t seq = 0;
+    while (!r->async_in.empty() && r->async_in.front().first <= p->join_bound) {
+      seq = r->async_in.front().second;
+      r->async_in.pop_front();
+      any = true;
+    }
+    if (any) TRY(stream_wait_geq(p->stream, r->in_sync->d + kSyncDone, seq));
   }
   return MP_OK;
 }
@@ -373,16 +583,140 @@ mp_status remote_serve_once(mp_pool* p, int64_t* served) {
 }
 
 // ------------------------------------------------------------ sender side
+namespace {
+
+// The transmission step of a cross-process transfer ("the sender
+// transmits the KV cache to the receiver using the fastest available path"),
+// issued on the sender's GPU.  (hs, hd): sources in the sender's HBM and
+// their destination ids; (ds, dd): sources swapped out to its pinned DRAM
+// (memory asymmetry), always stored by one kernel straight into
+// the receiver's blocks.  Transports of the HBM part:
+//   FUSED     one gather -> peer-store kernel (A6f; engine and split from the
+//             pool's peer_engine / peer_sched)
+//   CE        one copy-engine memcpy per (block, layer, K/V) chunk (the
+//             paper's discrete per-block transfer)
+//   CE_BATCH  one cudaMemcpyBatchAsync of all the chunks
+//   STAGED    pack into a staging slot (A4, the paper's aggregation
+//             P:549-550), one copy-engine memcpy of the slot into the
+//             receiver's inbound ring (A5), unpack there (A6) -- pipelined
+//             over the ring's slots by device-side flags
+mp_status remote_transmit(mp_pool* src, RemotePeer* r, uint32_t path, int j0, int nj,
+                          const std::vector<int32_t>& hs, const std::vector<int32_t>& hd,
+                          const std::vector<int32_t>& ds, const std::vector<int32_t>& dd,
+                          const RingGeom& geom, uint32_t slot0) {
+  TRY(flush_involving(src));
+  const bool staged = path == MP_XFER_PATH_STAGED;
+  // stores into the receiver's fresh blocks follow its allocation and every
+  // earlier use of them there (its event, recorded before the reply); the
+  // STAGED ring is ordered by its flags instead
+  if (!staged || !ds.empty()) CK(cudaStreamWaitEvent(src->stream, r->ev, 0));
+  const int64_t n = (int64_t)hs.size();
+  if (n > 0 && (path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED)) {
+    mpk::InlineIds si;
+    int *d_s = nullptr, *d_d = nullptr;
+    const bool both = pair_inline(hs, hd, &si);
+    if (!both) {
+      TRY(src_ids(src, hs, &d_s, &si));
+      TRY(upload_ids(src, hd, &d_d));
+    }
+    const LaunchBlocks lb{&src->bmarks, hs.data(), &r->bmarks, hd.data(), n};
+    // a receiver process on this same GPU: its IPC-mapped pool is local HBM,
+    // so the copy takes the loopback engine (bulk ring, claiming)
+    TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
+                             pool_ep(r->d_slabs, d_d), n, j0, nj, /*peer=*/!r->same_device, 0,
+                             si.n ? &si : nullptr, /*meta_dep=*/!both, &lb));
+  } else if (n > 0 && (path == MP_XFER_PATH_CE || path == MP_XFER_PATH_CE_BATCH)) {
+    std::vector<void*> dps, sps;
+    dps.reserve((size_t)(n * nj));
+    sps.reserve((size_t)(n * nj));
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = j0; j < j0 + nj; ++j) {
+        dps.push_back(r->slabs_h[(size_t)j] + (int64_t)hd[(size_t)i] * src->chunk);
+        sps.push_back(src->slabs[(size_t)j] + (int64_t)hs[(size_t)i] * src->chunk);
+      }
+    if (path == MP_XFER_PATH_CE) {
+      for (size_t i = 0; i < dps.size(); ++i)
+        CK(cudaMemcpyAsync(dps[i], sps[i], (size_t)src->chunk, cudaMemcpyDefault, src->stream));
+    } else {
+      std::vector<size_t> sz(dps.size(), (size_t)src->chunk);
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      size_t attr_idx = 0, fail = 0;
+      CK(cudaMemcpyBatchAsync(dps.data(), sps.data(), sz.data(), sz.size(), &attr, &attr_idx, 1,
+                              &fail, src->stream));
+    }
+    track_fence(src->track);
+    src->stats.bytes_moved += (uint64_t)(n * nj * src->chunk);
+  } else if (n > 0 && staged) {
+    TRY(staging_acquire(src, src->stream));
+    const int64_t per_block = (int64_t)nj * src->chunk;
+    uint32_t q = slot0;
+    for (int64_t off = 0; off < n; off += geom.k, ++q) {
+      const int slot = (int)(q % (uint32_t)geom.S);
+      const int64_t nb = std::min<int64_t>(geom.k, n - off);
+      char* mine = src->staging + (int64_t)slot * geom.slot_bytes;
+      // my slot: its previous copy out is done
+      CK(cudaStreamWaitEvent(src->stream, src->slot_ev[(size_t)slot], 0));
+      mpk::InlineIds si;
+      si.n = (int)nb;
+      std::memcpy(si.ids, hs.data() + off, (size_t)nb * sizeof(int32_t));
+      TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, nullptr),
+                               agg_ep(mine, per_block, nullptr), nb, j0, nj, false, 0, &si,
+                               /*meta_dep=*/false));
+      CK(cudaEventRecord(src->pack_ev[(size_t)slot], src->stream));
+      CK(cudaStreamWaitEvent(src->copy_stream, src->pack_ev[(size_t)slot], 0));
+      // the peer's slot: its previous unpack is done (free flag)
+      if (q >= (uint32_t)geom.S)
+        TRY(stream_wait_geq(src->copy_stream, r->out_sync->d + kSyncFree + slot,
+                            q + 1 - (uint32_t)geom.S));
+      CK(cudaMemcpyAsync(r->peer_ring + (int64_t)slot * geom.slot_bytes, mine,
+                         (size_t)(nb * per_block), cudaMemcpyDeviceToDevice, src->copy_stream));
+      TRY(stream_write_u32(src->copy_stream, r->out_sync->d + kSyncReady + slot, q + 1));
+      CK(cudaEventRecord(src->slot_ev[(size_t)slot], src->copy_stream));
+    }
+  }
+  if (!ds.empty()) {
+    int *d_s = nullptr, *d_d = nullptr;
+    mpk::InlineIds si;
+    TRY(src_ids(src, ds, &d_s, &si));
+    TRY(upload_ids(src, dd, &d_d));
+    TRY(launch_migrate_timed(src, src->stream,
+                             agg_ep(src->dram_dev + (int64_t)j0 * src->chunk, src->Pb, d_s),
+                             pool_ep(r->d_slabs, d_d), (int64_t)ds.size(), j0, nj,
+                             /*peer=*/true, 0, si.n ? &si : nullptr));
+  }
+  return MP_OK;
+}
+
+}  // namespace
+
 mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,
                           int64_t n_tok, const std::vector<int32_t>& sids,
                           const std::vector<uint8_t>& smeds, int64_t n, mp_addr* da,
                           uint32_t flags, int32_t l0, int32_t l1, const void* priv,
                           int64_t priv_len, int64_t* n_moved) {
   const uint32_t path = flags & MP_XFER_PATH_MASK;
-  if (path != MP_XFER_PATH_AUTO && path != MP_XFER_PATH_FUSED) {
-    set_err("cross-process transfers use the fused one-sided path");
+  if (path != MP_XFER_PATH_AUTO && path != MP_XFER_PATH_FUSED && path != MP_XFER_PATH_STAGED &&
+      path != MP_XFER_PATH_CE && path != MP_XFER_PATH_CE_BATCH) {
+    set_err("unknown transfer path");
     return MP_ERR_CONFIG;
   }
+  const bool staged = path == MP_XFER_PATH_STAGED;
+  const bool one_trip = (flags & MP_XFER_ASYNC) && !staged;
+  const int j0 = kind == 1 ? 0 : 2 * l0;
+  const int nj = kind == 1 ? src->nch : 2 * (l1 - l0);
+  RingGeom geom;
+  if (staged) {
+    geom = ring_geom(src->staging_bytes, src->staging_slots, r->staging_bytes, r->staging_slots,
+                     (int64_t)nj * src->chunk);
+    if (geom.k < 1) {
+      set_err("staging slot smaller than one block");
+      return MP_ERR_CONFIG;
+    }
+  }
+  // inbound one-round-trip transfers prepared after this point are not
+  // joined while this transfer is issued (mp_pool::join_bound)
+  const uint64_t start_stamp = src->prep_stamp;
   Channel* c = r->out;
   // ---- request: the receiver allocates ----
   Writer wr{c->req_payload(), kChanCap};
@@ -395,6 +729,9 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   if (flags & MP_XFER_DST_GIVEN) wr.bytes(da, n * (int64_t)sizeof(mp_addr));
   wr.put<int64_t>(priv_len);
   wr.bytes(priv, priv_len);
+  wr.put<int32_t>(j0);
+  wr.put<int32_t>(nj);
+  wr.bytes(smeds.data(), n);
   if (!wr.ok) {
     set_err("request larger than the mailbox");
     return MP_ERR_BUFFER_TOO_SMALL;
@@ -432,74 +769,87 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   Reader rd{c->rep_payload(), (int64_t)rp->len};
   const int64_t skip = rd.get<int64_t>();
   const int64_t nm = rd.get<int64_t>();
-  const int64_t off = rd.get<int64_t>();
   const int32_t* dids = (const int32_t*)rd.bytes(nm * 4);
-  if (!rd.ok || skip < 0 || skip + nm != n) {
+  cudaIpcMemHandle_t ring_hnd{};
+  uint64_t ring_id = 0;
+  uint32_t slot0 = 0, done_seq = 0;
+  int64_t nfin = 0;
+  const mp_addr* fin = nullptr;
+  if (staged) {
+    const void* hp = rd.bytes(sizeof(ring_hnd));
+    if (hp) std::memcpy(&ring_hnd, hp, sizeof(ring_hnd));
+    ring_id = rd.get<uint64_t>();
+    slot0 = rd.get<uint32_t>();
+  }
+  if (one_trip) {
+    done_seq = rd.get<uint32_t>();
+    nfin = rd.get<int64_t>();
+    fin = (const mp_addr*)rd.bytes(nfin * (int64_t)sizeof(mp_addr));
+  }
+  if (!rd.ok || skip < 0 || skip + nm != n || (staged && slot0 != r->out_slot)) {
     unpin();
     set_err("malformed allocation reply");
     return MP_ERR_INTERNAL;
   }
-  // ---- transmission: one-sided stores into the receiver's blocks ----
+  // ---- transmission ----
   mp_status xs = MP_OK;
+  uint32_t slot_end = slot0;
   {
     DevGuard g(src->dev);
-    // HBM-resident sources and (memory asymmetry) sources swapped
-    // out to our pinned DRAM, each with its destination ids
     std::vector<int32_t> hs, hd, ds_, dd_;
-    bool mixed = false;
     for (int64_t i = skip; i < n; ++i) {
       const bool dram = smeds[(size_t)i] == MP_DRAM;
-      mixed = mixed || dram;
       (dram ? ds_ : hs).push_back(sids[(size_t)i]);
       (dram ? dd_ : hd).push_back(dids[i - skip]);
     }
-    const int j0 = kind == 1 ? 0 : 2 * l0;
-    const int nj = kind == 1 ? src->nch : 2 * (l1 - l0);
-    xs = flush_involving(src);
-    if (xs == MP_OK && cudaStreamWaitEvent(src->stream, r->ev, 0) != cudaSuccess) xs = MP_ERR_CUDA;
-    if (xs == MP_OK && !hs.empty()) {
-      int* d_s = nullptr;
-      const int* d_d = nullptr;
-      mpk::InlineIds si;
-      xs = src_ids(src, hs, &d_s, &si);
-      if (xs == MP_OK) {
-        if (off >= 0 && !mixed) {
-          d_d = r->arena + off;  // the receiver's device allocator output, IPC mapped
+    if (staged) {
+      slot_end = slot0 + (uint32_t)(((int64_t)hs.size() + geom.k - 1) / geom.k);
+      r->out_slot = slot_end;  // the receiver has queued its unpacks for all of them
+      if (!hs.empty() && r->peer_ring_id != ring_id) {
+        if (r->peer_ring) cudaIpcCloseMemHandle(r->peer_ring);
+        r->peer_ring = nullptr;
+        void* m = nullptr;
+        if (cudaIpcOpenMemHandle(&m, ring_hnd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          set_err("cudaIpcOpenMemHandle of the peer's inbound ring failed");
+          xs = MP_ERR_CUDA;
         } else {
-          int* t = nullptr;
-          xs = upload_ids(src, hd, &t);
-          d_d = t;
+          r->peer_ring = (char*)m;
+          r->peer_ring_id = ring_id;
         }
       }
-      if (xs == MP_OK)
-        // a receiver process on this same GPU: its IPC-mapped pool is local
-        // HBM, so the copy takes the loopback engine (bulk ring, claiming)
-      {
-        const LaunchBlocks lb{&src->bmarks, hs.data(), &r->bmarks, hd.data(), (int64_t)hs.size()};
-        xs = launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
-                                  pool_ep(r->d_slabs, d_d), (int64_t)hs.size(), j0, nj,
-                                  /*peer=*/!r->same_device, 0, si.n ? &si : nullptr, true, &lb);
-      }
     }
-    if (xs == MP_OK && !ds_.empty()) {
-      int *d_s = nullptr, *d_d = nullptr;
-      mpk::InlineIds si;
-      xs = src_ids(src, ds_, &d_s, &si);
-      if (xs == MP_OK) xs = upload_ids(src, dd_, &d_d);
-      if (xs == MP_OK)
-        xs = launch_migrate_timed(src, src->stream,
-                                  agg_ep(src->dram_dev + (int64_t)j0 * src->chunk, src->Pb, d_s),
-                                  pool_ep(r->d_slabs, d_d), (int64_t)ds_.size(), j0, nj,
-                                  /*peer=*/true, 0, si.n ? &si : nullptr);
+    src->join_bound = start_stamp;
+    if (xs == MP_OK) xs = remote_transmit(src, r, path, j0, nj, hs, hd, ds_, dd_, geom, slot0);
+    src->join_bound = ~0ull;
+    if (xs != MP_OK) {
+      // release the peer's streams: every flag it waits on is raised from
+      // the host once this side's copies are drained (or dead)
+      cudaStreamSynchronize(src->stream);
+      cudaStreamSynchronize(src->copy_stream);
+      cudaGetLastError();
+      for (uint32_t q = slot0; q != slot_end; ++q)
+        host_raise(r->out_sync->h + kSyncReady + q % (uint32_t)geom.S, q + 1);
+      if (one_trip) host_raise(r->out_sync->h + kSyncDone, done_seq);
+    } else if (one_trip) {
+      xs = stream_write_u32(src->stream, r->out_sync->d + kSyncDone, done_seq);
+    } else {
+      if (cudaEventRecord(src->ev_ipc, src->stream) != cudaSuccess) xs = MP_ERR_CUDA;
+      if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);
     }
-    if (xs == MP_OK && cudaEventRecord(src->ev_ipc, src->stream) != cudaSuccess) xs = MP_ERR_CUDA;
-    if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);
     src->stats.blocks_moved += (uint64_t)nm;
   }
   if (tm) {
     const double t = now_s();
     g_phase.add(1, t - t0);
     t0 = t;
+  }
+  if (one_trip) {  // committed at the receiver's allocation step: no second round trip
+    unpin();
+    if (xs != MP_OK) return xs;
+    std::memcpy(da, fin, (size_t)nfin * sizeof(mp_addr));
+    if (n_moved) *n_moved = nm;
+    return MP_OK;
   }
   // ---- notify; the receiver inserts and answers ok ----
   Writer w2{c->req_payload(), kChanCap};
@@ -514,13 +864,13 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   rp = c->rep();
   if (rp->status != MP_OK) return (mp_status)rp->status;
   Reader r2{c->rep_payload(), (int64_t)rp->len};
-  const int64_t nfin = r2.get<int64_t>();
-  const void* fin = r2.bytes(nfin * (int64_t)sizeof(mp_addr));
+  const int64_t nf2 = r2.get<int64_t>();
+  const void* f2 = r2.bytes(nf2 * (int64_t)sizeof(mp_addr));
   if (!r2.ok) {
     set_err("malformed completion reply");
     return MP_ERR_INTERNAL;
   }
-  std::memcpy(da, fin, (size_t)nfin * sizeof(mp_addr));
+  std::memcpy(da, f2, (size_t)nf2 * sizeof(mp_addr));
   if (n_moved) *n_moved = nm;
   return MP_OK;
 }
@@ -535,13 +885,14 @@ struct WireHandle {
   uint32_t magic, version;
   int32_t inst, dev, L, H, D, elem, B, nch;
   int64_t n_hbm, chunk;
+  int64_t staging_bytes;  // STAGED ring geometry
+  int32_t staging_slots, pad0;
   uint64_t uid;
   char bus_id[32];
   int32_t n_allocs, pad;
   cudaIpcMemHandle_t allocs[kMaxSlabs];
   int32_t slab_alloc[kMaxSlabs];
   int64_t slab_off[kMaxSlabs];
-  cudaIpcMemHandle_t arena;
   cudaIpcEventHandle_t ev;
 };
 
@@ -577,6 +928,13 @@ std::string chan_name(uint64_t from, uint64_t to) {
   return buf;
 }
 
+std::string sync_name(uint64_t from, uint64_t to) {
+  char buf[64];
+  snprintf(buf, sizeof(buf), "/mps_%016llx_%016llx", (unsigned long long)from,
+           (unsigned long long)to);
+  return buf;
+}
+
 }  // namespace
 
 void remote_close_all(mp_pool* p) {
@@ -586,13 +944,20 @@ void remote_close_all(mp_pool* p) {
     RemotePeer* r = kv.second;
     {
       DevGuard g(p->dev);
+      if (r->recv_stream) cudaStreamSynchronize(r->recv_stream);
       if (r->d_slabs) cudaFree(r->d_slabs);
       for (void* m : r->mapped) cudaIpcCloseMemHandle(m);
-      if (r->arena) cudaIpcCloseMemHandle(r->arena);
+      if (r->peer_ring) cudaIpcCloseMemHandle(r->peer_ring);
+      if (r->ring) cudaFree(r->ring);
       if (r->ev) cudaEventDestroy(r->ev);
+      if (r->recv_dep) cudaEventDestroy(r->recv_dep);
+      if (r->recv_ev) cudaEventDestroy(r->recv_ev);
+      if (r->recv_stream) cudaStreamDestroy(r->recv_stream);
     }
     chan_close(r->out, true);
     chan_close(r->in, true);
+    sync_close(r->out_sync);
+    sync_close(r->in_sync);
     delete r;
   }
   p->remotes.clear();
@@ -620,7 +985,7 @@ mp_status mp_export_handle(mp_pool* p, void* buf, int64_t cap, int64_t* len) {
   WireHandle* h = new WireHandle();
   std::memset(h, 0, sizeof(*h));
   h->magic = kHandleMagic;
-  h->version = 1;
+  h->version = 2;
   h->inst = p->inst;
   h->dev = p->dev;
   h->L = p->L;
@@ -631,6 +996,8 @@ mp_status mp_export_handle(mp_pool* p, void* buf, int64_t cap, int64_t* len) {
   h->nch = p->nch;
   h->n_hbm = p->n_hbm;
   h->chunk = p->chunk;
+  h->staging_bytes = p->staging_bytes;
+  h->staging_slots = p->staging_slots;
   h->uid = p->uid;
   if (cudaDeviceGetPCIBusId(h->bus_id, sizeof(h->bus_id), p->dev) != cudaSuccess) {
     delete h;
@@ -659,10 +1026,9 @@ mp_status mp_export_handle(mp_pool* p, void* buf, int64_t cap, int64_t* len) {
     h->slab_off[j] = p->slabs[(size_t)j] - base;
   }
   h->n_allocs = (int32_t)bases.size();
-  if (cudaIpcGetMemHandle(&h->arena, p->ar.d) != cudaSuccess ||
-      cudaIpcGetEventHandle(&h->ev, p->ev_ipc) != cudaSuccess) {
+  if (cudaIpcGetEventHandle(&h->ev, p->ev_ipc) != cudaSuccess) {
     delete h;
-    set_err("cudaIpcGet*Handle failed (arena / event)");
+    set_err("cudaIpcGetEventHandle failed");
     return MP_ERR_CUDA;
   }
   std::memcpy(buf, h, sizeof(*h));
@@ -679,7 +1045,7 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
     delete h;
     return s;
   };
-  if (h->magic != kHandleMagic || h->version != 1) return fail(MP_ERR_CONFIG, "bad handle");
+  if (h->magic != kHandleMagic || h->version != 2) return fail(MP_ERR_CONFIG, "bad handle");
   if (h->inst == p->inst || p->peers.count(h->inst) || p->remotes.count(h->inst))
     return fail(MP_ERR_CONFIG, "instance id already known");
   if (h->L != p->L || h->chunk != p->chunk || h->B != p->B || h->nch != p->nch)
@@ -691,8 +1057,10 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
   r->uid = h->uid;
   char mine[32] = {0};
   cudaDeviceGetPCIBusId(mine, sizeof(mine), p->dev);
-  r->same_device = std::strncmp(mine, h->bus_id, sizeof(mine)) == 0;
+  r->same_device = std::strncmp(mine, h->bus_id, sizeof(mine)) == 0 && !p->force_peer;
   r->bmarks.reset((size_t)h->n_hbm);
+  r->staging_bytes = h->staging_bytes;
+  r->staging_slots = h->staging_slots;
   bool ok = true;
   for (int k = 0; k < h->n_allocs && ok; ++k) {
     void* m = nullptr;
@@ -702,9 +1070,7 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
   std::vector<char*> slabs((size_t)h->nch);
   for (int j = 0; ok && j < h->nch; ++j)
     slabs[(size_t)j] = (char*)r->mapped[(size_t)h->slab_alloc[j]] + h->slab_off[j];
-  void* ar = nullptr;
-  if (ok) ok = cudaIpcOpenMemHandle(&ar, h->arena, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
-  r->arena = (int*)ar;
+  r->slabs_h = slabs;
   if (ok) ok = cudaIpcOpenEventHandle(&r->ev, h->ev) == cudaSuccess;
   if (ok) ok = cudaMalloc(&r->d_slabs, sizeof(char*) * (size_t)h->nch) == cudaSuccess;
   if (ok)
@@ -714,6 +1080,11 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
     r->out = chan_open(chan_name(p->uid, r->uid));
     r->in = chan_open(chan_name(r->uid, p->uid));
     ok = r->out && r->in;
+  }
+  if (ok) {
+    r->out_sync = sync_open(sync_name(p->uid, r->uid));
+    r->in_sync = sync_open(sync_name(r->uid, p->uid));
+    ok = r->out_sync && r->in_sync;
   }
   if (!ok) {
     std::string why = std::string("import failed: ") + cudaGetErrorString(cudaGetLastError());

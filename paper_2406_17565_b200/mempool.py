@@ -81,6 +81,7 @@ class PoolConfig(C.Structure):
         ("slabs", C.POINTER(C.c_void_p)), ("dram_base", C.c_void_p),
         ("staging_bytes", C.c_int64), ("staging_slots", C.c_int32), ("max_ctas", C.c_int32),
         ("copy_kernel", C.c_int32), ("coalesce_mib", C.c_int32),
+        ("peer_engine", C.c_int32), ("peer_sched", C.c_int32), ("force_peer", C.c_int32),
     ]
 
 
@@ -255,7 +256,8 @@ class Pool:
                  head_dim: int, block_tokens: int, hbm_blocks: int, dram_blocks: int = 0,
                  elem_bytes: int = 2, slabs=None, dram_base=None, staging_bytes: int = 0,
                  staging_slots: int = 0, max_ctas: int = 0, verify: bool = False,
-                 copy_kernel: int = 0, coalesce_mib: int = 0):
+                 copy_kernel: int = 0, coalesce_mib: int = 0, peer_engine: int = 0,
+                 peer_sched: int = 0, force_peer: bool = False):
         self.inst = instance_id
         self.B = block_tokens
         self.L = layers
@@ -263,7 +265,7 @@ class Pool:
         cfg = PoolConfig(instance_id, device, layers, kv_heads, head_dim, elem_bytes,
                          block_tokens, int(verify), hbm_blocks, dram_blocks, None,
                          dram_base, staging_bytes, staging_slots, max_ctas, copy_kernel,
-                         coalesce_mib)
+                         coalesce_mib, peer_engine, peer_sched, int(force_peer))
         if slabs is not None:
             assert len(slabs) == 2 * layers
             self._slab_arr = (C.c_void_p * len(slabs))(*[int(s) for s in slabs])

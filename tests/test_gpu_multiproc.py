@@ -14,8 +14,24 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
+# Cross-process transports (name -> (pool keywords, path flag)).  On a 1-GPU
+# box both processes share cuda:0; force_peer makes the sender treat the
+# receiver as a remote GPU, so the NVLink dispatch (one-sided stores with
+# the peer engine / split) is what runs and is checked here.
+TINY_BLOCK = 16 * 1024
+TRANSPORTS = {
+    "fused-loopback": ({}, "PATH_FUSED"),
+    "fused-vector-static": ({"force_peer": True, "peer_engine": 1, "peer_sched": 1},
+                            "PATH_FUSED"),
+    "fused-bulk-dynamic": ({"force_peer": True, "peer_engine": 2, "peer_sched": 2},
+                           "PATH_FUSED"),
+    # 2 slots of 2 tiny blocks: the ring wraps inside one transfer
+    "ce-staged": ({"staging_bytes": 4 * TINY_BLOCK, "staging_slots": 2}, "PATH_STAGED"),
+    "ce-batch": ({}, "PATH_CE_BATCH"),
+}
 
-def _run(rank, port, dedup, q):
+
+def _run(rank, port, dedup, q, transport="fused-loopback"):
     try:
         import torch
         import torch.distributed as dist
@@ -27,8 +43,10 @@ def _run(rank, port, dedup, q):
         dist.init_process_group("gloo", rank=rank, world_size=2)
         torch.cuda.set_device(0)
         s = TINY
+        kw, pname = TRANSPORTS[transport]
+        path = getattr(M, pname)
         pool = M.Pool(rank, 0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64,
-                      dram_blocks=16 if rank == 0 else 0, verify=True)
+                      dram_blocks=16 if rank == 0 else 0, verify=True, **kw)
         blobs = M.exchange_handles(pool)
         pool.import_peer(blobs[1 - rank][1])
         dist.barrier()
@@ -42,7 +60,7 @@ def _run(rank, port, dedup, q):
                 pool.debug_fill(new, 17565)
                 full = np.concatenate([matched, new])
                 pool.insert(p, full[: len(p) // 16])
-                fl = M.XFER_DEDUP if dedup else 0
+                fl = (M.XFER_DEDUP if dedup else 0) | path
                 if i == 2:
                     fl |= M.XFER_ASYNC
                 final, moved = pool.transfer_with_insert(1, p, full, flags=fl,
@@ -50,12 +68,12 @@ def _run(rank, port, dedup, q):
                 finals.append((M.addr_indices(final).tolist(), moved))
             extra = pool.alloc_mem(3)
             pool.debug_fill(extra, 17565)
-            d = pool.transfer(1, extra, priv=b"plain")
+            d = pool.transfer(1, extra, flags=path, priv=b"plain")
             finals.append((M.addr_indices(d).tolist(), 3))
             # memory asymmetry: historical KV swapped out to this
             # process's pinned DRAM goes straight into the peer's HBM
             _old, dram = pool.swap_out(2)
-            d = pool.transfer(1, dram, priv=b"from-dram")
+            d = pool.transfer(1, dram, flags=path, priv=b"from-dram")
             finals.append((M.addr_indices(d).tolist(), 2))
             pool.send_mark(1, 7)
             out["finals"] = finals
@@ -83,15 +101,16 @@ def _run(rank, port, dedup, q):
         q.put((rank, {"error": traceback.format_exc() + repr(e)}))
 
 
+@pytest.mark.parametrize("transport", list(TRANSPORTS))
 @pytest.mark.parametrize("dedup", [False, True])
-def test_two_process_golden(dedup):
+def test_two_process_golden(dedup, transport):
     import oracle as O
     from workloads.configs import TINY
     from workloads.traces import golden_prompts
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29700 + (os.getpid() % 200) + int(dedup)
-    ps = [ctx.Process(target=_run, args=(r, port, dedup, q)) for r in range(2)]
+    port = 29700 + (os.getpid() % 200) + int(dedup) + 2 * list(TRANSPORTS).index(transport)
+    ps = [ctx.Process(target=_run, args=(r, port, dedup, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
     res = {}
@@ -140,7 +159,7 @@ def test_two_process_golden(dedup):
     assert res[1]["msgs"] == want_msgs
 
 
-def _stress(rank, port, q):
+def _stress(rank, port, q, transport="fused-loopback"):
     """Rank 0 streams back-to-back ASYNC transfers (random scattered 7B
     blocks) into rank 1's pool through the cross-process path, rank 1 serves;
     then every received block is compared with its source by weighted
@@ -158,8 +177,12 @@ def _stress(rank, port, q):
         c = S.chunk_bytes
         region = torch.empty(2 * S.layers * n * c, dtype=torch.uint8, device="cuda:0")
         slabs = [region.data_ptr() + j * n * c for j in range(2 * S.layers)]
+        kw, pname = TRANSPORTS[transport]
+        if "staging_bytes" in kw:   # 7B blocks: 3 slots of 2 blocks
+            kw = {"staging_bytes": 6 * S.block_bytes, "staging_slots": 3}
+        path = getattr(M, pname)
         pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, n,
-                      slabs=slabs, verify=True)
+                      slabs=slabs, verify=True, **kw)
         blobs = M.exchange_handles(pool)
         pool.import_peer(blobs[1 - rank][1])
         dist.barrier()
@@ -171,7 +194,7 @@ def _stress(rank, port, q):
             for rnd in range(3):
                 for _ in range(30):
                     sel = src[rng.choice(n, int(rng.integers(1, 12)), replace=False)]
-                    d = pool.transfer(1, sel, flags=M.XFER_ASYNC)
+                    d = pool.transfer(1, sel, flags=M.XFER_ASYNC | path)
                     if rnd == 2:
                         pairs += list(zip(M.addr_indices(sel).tolist(),
                                           M.addr_indices(d).tolist()))
@@ -205,11 +228,15 @@ def _stress(rank, port, q):
         q.put((rank, {"error": traceback.format_exc() + repr(e)}))
 
 
-def test_two_process_back_to_back_async():
+@pytest.mark.parametrize("transport", ["fused-loopback", "fused-vector-static",
+                                       "fused-bulk-dynamic", "ce-staged", "ce-batch"])
+def test_two_process_back_to_back_async(transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29950 + (os.getpid() % 40)
-    ps = [ctx.Process(target=_stress, args=(r, port, q)) for r in range(2)]
+    port = 30300 + (os.getpid() % 40) + 50 * ["fused-loopback", "fused-vector-static",
+                                              "fused-bulk-dynamic", "ce-staged",
+                                              "ce-batch"].index(transport)
+    ps = [ctx.Process(target=_stress, args=(r, port, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
     res = {}
@@ -390,7 +417,7 @@ def _d_retire(msgs, prompts, phase_ops):
     return frees, deletes
 
 
-def _rand_worker(rank, port, seed, q):
+def _rand_worker(rank, port, seed, q, transport="fused-loopback"):
     try:
         import torch
         import torch.distributed as dist
@@ -401,8 +428,11 @@ def _rand_worker(rank, port, seed, q):
         dist.init_process_group("gloo", rank=rank, world_size=2)
         torch.cuda.set_device(0)
         prompts, phases = _rand_ops(seed)
+        kw, pname = TRANSPORTS[transport]
+        path = getattr(M, pname)
         pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens,
-                      48 if rank == 0 else 24, dram_blocks=12 if rank == 0 else 0, verify=True)
+                      48 if rank == 0 else 24, dram_blocks=12 if rank == 0 else 0, verify=True,
+                      **kw)
         blobs = M.exchange_handles(pool)
         pool.import_peer(blobs[1 - rank][1])
         dist.barrier()
@@ -419,7 +449,8 @@ def _rand_worker(rank, port, seed, q):
                             pool.debug_fill(new, 17565)
                             full = np.concatenate([m, new])
                             pool.insert(t, full[: len(t) // 16])
-                            fl = (M.XFER_DEDUP if dedup else 0) | (M.XFER_ASYNC if asy else 0)
+                            fl = ((M.XFER_DEDUP if dedup else 0) | (M.XFER_ASYNC if asy else 0)
+                                  | path)
                             fin, moved = pool.transfer_with_insert(1, t, full, flags=fl)
                             if len(t) % 16:
                                 pool.free_mem(full[-1:])
@@ -434,7 +465,7 @@ def _rand_worker(rank, port, seed, q):
                             if ids:
                                 src = np.array([M.make_addr(0, M.DRAM, i) for i in ids],
                                                np.uint64)
-                                d = pool.transfer(1, src)
+                                d = pool.transfer(1, src, flags=path)
                                 res.append(("xfer_dram", ids, M.addr_indices(d).tolist()))
                         elif op[0] == "p_delete":
                             pool.delete(prompts[op[1]])
@@ -524,13 +555,16 @@ def _rand_oracle(seed):
     return P, D, res
 
 
-@pytest.mark.parametrize("seed", [3, 11, 29])
-def test_two_process_random_ops(seed):
+@pytest.mark.parametrize("seed,transport", [(3, "fused-loopback"), (11, "fused-loopback"),
+                                            (29, "fused-loopback"), (5, "fused-vector-static"),
+                                            (7, "fused-bulk-dynamic"), (13, "ce-staged"),
+                                            (17, "ce-batch")])
+def test_two_process_random_ops(seed, transport):
     import oracle as O
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29990 + (os.getpid() % 8) + seed
-    ps = [ctx.Process(target=_rand_worker, args=(r, port, seed, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rand_worker, args=(r, port, seed, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
     got = {}

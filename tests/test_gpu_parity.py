@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 
 PATHS = [M.PATH_FUSED, M.PATH_STAGED, M.PATH_CE]
 # stream-ordered (MP_XFER_ASYNC) variants: results must not depend on the sync
-PATHS_ASYNC = [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_CE | M.XFER_ASYNC]
+PATHS_ASYNC = [M.PATH_FUSED | M.XFER_ASYNC, M.PATH_CE | M.XFER_ASYNC,
+               M.PATH_STAGED | M.XFER_ASYNC]
 
 
 def golden_pair(dedup, path, n_dram=64):
@@ -119,9 +120,10 @@ def test_dram_source_memory_asymmetry(path):
 
 
 def random_ops(seed, shape, n_ops, path, n_hbm=48, n_dram=24, copy_kernel=0, coalesce_mib=0,
-               swap_flags=0, staging_bytes=0, n_pools=2):
+               swap_flags=0, staging_bytes=0, n_pools=2, **pool_kw):
     rng = np.random.default_rng(seed)
-    kw = dict(copy_kernel=copy_kernel, coalesce_mib=coalesce_mib, staging_bytes=staging_bytes)
+    kw = dict(copy_kernel=copy_kernel, coalesce_mib=coalesce_mib, staging_bytes=staging_bytes,
+              **pool_kw)
     twins = [Twin(i, shape, n_hbm, n_dram, **kw) for i in range(n_pools)]
     for t in twins:
         t.swap_flags = swap_flags
@@ -283,6 +285,39 @@ def test_multi_piece_chunks(copy_kernel):
     shape = KVShape("mp", 2, 16, 88, 16)
     random_ops(21, shape, 120, M.PATH_FUSED | M.XFER_ASYNC, n_hbm=40, n_dram=8,
                copy_kernel=copy_kernel)
+
+
+# The NVLink dispatch on one GPU: force_peer makes same-GPU pools take the
+# peer path (one-sided stores from the sender's stream through the peer slab
+# table, the pool's peer engine and split), the path two pools on two GPUs
+# take; every engine x split combination against the oracle.
+PEER_ENGINES = {"vector-static": dict(peer_engine=1, peer_sched=1),
+                "vector-dynamic": dict(peer_engine=1, peer_sched=2),
+                "bulk-static": dict(peer_engine=2, peer_sched=1),
+                "bulk-dynamic": dict(peer_engine=2, peer_sched=2)}
+
+
+@pytest.mark.parametrize("engine", list(PEER_ENGINES))
+@pytest.mark.parametrize("path", [M.PATH_FUSED, M.PATH_FUSED | M.XFER_ASYNC])
+def test_random_ops_peer_dispatch(engine, path):
+    for seed in range(2):
+        random_ops(600 + seed, TINY, 300, path, force_peer=True, **PEER_ENGINES[engine])
+
+
+@pytest.mark.parametrize("engine", list(PEER_ENGINES))
+def test_multi_piece_chunks_peer_dispatch(engine):
+    # 45056 B chunks: 2.75 bulk pieces / 11 vector units per chunk
+    shape = KVShape("mp", 2, 16, 88, 16)
+    random_ops(31, shape, 120, M.PATH_FUSED | M.XFER_ASYNC, n_hbm=40, n_dram=8,
+               force_peer=True, **PEER_ENGINES[engine])
+
+
+def test_random_ops_staged_async_small_ring():
+    """STAGED without a host wait: 2 slots of 2 blocks, so one transfer wraps
+    the ring and consecutive transfers reuse slots still being unpacked."""
+    for seed in range(2):
+        random_ops(700 + seed, TINY, 300, M.PATH_STAGED | M.XFER_ASYNC,
+                   staging_bytes=4 * TINY.block_bytes, staging_slots=2)
 
 
 def test_pack_unpack_np_take():
