@@ -100,7 +100,6 @@ typedef enum {
 #define MP_XFER_PATH_FUSED (1u << MP_XFER_PATH_SHIFT)  /* one gather->store kernel, no staging (A6f) */
 #define MP_XFER_PATH_STAGED (2u << MP_XFER_PATH_SHIFT) /* pack -> copy -> unpack (A4, A5, A6) */
 #define MP_XFER_PATH_CE (3u << MP_XFER_PATH_SHIFT)     /* copy engines, one memcpy per chunk (library baseline) */
-#define MP_XFER_PATH_CE_BATCH (4u << MP_XFER_PATH_SHIFT) /* one cudaMemcpyBatchAsync of all chunks (library baseline) */
 /* Swap transport (mp_swap_out / mp_swap_in flags).  Default (0): MP_SWAP_CE
  * when the pool's staging buffer holds at least one block, else zero-copy. */
 #define MP_SWAP_ZERO_COPY (1u << 0) /* SM loads/stores straight to mapped pinned DRAM */
@@ -359,8 +358,12 @@ mp_status mp_export_handle(mp_pool* pool, void* buf, int64_t cap, int64_t* len);
  * dst_instance: the caller's process sends the request, the peer's process
  * executes the receiver's half of the workflow (allocation, insertion;
  * P:361-365) inside mp_serve -- or inside any of its own blocking transfer
- * calls -- and the caller's fused kernel stores the blocks one-sided into
- * the peer's IPC-mapped slabs (FUSED path only).  Shapes must match. */
+ * calls -- and the caller's process moves the blocks one-sided into the
+ * peer's IPC-mapped memory with any transport: FUSED (one kernel storing
+ * into the peer's slabs; engine and split from peer_engine / peer_sched),
+ * CE (one copy-engine memcpy per chunk) or STAGED (pack, one copy per slot
+ * into the peer's IPC-exported inbound ring, unpacked by the peer's recv
+ * stream; slots handed over by device-side flags).  Shapes must match. */
 mp_status mp_import_peer(mp_pool* pool, const void* buf, int64_t len);
 /* Receiver loop: serve requests of imported peers until an end-of-batch
  * mark arrives (until_mark != 0) or timeout_ms elapses (< 0: no timeout;

@@ -191,32 +191,14 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
     src->stats.blocks_moved += (uint64_t)n;
     return link(src, dst);
   }
-  if (path == MP_XFER_PATH_CE || path == MP_XFER_PATH_CE_BATCH) {
+  if (path == MP_XFER_PATH_CE) {
     TRY(link(dst, src));
     DevGuard g(src->dev);
-    if (path == MP_XFER_PATH_CE) {
-      for (int64_t i = 0; i < n; ++i)
-        for (int j = j0; j < j0 + nj; ++j)
-          CK(cudaMemcpyAsync(dst->slabs[(size_t)j] + (int64_t)dids[(size_t)i] * dst->chunk,
-                             src->slabs[(size_t)j] + (int64_t)sids[(size_t)i] * src->chunk,
-                             (size_t)src->chunk, cudaMemcpyDefault, src->stream));
-    } else {
-      // one cudaMemcpyBatchAsync of all n * nj chunk copies (library baseline)
-      std::vector<void*> ds, ss;
-      std::vector<size_t> sz((size_t)(n * nj), (size_t)src->chunk);
-      ds.reserve(sz.size());
-      ss.reserve(sz.size());
-      for (int64_t i = 0; i < n; ++i)
-        for (int j = j0; j < j0 + nj; ++j) {
-          ds.push_back(dst->slabs[(size_t)j] + (int64_t)dids[(size_t)i] * dst->chunk);
-          ss.push_back(src->slabs[(size_t)j] + (int64_t)sids[(size_t)i] * src->chunk);
-        }
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t attr_idx = 0, fail = 0;
-      CK(cudaMemcpyBatchAsync(ds.data(), ss.data(), sz.data(), sz.size(), &attr, &attr_idx, 1,
-                              &fail, src->stream));
-    }
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = j0; j < j0 + nj; ++j)
+        CK(cudaMemcpyAsync(dst->slabs[(size_t)j] + (int64_t)dids[(size_t)i] * dst->chunk,
+                           src->slabs[(size_t)j] + (int64_t)sids[(size_t)i] * src->chunk,
+                           (size_t)src->chunk, cudaMemcpyDefault, src->stream));
     track_fence(src->track);  // copies the launch window knows nothing about
     src->stats.bytes_moved += (uint64_t)(n * nj * src->chunk);
     src->stats.blocks_moved += (uint64_t)n;
@@ -461,7 +443,6 @@ mp_status transmit_precheck(mp_pool* src, mp_pool* dst, uint32_t path, int nj,
     case MP_XFER_PATH_AUTO:
     case MP_XFER_PATH_FUSED:
     case MP_XFER_PATH_CE:
-    case MP_XFER_PATH_CE_BATCH:
       return MP_OK;
     case MP_XFER_PATH_STAGED: {
       bool any_hbm = false;  // DRAM sources take the direct DRAM kernel, not the ring

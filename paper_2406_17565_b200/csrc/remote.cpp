@@ -13,14 +13,14 @@
 //    pair of pools (request slot + reply slot, sequence numbers with
 //    acquire/release ordering) -- both processes are on the same 8-GPU box;
 //  * the receiver's slabs are CUDA-IPC mapped into the sender, and the
-//    transmission is one-sided, on the sender's GPU, in one of four
+//    transmission is one-sided, on the sender's GPU, in one of three
 //    transports (remote_transmit): FUSED -- one gather -> peer-store kernel
 //    writing the scattered source chunks straight into the receiver's fresh
 //    blocks over NVLink (no staging, no per-block calls, no ordering thread;
-//    the paper's NCCL send/recv needs one per communicator); CE /
-//    CE_BATCH -- copy-engine memcpys per chunk; STAGED -- pack, one
-//    copy-engine copy per slot into the receiver's inbound ring, unpack by
-//    the receiver, pipelined by device-side flags;
+//    the paper's NCCL send/recv needs one per communicator); CE --
+//    one copy-engine memcpy per chunk; STAGED -- pack, one copy-engine copy
+//    per slot into the receiver's inbound ring, unpack by the receiver,
+//    pipelined by device-side flags;
 //  * the two processes' streams are ordered with interprocess CUDA events
 //    (the sender's copy waits for the receiver's allocation; the receiver's
 //    later work waits for a completed copy) and, where a wait must be
@@ -595,7 +595,6 @@ namespace {
 //             pool's peer_engine / peer_sched)
 //   CE        one copy-engine memcpy per (block, layer, K/V) chunk (the
 //             paper's discrete per-block transfer)
-//   CE_BATCH  one cudaMemcpyBatchAsync of all the chunks
 //   STAGED    pack into a staging slot (A4, the paper's aggregation
 //             P:549-550), one copy-engine memcpy of the slot into the
 //             receiver's inbound ring (A5), unpack there (A6) -- pipelined
@@ -625,26 +624,12 @@ mp_status remote_transmit(mp_pool* src, RemotePeer* r, uint32_t path, int j0, in
     TRY(launch_migrate_timed(src, src->stream, pool_ep(src->d_slabs, d_s),
                              pool_ep(r->d_slabs, d_d), n, j0, nj, /*peer=*/!r->same_device, 0,
                              si.n ? &si : nullptr, /*meta_dep=*/!both, &lb));
-  } else if (n > 0 && (path == MP_XFER_PATH_CE || path == MP_XFER_PATH_CE_BATCH)) {
-    std::vector<void*> dps, sps;
-    dps.reserve((size_t)(n * nj));
-    sps.reserve((size_t)(n * nj));
+  } else if (n > 0 && path == MP_XFER_PATH_CE) {
     for (int64_t i = 0; i < n; ++i)
-      for (int j = j0; j < j0 + nj; ++j) {
-        dps.push_back(r->slabs_h[(size_t)j] + (int64_t)hd[(size_t)i] * src->chunk);
-        sps.push_back(src->slabs[(size_t)j] + (int64_t)hs[(size_t)i] * src->chunk);
-      }
-    if (path == MP_XFER_PATH_CE) {
-      for (size_t i = 0; i < dps.size(); ++i)
-        CK(cudaMemcpyAsync(dps[i], sps[i], (size_t)src->chunk, cudaMemcpyDefault, src->stream));
-    } else {
-      std::vector<size_t> sz(dps.size(), (size_t)src->chunk);
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t attr_idx = 0, fail = 0;
-      CK(cudaMemcpyBatchAsync(dps.data(), sps.data(), sz.data(), sz.size(), &attr, &attr_idx, 1,
-                              &fail, src->stream));
-    }
+      for (int j = j0; j < j0 + nj; ++j)
+        CK(cudaMemcpyAsync(r->slabs_h[(size_t)j] + (int64_t)hd[(size_t)i] * src->chunk,
+                           src->slabs[(size_t)j] + (int64_t)hs[(size_t)i] * src->chunk,
+                           (size_t)src->chunk, cudaMemcpyDefault, src->stream));
     track_fence(src->track);
     src->stats.bytes_moved += (uint64_t)(n * nj * src->chunk);
   } else if (n > 0 && staged) {
@@ -697,7 +682,7 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
                           int64_t priv_len, int64_t* n_moved) {
   const uint32_t path = flags & MP_XFER_PATH_MASK;
   if (path != MP_XFER_PATH_AUTO && path != MP_XFER_PATH_FUSED && path != MP_XFER_PATH_STAGED &&
-      path != MP_XFER_PATH_CE && path != MP_XFER_PATH_CE_BATCH) {
+      path != MP_XFER_PATH_CE) {
     set_err("unknown transfer path");
     return MP_ERR_CONFIG;
   }

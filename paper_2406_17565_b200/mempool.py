@@ -29,7 +29,6 @@ PATH_AUTO = 0 << 8
 PATH_FUSED = 1 << 8
 PATH_STAGED = 2 << 8
 PATH_CE = 3 << 8
-PATH_CE_BATCH = 4 << 8
 SWAP_ZERO_COPY = 1
 SWAP_CE = 2
 

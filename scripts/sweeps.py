@@ -46,8 +46,7 @@ def transfer_sweep():
            "results": []}
     seed = seed_for(1)
     engines = [("fused_vector", M.PATH_FUSED, 1), ("fused_bulk", M.PATH_FUSED, 2),
-               ("staged_bulk", M.PATH_STAGED, 2), ("ce_per_chunk", M.PATH_CE, 1),
-               ("ce_batch", M.PATH_CE_BATCH, 1)]
+               ("staged_bulk", M.PATH_STAGED, 2), ("ce_per_chunk", M.PATH_CE, 1)]
     for name, path, ck in engines:
         P = pool(0, 2048, copy_kernel=ck, coalesce_mib=-1, staging_bytes=1 << 30)
         D = pool(1, 1024, copy_kernel=ck, coalesce_mib=-1, staging_bytes=1 << 30)

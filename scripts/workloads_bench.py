@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-from bench import Clocks, load_peaks, make_pool  # noqa: E402
+from bench import Clocks, cupti_busy, load_peaks, make_pool  # noqa: E402
 from paper_2406_17565_b200 import mempool as M  # noqa: E402
 from workloads import traces  # noqa: E402
 from workloads.configs import LLAMA2_13B, seed_for  # noqa: E402
@@ -133,10 +133,11 @@ def react_steps(P, D, sess):
         k = len(t.prompt) // B
         D.free_mem(fin_d[k:])                                 # the prompt's partial block
         d_addrs = prefill(D, whole)                           # decode appends blocks
-        _, nm2 = D.transfer_with_insert(P.inst, whole, d_addrs[k:], flags=M.XFER_ASYNC)
+        fin_p, nm2 = D.transfer_with_insert(P.inst, whole, d_addrs[k:], flags=M.XFER_ASYNC)
         moved += nm2
         DIR["d2p_moved"] += nm2
         D.free_mem(d_addrs[len(whole) // B:])
+        P.free_mem(fin_p[len(whole) // B:])                   # P's copy of whole's partial
         P.free_mem(src[k:])
         retire.append(whole)
         yield moved
@@ -183,6 +184,8 @@ def main():
                     help="time every k-th migration launch (1: all; events cost a few us each)")
     ap.add_argument("--no-profile", action="store_true",
                     help="no per-launch timing events (kernel shares are then unavailable)")
+    ap.add_argument("--cupti-sessions", type=int, default=8,
+                    help="sessions of the untimed CUPTI pass (0: skip)")
     ap.add_argument("--concurrent", type=int, default=1,
                     help="react: sessions in flight, interleaved turn by turn")
     ap.add_argument("--coalesce-mib", type=int, default=0,
@@ -244,6 +247,7 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     st = [x.stats() for x in (P, D)]
+    dirs = dict(DIR)             # the timed region's counts (later passes add to DIR)
     turn_lat = None
     if args.workload == "loogle":
         # device time of each turn's transfer (untimed pass after the region,
@@ -264,6 +268,31 @@ def main():
                     "turns2to5_blocks_moved_p50": float(np.median(nrest)),
                     "sessions": 4}
         TURN_EV = None
+    # CUPTI pass (untimed, no events around launches): the migration kernels'
+    # busy time (union of their intervals) and the HBM rate while busy
+    cupti = None
+    if args.cupti_sessions > 0:
+        from torch.profiler import ProfilerActivity, profile
+        for x in (P, D):
+            x.sync()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            c0.record()
+            cm = sum(fn(P, D, s) for s in sessions[: args.cupti_sessions])
+            for x in (P, D):
+                x.sync()
+            c1.record()
+            torch.cuda.synchronize()
+        nl, tot, busy = cupti_busy(prof)
+        pms = c0.elapsed_time(c1)
+        cab = 2 * cm * S.block_bytes / (busy * 1e-6) / 1e9 if busy else None
+        cupti = {"sessions": args.cupti_sessions, "launches": nl,
+                 "avg_launch_us": round(tot / nl, 3) if nl else None,
+                 "busy_ms": round(busy / 1e3, 3), "pass_ms": round(pms, 3),
+                 "share_of_time": round(busy / 1e3 / pms, 4) if pms else None,
+                 "achieved_over_busy_GBps": round(cab, 1) if cab else None,
+                 "what": "CUPTI records (torch.profiler) of the migration kernels over an untimed "
+                         "pass; achieved = 2 x payload / union of the kernels' intervals"}
     # sampled launches stand for every profiled one (per pool; ratio
     # estimator: kernel time per byte of the sampled launches x all bytes)
     kms = sum(s["kernel_ms"] * s["profiled_bytes"] / s["timed_bytes"]
@@ -271,6 +300,8 @@ def main():
     kl = sum(s["profiled_launches"] for s in st)
     kb = sum(s["profiled_bytes"] for s in st)
     peak, src = load_peaks()
+    if cupti and cupti["achieved_over_busy_GBps"]:
+        cupti["frac_over_busy"] = round(cupti["achieved_over_busy_GBps"] / peak, 4)
     ach = 2 * kb / (kms * 1e-3) / 1e9 if kms else None
     print(json.dumps({
         "metric": "KV migration GB/s (payload, both directions)",
@@ -284,11 +315,12 @@ def main():
                      "launches": kl, "share_of_time": round(kms / ms, 4),
                      "timed_every": args.profile_every,
                      "host_ms": round(host_ms, 3)},
+        "cupti": cupti,
         "turn_latency": turn_lat,
-        "directions": ({"p_to_d_blocks_sent": DIR["p2d_sent"],
-                        "p_to_d_blocks_moved": DIR["p2d_moved"],
-                        "p_to_d_blocks_avoided_by_dedup": DIR["p2d_sent"] - DIR["p2d_moved"],
-                        "d_to_p_blocks_moved": DIR["d2p_moved"]}
+        "directions": ({"p_to_d_blocks_sent": dirs["p2d_sent"],
+                        "p_to_d_blocks_moved": dirs["p2d_moved"],
+                        "p_to_d_blocks_avoided_by_dedup": dirs["p2d_sent"] - dirs["p2d_moved"],
+                        "d_to_p_blocks_moved": dirs["d2p_moved"]}
                        if args.workload == "react" else None),
         "engine_alloc": "drain" if args.drain_alloc else "stream_ordered",
         "sessions_retained": RETAIN,

@@ -27,7 +27,6 @@ modes = [
     ("fused_bulk_async", M.PATH_FUSED | M.XFER_ASYNC, {"copy_kernel": 2}),
     ("staged", M.PATH_STAGED, {}),
     ("ce", M.PATH_CE, {}),
-    ("ce_batch_swapce", M.PATH_CE_BATCH, {"swap_flags": M.SWAP_CE}),
     ("fused_swap_zerocopy", M.PATH_FUSED, {"swap_flags": M.SWAP_ZERO_COPY}),
 ]
 # chunk shapes: tiny (4 KiB), ragged (1152 B: predicated tails), multi-piece

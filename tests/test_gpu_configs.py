@@ -148,3 +148,112 @@ def test_config4_swap_sweep_7b():
         assert len(back) == len(moved)
     S.check_state(sample=32, rng=rng)
     _close(S)
+
+
+def test_config2_loogle_13b_32k_document_one_launch():
+    """configs[2]'s long end: a 32768-token document is 2048 blocks (25 GiB
+    at 13B) moved by ONE transfer_with_insert launch, then a question turn
+    moves only its new blocks (DEDUP).  The prefix-tuple oracle is
+    quadratic in the document, so the checks are closed forms and the plain
+    definition instead: (1) the receiver starts empty, so its ids are the
+    lowest-first 0..n-1 (S:128) and match(document) returns exactly them;
+    (2) every byte of every destination block equals its source block
+    (device compare, torch indexing of both pools' slabs: dst[d_j] = src[s_j]);
+    (3) 64 sampled blocks equal the seeded content generator's words for
+    (instance 0, epoch 1, source block) -- the same tags the oracle's fill
+    gives (workloads/kvgen.py)."""
+    import torch
+    from workloads import kvgen
+    shape, seed = LLAMA2_13B, seed_for(2)
+    B, L2, c = shape.block_tokens, 2 * shape.layers, shape.chunk_bytes
+    nb = 2100
+    regions, pools = [], []
+    for inst in (0, 1):
+        r = torch.empty(L2 * nb * c, dtype=torch.uint8, device="cuda:0")
+        regions.append(r)
+        pools.append(M.Pool(inst, 0, shape.layers, shape.kv_heads, shape.head_dim, B, nb,
+                            slabs=[r.data_ptr() + j * nb * c for j in range(L2)]))
+    P, D = pools
+    M.connect(P, D)
+    rng = np.random.default_rng(seed)
+    doc = rng.integers(3, 32000, size=32768, dtype=np.int32)
+    n = len(doc) // B
+    src = P.alloc_mem(n)
+    P.debug_fill(src, seed)                      # epoch 1 of instance 0
+    P.insert(doc, src)
+    P.sync()
+    P.stats_reset()
+    D.stats_reset()
+    fin, moved = P.transfer_with_insert(1, doc, src, flags=M.XFER_DEDUP | ASYNC)
+    P.sync()
+    D.sync()
+    launches = P.stats()["kernel_launches"] + D.stats()["kernel_launches"]
+    assert moved == n and launches == 1, (moved, launches)
+    assert M.addr_indices(fin).tolist() == list(range(n))
+    _, m = D.match(doc)
+    assert M.addr_indices(m).tolist() == list(range(n))
+    P.sync()
+    D.sync()
+    sv = regions[0].view(L2, nb, c)
+    dv = regions[1].view(L2, nb, c)
+    s_ids = torch.as_tensor(M.addr_indices(src).astype(np.int64), device="cuda:0")
+    d_ids = torch.as_tensor(M.addr_indices(fin).astype(np.int64), device="cuda:0")
+    for j in range(L2):                          # all 25 GiB, one slab at a time
+        assert bool((sv[j][s_ids] == dv[j][d_ids]).all()), j
+    W = c // 8
+    for k in rng.choice(n, 64, replace=False).tolist() + [0, n - 1]:
+        tag = kvgen.make_tag(0, 1, int(M.addr_indices(src)[k]))
+        want = kvgen.block_words(seed, [tag] * L2, W)
+        got = D.debug_read_block(fin[k]).view(np.uint64).reshape(L2, W)
+        assert np.array_equal(got, want), k
+    # a question turn: only the new blocks move
+    q = np.concatenate([doc, rng.integers(3, 32000, size=300, dtype=np.int32)])
+    _, pm = P.match(q)
+    new = P.alloc_mem(-(-len(q) // B) - len(pm))
+    P.debug_fill(new, seed)
+    fin2, moved2 = P.transfer_with_insert(1, q, np.concatenate([pm, new]),
+                                          flags=M.XFER_DEDUP | ASYNC)
+    assert moved2 == len(new) == -(-300 // B)
+    assert M.addr_indices(fin2[:n]).tolist() == list(range(n))
+    D.sync()
+    P.close()
+    D.close()
+    del regions
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_config1_staged_7b_fullsize_64k_geometry():
+    """The STAGED transport (pack -> copy -> unpack, A4-A6) at configs[1]'s
+    full size with 1 GiB staging slots (128 blocks of 8 MiB), so pack and
+    unpack run the large-launch bulk geometry (64 KiB x 3 stages) -- every
+    result, the index, states, bitmap and sampled bytes against the oracle."""
+    shape, seed = LLAMA2_7B, seed_for(1)
+    B = shape.block_tokens
+    kw = dict(staging_bytes=4 << 30, staging_slots=4)
+    P = Twin(0, shape, 4096, seed=seed, **kw)
+    D = Twin(1, shape, 4096, seed=seed, **kw)
+    connect(P, D)
+    rng = np.random.default_rng(seed + 5)
+    sessions = traces.sharegpt_like(seed, n_sessions=40)
+    reqs = []
+    for s in sessions:
+        for t in s.turns:
+            full = prefill(P, t.prompt, B)
+            reqs.append((t.prompt, full[len(t.prompt) // B:]))
+        if 4096 - P.o.free_count(O.HBM) > 2500:
+            break
+    # one long request too: a 300-block prompt spans three slots (ring wraps)
+    long = rng.integers(3, 32000, size=300 * B + 5, dtype=np.int32)
+    full = prefill(P, long, B)
+    reqs.append((long, full[len(long) // B:]))
+    finals = []
+    for prompt, partial in reqs:
+        _, matched = P.match(prompt)
+        final, moved, _ = transfer_with_insert(P, D, prompt, matched + partial,
+                                               oflags=O.FLAG_DEDUP,
+                                               path=M.PATH_STAGED | M.XFER_ASYNC)
+        finals.append((prompt, final))
+    D.check_state(sample=64, rng=rng)
+    P.check_state(sample=16, rng=rng)
+    _close(P, D)

@@ -27,7 +27,7 @@ TRANSPORTS = {
                            "PATH_FUSED"),
     # 2 slots of 2 tiny blocks: the ring wraps inside one transfer
     "ce-staged": ({"staging_bytes": 4 * TINY_BLOCK, "staging_slots": 2}, "PATH_STAGED"),
-    "ce-batch": ({}, "PATH_CE_BATCH"),
+    "ce-per-chunk": ({}, "PATH_CE"),
 }
 
 
@@ -228,14 +228,11 @@ def _stress(rank, port, q, transport="fused-loopback"):
         q.put((rank, {"error": traceback.format_exc() + repr(e)}))
 
 
-@pytest.mark.parametrize("transport", ["fused-loopback", "fused-vector-static",
-                                       "fused-bulk-dynamic", "ce-staged", "ce-batch"])
+@pytest.mark.parametrize("transport", list(TRANSPORTS))
 def test_two_process_back_to_back_async(transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 30300 + (os.getpid() % 40) + 50 * ["fused-loopback", "fused-vector-static",
-                                              "fused-bulk-dynamic", "ce-staged",
-                                              "ce-batch"].index(transport)
+    port = 30300 + (os.getpid() % 40) + 50 * list(TRANSPORTS).index(transport)
     ps = [ctx.Process(target=_stress, args=(r, port, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
@@ -558,7 +555,7 @@ def _rand_oracle(seed):
 @pytest.mark.parametrize("seed,transport", [(3, "fused-loopback"), (11, "fused-loopback"),
                                             (29, "fused-loopback"), (5, "fused-vector-static"),
                                             (7, "fused-bulk-dynamic"), (13, "ce-staged"),
-                                            (17, "ce-batch")])
+                                            (17, "ce-per-chunk")])
 def test_two_process_random_ops(seed, transport):
     import oracle as O
     ctx = mp.get_context("spawn")
@@ -589,3 +586,176 @@ def test_two_process_random_ops(seed, transport):
                 assert np.array_equal(b, pool_o.block_bytes((r, med, i))), (r, med, i)
                 n += 1
         assert n > 0
+
+
+# ---------------------------------------------------------------------------
+# Cross-process ReAct (configs[3] shape of work, PD-Caching-3) at
+# tiny size, against the oracle: per turn P -> D transfer_with_insert with
+# DEDUP of the prompt, D appends the generated blocks (engine stand-in fills
+# them), D -> P suffix transfer_with_insert from block floor(prompt/B) (R3);
+# both sides free their partial blocks, sessions end with deletes.  Lockstep
+# (end-of-step marks both ways) so the oracle can replay the same order.
+def _react_sessions(seed, n_sessions=4):
+    rng = np.random.default_rng(seed)
+    tok = lambda n: rng.integers(3, 40, size=n).astype(np.int32)  # noqa: E731
+    shared = tok(40)
+    out = []
+    for _ in range(n_sessions):
+        prompt = np.concatenate([shared, tok(int(rng.integers(3, 20)))])
+        turns = []
+        for _ in range(int(rng.integers(2, 4))):
+            gen = tok(int(rng.integers(5, 40)))
+            turns.append((prompt, gen))
+            prompt = np.concatenate([prompt, gen, tok(int(rng.integers(3, 20)))])
+        out.append(turns)
+    return out
+
+
+def _react_worker(rank, port, seed, q, transport):
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import TINY as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        kw, pname = TRANSPORTS[transport]
+        path = getattr(M, pname)
+        pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, 96,
+                      verify=True, **kw)
+        blobs = M.exchange_handles(pool)
+        pool.import_peer(blobs[1 - rank][1])
+        dist.barrier()
+        B, other = S.block_tokens, 1 - rank
+        res, step = [], 0
+
+        def prefill(t):
+            _, m = pool.match(t)
+            new = pool.alloc_mem(-(-len(t) // B) - len(m))
+            if len(new):
+                pool.debug_fill(new, 17565)
+            full = np.concatenate([m, new])
+            pool.insert(t, full[: len(t) // B])
+            return full
+
+        def poll():
+            m = pool.recv_poll()
+            assert m is not None and pool.recv_poll() is None
+            return m[3]
+
+        for turns in _react_sessions(seed):
+            for prompt, gen in turns:
+                whole = np.concatenate([prompt, gen])
+                k = len(prompt) // B
+                if rank == 0:
+                    src = prefill(prompt)
+                    fin, nm = pool.transfer_with_insert(1, prompt, src,
+                                                        flags=M.XFER_DEDUP | M.XFER_ASYNC | path)
+                    res.append(("p2d", M.addr_indices(fin).tolist(), nm))
+                    pool.send_mark(1, step)
+                    _s, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+                    assert mark == step + 1, (mark, step)
+                    back = poll()
+                    res.append(("d2p_final", M.addr_indices(back).tolist()))
+                    pool.free_mem(back[len(whole) // B:])
+                    pool.free_mem(src[k:])
+                else:
+                    _s, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+                    assert mark == step, (mark, step)
+                    fin = poll()
+                    pool.free_mem(fin[k:])
+                    d = prefill(whole)
+                    _, nm = pool.transfer_with_insert(0, whole, d[k:], flags=M.XFER_ASYNC | path)
+                    res.append(("d2p", nm))
+                    pool.free_mem(d[len(whole) // B:])
+                    pool.send_mark(0, step + 1)
+                step += 2
+            for prompt, gen in turns:
+                pool.delete(np.concatenate([prompt, gen]))
+            dist.barrier()
+        pool.sync()
+        out = {"res": res, "dump": pool.dump_index(), "states": pool.block_states(M.HBM).tolist()}
+        out["bytes"] = {i: pool.debug_read_block(M.make_addr(rank, M.HBM, i))
+                        for i, s in enumerate(out["states"]) if s != 0}
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+def _react_oracle(seed):
+    import oracle as O
+    from workloads.configs import TINY as S
+    B = S.block_tokens
+    mk = lambda inst: O.OraclePool(inst, S.layers, S.kv_heads, S.head_dim, B, 96,  # noqa: E731
+                                   seed=17565)
+    P, D = mk(0), mk(1)
+    res = {0: [], 1: []}
+
+    def prefill(X, t):
+        _, m = X.match(t)
+        new = X.alloc_mem(-(-len(t) // B) - len(m), O.HBM)
+        if new:
+            X.fill(new)
+        full = list(m) + new
+        X.insert(t, full[: len(t) // B])
+        return full
+
+    for turns in _react_sessions(seed):
+        for prompt, gen in turns:
+            whole = np.concatenate([prompt, gen])
+            k = len(prompt) // B
+            src = prefill(P, prompt)
+            fin, nm, _ = O.transfer_with_insert(P, D, prompt, src, flags=O.FLAG_DEDUP)
+            res[0].append(("p2d", [a[2] for a in fin], nm))
+            D.free_mem(fin[k:])
+            d = prefill(D, whole)
+            back, nm2, _ = O.transfer_with_insert(D, P, whole, d[k:], flags=0)
+            res[1].append(("d2p", nm2))
+            D.free_mem(d[len(whole) // B:])
+            res[0].append(("d2p_final", [a[2] for a in back]))
+            P.free_mem(back[len(whole) // B:])
+            P.free_mem(src[k:])
+        for prompt, gen in turns:
+            w = np.concatenate([prompt, gen])
+            P.delete(w)
+            D.delete(w)
+    return P, D, res
+
+
+@pytest.mark.parametrize("seed,transport", [(41, "fused-loopback"), (43, "fused-vector-static"),
+                                            (47, "ce-staged"), (53, "ce-per-chunk")])
+def test_two_process_react_vs_oracle(seed, transport):
+    import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30700 + (os.getpid() % 20) + seed
+    ps = [ctx.Process(target=_react_worker, args=(r, port, seed, q, transport))
+          for r in range(2)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in ps:
+        r, out = q.get(timeout=600)
+        got[r] = out
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in got[r], got[r].get("error")
+    P, D, res = _react_oracle(seed)
+    smap = {O.FREE: 0, O.ACTIVE: 1, O.INDEXED: 2, O.ORPHAN: 3}
+    for pool_o, r in ((P, 0), (D, 1)):
+        assert got[r]["res"] == res[r], r
+        assert got[r]["dump"] == pool_o.dump_index(), r
+        assert got[r]["states"] == [smap[x] for x in pool_o.state[O.HBM]], r
+        n = 0
+        for i, b in got[r]["bytes"].items():
+            if all(t is not None for t in pool_o.tags[O.HBM][i]):
+                assert np.array_equal(b, pool_o.block_bytes((r, O.HBM, i))), (r, i)
+                n += 1
+        assert n > 0, r

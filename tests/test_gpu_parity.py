@@ -247,12 +247,12 @@ def test_random_ops_three_pools_coalesced(path, monkeypatch):
         random_ops(500 + seed, TINY, 400, path, coalesce_mib=1, n_pools=3)
 
 
-def test_random_ops_ce_batch_and_swap_ce():
-    """The library baselines: one cudaMemcpyBatchAsync per transfer, and swap
+def test_random_ops_ce_and_swap_ce():
+    """The library baselines: one copy-engine memcpy per chunk, and swap
     through device staging + copy-engine D2H/H2D (small staging: 2 blocks per
     round so multi-round swaps are exercised)."""
     for seed in range(2):
-        random_ops(400 + seed, TINY, 300, M.PATH_CE_BATCH, swap_flags=M.SWAP_CE,
+        random_ops(400 + seed, TINY, 300, M.PATH_CE, swap_flags=M.SWAP_CE,
                    staging_bytes=2 * TINY.block_bytes)
 
 
