@@ -471,6 +471,12 @@ def run_ours(args, rank, world, dist):
             cupti = {"error": str(e)[:300]}
         if rank == 0:
             roof["cupti"] = cupti
+            if cupti and cupti.get("share_of_step") is not None:
+                # the step's kernel share from un-bracketed (CUPTI) durations
+                roof["share_of_step_events"] = roof["share_of_step"]
+                roof["share_of_step"] = cupti["share_of_step"]
+                roof["share_source"] = "cupti (roofline.cupti); share_of_step_events: the " \
+                                       "event-sampled estimate"
     if not args.no_extras and dist is not None and role.kind != "PD":
         try:
             pair_nccl = nccl_pair_point(M, torch, dist, role, P if P is not None else D,

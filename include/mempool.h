@@ -345,15 +345,16 @@ mp_status mp_gs_route(mp_gs* gs, int32_t kind, const mp_token* tokens, int64_t n
 /* ------------------- multi-process (one process per GPU) ----------------- */
 /* Serialize what a pool in ANOTHER process needs to reach this one: CUDA-IPC
  * handles of the slab allocations (slabs must come from cudaMalloc, e.g. the
- * torch caching allocator) and of the id arena, an interprocess event, the
- * shape and a random pool uid (mailbox names).  len receives the size; call
+ * torch caching allocator), the shape, the staging geometry and a random
+ * pool uid (names of the pair's mailboxes and flag pages).  len receives the size; call
  * with buf = NULL to query it.  The blob is plain bytes (exchange it with
  * torch.distributed / any transport). */
 mp_status mp_export_handle(mp_pool* pool, void* buf, int64_t cap, int64_t* len);
 /* Map a peer's exported pool: its slabs and arena are opened with
- * cudaIpcOpenMemHandle (peer access over NVLink when on another GPU), its
- * event with cudaIpcOpenEventHandle, and the two shared-memory mailboxes of
- * the pair are created / opened.  Both sides import each other.  Afterwards
+ * cudaIpcOpenMemHandle (peer access over NVLink when on another GPU), and the
+ * pair's two shared-memory mailboxes and two pinned flag pages (monotonic
+ * sequence numbers that the two GPUs' streams raise and wait on) are
+ * created / opened.  Both sides import each other.  Afterwards
  * mp_transfer / mp_transfer_with_insert accept the peer's instance id as
  * dst_instance: the caller's process sends the request, the peer's process
  * executes the receiver's half of the workflow (allocation, insertion;

@@ -709,7 +709,6 @@ void mp_pool_destroy(mp_pool* p) {
     if (p->staging) cudaFree(p->staging);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
     if (p->ev_meta) cudaEventDestroy(p->ev_meta);
-    if (p->ev_ipc) cudaEventDestroy(p->ev_ipc);
     for (auto e : p->slot_ev) cudaEventDestroy(e);
     for (auto e : p->pack_ev) cudaEventDestroy(e);
     for (auto e : p->swap_ev)
@@ -831,7 +830,6 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
   }
   CKC(cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_meta, cudaEventDisableTiming));
-  CKC(cudaEventCreateWithFlags(&p->ev_ipc, cudaEventDisableTiming | cudaEventInterprocess));
   p->uid = new_uid();
   p->slot_ev.resize((size_t)p->staging_slots);
   for (auto& e : p->slot_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

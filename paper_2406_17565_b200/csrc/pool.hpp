@@ -148,11 +148,16 @@ struct Channel;  // shared-memory mailbox (remote.cpp)
 // device-side flags of one ordered pair of pools (remote.cpp): GPU streams
 // write them with stream memory operations and wait on them with
 // cuStreamWaitValue32, so the two processes' streams synchronise without a
-// host round trip.  Layout (uint32 words): [0] done sequence of one-round-
-// trip (ASYNC) transfers, [kSyncReady + s] STAGED slot s filled, [kSyncFree
-// + s] slot s drained.
+// host round trip.  Layout (uint32 words): [kSyncDone] done sequence of the
+// pair's transfers (raised by the sender's stream after its copies),
+// [kSyncPrep] prepare sequence (raised by the receiver's data stream after
+// the allocation step and every earlier use of the blocks), [kSyncReady + s]
+// STAGED slot s filled, [kSyncFree + s] slot s drained.  Every value only
+// grows, so a wait for ">= v" taken at any time means the same thing -- unlike
+// an interprocess event, whose re-recording by a third party could make a
+// waiter depend on its own future work.
 constexpr int kMaxSyncSlots = 64;
-constexpr int kSyncDone = 0, kSyncReady = 16, kSyncFree = 16 + kMaxSyncSlots;
+constexpr int kSyncDone = 0, kSyncPrep = 1, kSyncReady = 16, kSyncFree = 16 + kMaxSyncSlots;
 struct SyncPage {
   std::string name;
   int fd = -1;
@@ -170,16 +175,16 @@ mp_status stream_write_u32(cudaStream_t s, uint32_t* dptr, uint32_t v);
 mp_status staging_acquire(mp_pool* p, cudaStream_t s);
 
 // A pool living in another process (one process per GPU), imported with
-// mp_import_peer: its slabs and id arena are CUDA-IPC mapped into this
-// process, its interprocess event orders the two processes' streams, and two
-// mailboxes carry the control messages of the workflow.
+// mp_import_peer: its slabs are CUDA-IPC mapped into this process, a pinned
+// shared-memory page of monotonic flags per direction orders the two
+// processes' streams (SyncPage), and two mailboxes carry the control
+// messages of the workflow.
 struct RemotePeer {
   int32_t inst = -1, dev = -1;
   uint64_t uid = 0;
   bool same_device = false;
   std::vector<void*> mapped;      // IPC-opened allocation bases
   char** d_slabs = nullptr;       // the peer's slab pointers, valid on my device
-  cudaEvent_t ev = nullptr;       // the peer's interprocess event
   Channel* out = nullptr;         // me -> peer requests
   Channel* in = nullptr;          // peer -> me requests
   bool has_pending = false;       // peer's transfer between prepare and commit
@@ -205,16 +210,16 @@ struct RemotePeer {
   cudaStream_t recv_stream = nullptr;
   cudaEvent_t recv_dep = nullptr, recv_ev = nullptr;
   bool recv_join = false;         // recv_ev (the last staged inbound's unpacks) not yet joined
-  // one-round-trip ASYNC transfers from the peer (committed at allocation):
-  // their copies have landed once the done flag reaches seq; joined to my
-  // data stream lazily, oldest first: (prepare stamp, seq)
-  uint32_t in_seq = 0;
+  // inbound transfers from the peer whose copies may still run: one-round-
+  // trip ones from their allocation step on, two-round-trip ones from their
+  // completion message on.  Their copies have landed once the done flag
+  // reaches seq; joined to my data stream lazily, oldest first, as
+  // (stamp, seq) -- the stamp bounds which ones a transfer I am issuing may
+  // join (mp_pool::join_bound)
+  uint32_t in_seq = 0;            // receiver side: done sequence numbers handed out
+  uint32_t prep_seq = 0;          // receiver side: prepares served for this peer
+  uint32_t pending_done = 0;      // done sequence of the two-round-trip transfer in `pending`
   std::deque<std::pair<uint64_t, uint32_t>> async_in;
-  // the peer has stored into this pool since this pool's data stream last
-  // waited for the peer's event: the wait is applied lazily, before this
-  // pool's next data-stream work (remote_apply_waits), so consecutive inbound
-  // copies are not chained through the two processes' streams
-  bool inbound_pending = false;
 };
 
 }  // namespace mp
@@ -338,7 +343,6 @@ struct mp_pool {
   bool idle_flush = true;
   // multi-process
   uint64_t uid = 0;                        // random identity (mailbox names)
-  cudaEvent_t ev_ipc = nullptr;            // interprocess event of this pool
   std::map<int32_t, mp::RemotePeer*> remotes;
   std::vector<int32_t> marks;              // end-of-batch marks received (mp_serve)
 };
@@ -450,7 +454,7 @@ mp_status transmit_precheck(mp_pool* src, mp_pool* dst, uint32_t path, int nj,
 // remote.cpp
 uint64_t new_uid();
 // Make p's data stream wait for every peer that stored into p since the last
-// call (see RemotePeer::inbound_pending).  Cheap when nothing is pending.
+// call (RemotePeer::async_in, recv_join).  Cheap when nothing is pending.
 mp_status remote_apply_waits(mp_pool* p);
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
 void remote_close_all(mp_pool* p);

@@ -21,21 +21,26 @@
 //    one copy-engine memcpy per chunk; STAGED -- pack, one copy-engine copy
 //    per slot into the receiver's inbound ring, unpack by the receiver,
 //    pipelined by device-side flags;
-//  * the two processes' streams are ordered with interprocess CUDA events
-//    (the sender's copy waits for the receiver's allocation; the receiver's
-//    later work waits for a completed copy) and, where a wait must be
-//    enqueued before its producer, with flags in a pinned shared-memory page
-//    per ordered pair that GPU streams raise and wait on (SyncPage);
+//  * the two processes' streams are ordered with flags in a pinned
+//    shared-memory page per ordered pair that GPU streams raise
+//    (cuStreamWriteValue32) and wait on (cuStreamWaitValue32) -- SyncPage:
+//    the sender's copy waits for the receiver's prepare flag (allocation
+//    done), the receiver's later work for the sender's done flag (copy
+//    landed), STAGED slots for ready / free flags.  The values only grow, so
+//    a wait means the same whenever it is enqueued (an interprocess event
+//    re-recorded for another sender could make a waiter depend on its own
+//    later copy: the fan-in deadlock this replaced);
 //  * an MP_XFER_ASYNC transfer takes ONE round trip: the receiver allocates,
 //    inserts and delivers `private` when the request arrives (R15: host-side
 //    effects at call time) and joins the sender's copy through the pair's
 //    done flag before its next data-stream work; synchronous transfers keep
 //    the paper's two round trips (the sender completes once the receiver
 //    has the data and answered ok).
-//  Waits across processes never form a cycle: a pool issuing a transfer
-//  joins only inbound one-round-trip transfers prepared before its own
-//  transfer started (mp_pool::join_bound), so every device wait points at
-//  an earlier-started transfer or at an event already recorded.
+//  Waits across processes never form a cycle: a receiver's prepare flag for
+//  transfer t is raised after waits on transfers stamped before t only, and
+//  a pool issuing a transfer joins only inbound transfers stamped before its
+//  own transfer started (mp_pool::join_bound), so every device wait points
+//  at an earlier-started transfer.
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -401,6 +406,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       else
         s = dst_prepare_xfer(p, r->inst, m, flags, given, priv, plen, &r->pending);
       const uint32_t slot0 = r->in_slot;
+      uint32_t prep_seq = 0, done_seq = 0;
       if (s == MP_OK) {
         r->has_pending = true;
         // the sender's copy must follow this allocation and every earlier use
@@ -409,7 +415,10 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         // earlier copies are ordered by its stream already
         s = remote_apply_waits(p);
         if (s == MP_OK) s = meta_fence(p);
-        if (s == MP_OK && cudaEventRecord(p->ev_ipc, p->stream) != cudaSuccess) s = MP_ERR_CUDA;
+        if (s == MP_OK) {
+          prep_seq = ++r->prep_seq;
+          s = stream_write_u32(p->stream, r->in_sync->d + kSyncPrep, prep_seq);
+        }
         if (s == MP_OK && staged) s = staged_recv(p, r, r->pending, meds, j0, nj);
         if (s != MP_OK) {
           dst_abort(p, r->pending);
@@ -417,17 +426,16 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         }
       }
       std::vector<mp_addr> fin;
-      uint32_t done_seq = 0;
+      // every transfer: the sender's stream raises the done flag to this
+      // value after its copies into this pool
+      if (s == MP_OK) done_seq = r->pending_done = ++r->in_seq;
       if (s == MP_OK && one_trip) {
         r->has_pending = false;
         const int64_t nfin = r->pending.kind == 1 ? r->pending.ceil_b : r->pending.nm;
         fin.assign((size_t)std::max<int64_t>(nfin, 1), 0);
         s = dst_commit(p, r->pending, fin.data());
         fin.resize((size_t)nfin);
-        if (s == MP_OK) {
-          done_seq = ++r->in_seq;
-          r->async_in.push_back({++p->prep_stamp, done_seq});
-        }
+        if (s == MP_OK) r->async_in.push_back({++p->prep_stamp, done_seq});
       }
       rtype = REP_PREP;
       rstatus = s;
@@ -435,6 +443,8 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         wr.put<int64_t>(r->pending.skip);
         wr.put<int64_t>(r->pending.nm);
         wr.bytes(r->pending.dids.data(), (int64_t)r->pending.dids.size() * 4);
+        wr.put<uint32_t>(prep_seq);
+        wr.put<uint32_t>(done_seq);
         if (staged) {
           cudaIpcMemHandle_t hnd;
           if (cudaIpcGetMemHandle(&hnd, r->ring) != cudaSuccess) rstatus = MP_ERR_CUDA;
@@ -443,7 +453,6 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
           wr.put<uint32_t>(slot0);
         }
         if (one_trip) {
-          wr.put<uint32_t>(done_seq);
           wr.put<int64_t>((int64_t)fin.size());
           wr.bytes(fin.data(), (int64_t)fin.size() * (int64_t)sizeof(mp_addr));
         }
@@ -483,10 +492,10 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         rstatus = sender_status;
         break;
       }
-      // later data-stream work of this pool must follow the sender's copy:
-      // applied lazily (remote_apply_waits), not chained into the next
-      // allocation the sender waits for
-      r->inbound_pending = true;
+      // later data-stream work of this pool must follow the sender's copy
+      // (its done flag): applied lazily (remote_apply_waits), not chained
+      // into the next allocation the sender waits for
+      r->async_in.push_back({++p->prep_stamp, r->pending_done});
       const int64_t nfin = r->pending.kind == 1 ? r->pending.ceil_b : r->pending.nm;
       std::vector<mp_addr> fin((size_t)std::max<int64_t>(nfin, 1));
       rstatus = dst_commit(p, r->pending, fin.data());
@@ -546,18 +555,14 @@ mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
 mp_status remote_apply_waits(mp_pool* p) {
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
-    if (!r->inbound_pending && !r->recv_join && r->async_in.empty()) continue;
+    if (!r->recv_join && r->async_in.empty()) continue;
     DevGuard g(p->dev);
-    if (r->inbound_pending) {  // a completed two-round-trip transfer (event recorded before DONE)
-      CK(cudaStreamWaitEvent(p->stream, r->ev, 0));
-      r->inbound_pending = false;
-    }
     if (r->recv_join) {  // the unpacks of a completed STAGED transfer
       CK(cudaStreamWaitEvent(p->stream, r->recv_ev, 0));
       r->recv_join = false;
     }
-    // one-round-trip transfers: only those prepared before the transfer this
-    // pool is issuing right now (join_bound), whose senders started earlier
+    // inbound copies: only those stamped before the transfer this pool is
+    // issuing right now (join_bound), whose senders started earlier
     bool any = false;
     uint32_t seq = 0;
     while (!r->async_in.empty() && r->async_in.front().first <= p->join_bound) {
@@ -602,13 +607,14 @@ namespace {
 mp_status remote_transmit(mp_pool* src, RemotePeer* r, uint32_t path, int j0, int nj,
                           const std::vector<int32_t>& hs, const std::vector<int32_t>& hd,
                           const std::vector<int32_t>& ds, const std::vector<int32_t>& dd,
-                          const RingGeom& geom, uint32_t slot0) {
+                          const RingGeom& geom, uint32_t slot0, uint32_t prep_seq) {
   TRY(flush_involving(src));
   const bool staged = path == MP_XFER_PATH_STAGED;
   // stores into the receiver's fresh blocks follow its allocation and every
-  // earlier use of them there (its event, recorded before the reply); the
-  // STAGED ring is ordered by its flags instead
-  if (!staged || !ds.empty()) CK(cudaStreamWaitEvent(src->stream, r->ev, 0));
+  // earlier use of them there (its prepare flag, raised by its data stream
+  // before the reply); the STAGED ring is ordered by its slot flags instead
+  if (!staged || !ds.empty())
+    TRY(stream_wait_geq(src->stream, r->out_sync->d + kSyncPrep, prep_seq));
   const int64_t n = (int64_t)hs.size();
   if (n > 0 && (path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED)) {
     mpk::InlineIds si;
@@ -757,7 +763,9 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   const int32_t* dids = (const int32_t*)rd.bytes(nm * 4);
   cudaIpcMemHandle_t ring_hnd{};
   uint64_t ring_id = 0;
-  uint32_t slot0 = 0, done_seq = 0;
+  uint32_t slot0 = 0;
+  const uint32_t prep_seq = rd.get<uint32_t>();
+  const uint32_t done_seq = rd.get<uint32_t>();
   int64_t nfin = 0;
   const mp_addr* fin = nullptr;
   if (staged) {
@@ -767,7 +775,6 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     slot0 = rd.get<uint32_t>();
   }
   if (one_trip) {
-    done_seq = rd.get<uint32_t>();
     nfin = rd.get<int64_t>();
     fin = (const mp_addr*)rd.bytes(nfin * (int64_t)sizeof(mp_addr));
   }
@@ -805,7 +812,8 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
       }
     }
     src->join_bound = start_stamp;
-    if (xs == MP_OK) xs = remote_transmit(src, r, path, j0, nj, hs, hd, ds_, dd_, geom, slot0);
+    if (xs == MP_OK)
+      xs = remote_transmit(src, r, path, j0, nj, hs, hd, ds_, dd_, geom, slot0, prep_seq);
     src->join_bound = ~0ull;
     if (xs != MP_OK) {
       // release the peer's streams: every flag it waits on is raised from
@@ -815,12 +823,10 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
       cudaGetLastError();
       for (uint32_t q = slot0; q != slot_end; ++q)
         host_raise(r->out_sync->h + kSyncReady + q % (uint32_t)geom.S, q + 1);
-      if (one_trip) host_raise(r->out_sync->h + kSyncDone, done_seq);
-    } else if (one_trip) {
-      xs = stream_write_u32(src->stream, r->out_sync->d + kSyncDone, done_seq);
+      host_raise(r->out_sync->h + kSyncDone, done_seq);
     } else {
-      if (cudaEventRecord(src->ev_ipc, src->stream) != cudaSuccess) xs = MP_ERR_CUDA;
-      if (xs == MP_OK && !(flags & MP_XFER_ASYNC)) xs = sync(src);
+      xs = stream_write_u32(src->stream, r->out_sync->d + kSyncDone, done_seq);
+      if (xs == MP_OK && !one_trip && !(flags & MP_XFER_ASYNC)) xs = sync(src);
     }
     src->stats.blocks_moved += (uint64_t)nm;
   }
@@ -878,7 +884,6 @@ struct WireHandle {
   cudaIpcMemHandle_t allocs[kMaxSlabs];
   int32_t slab_alloc[kMaxSlabs];
   int64_t slab_off[kMaxSlabs];
-  cudaIpcEventHandle_t ev;
 };
 
 typedef int (*GetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
@@ -934,7 +939,6 @@ void remote_close_all(mp_pool* p) {
       for (void* m : r->mapped) cudaIpcCloseMemHandle(m);
       if (r->peer_ring) cudaIpcCloseMemHandle(r->peer_ring);
       if (r->ring) cudaFree(r->ring);
-      if (r->ev) cudaEventDestroy(r->ev);
       if (r->recv_dep) cudaEventDestroy(r->recv_dep);
       if (r->recv_ev) cudaEventDestroy(r->recv_ev);
       if (r->recv_stream) cudaStreamDestroy(r->recv_stream);
@@ -970,7 +974,7 @@ mp_status mp_export_handle(mp_pool* p, void* buf, int64_t cap, int64_t* len) {
   WireHandle* h = new WireHandle();
   std::memset(h, 0, sizeof(*h));
   h->magic = kHandleMagic;
-  h->version = 2;
+  h->version = 3;
   h->inst = p->inst;
   h->dev = p->dev;
   h->L = p->L;
@@ -1011,11 +1015,6 @@ mp_status mp_export_handle(mp_pool* p, void* buf, int64_t cap, int64_t* len) {
     h->slab_off[j] = p->slabs[(size_t)j] - base;
   }
   h->n_allocs = (int32_t)bases.size();
-  if (cudaIpcGetEventHandle(&h->ev, p->ev_ipc) != cudaSuccess) {
-    delete h;
-    set_err("cudaIpcGetEventHandle failed");
-    return MP_ERR_CUDA;
-  }
   std::memcpy(buf, h, sizeof(*h));
   delete h;
   return MP_OK;
@@ -1030,7 +1029,7 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
     delete h;
     return s;
   };
-  if (h->magic != kHandleMagic || h->version != 2) return fail(MP_ERR_CONFIG, "bad handle");
+  if (h->magic != kHandleMagic || h->version != 3) return fail(MP_ERR_CONFIG, "bad handle");
   if (h->inst == p->inst || p->peers.count(h->inst) || p->remotes.count(h->inst))
     return fail(MP_ERR_CONFIG, "instance id already known");
   if (h->L != p->L || h->chunk != p->chunk || h->B != p->B || h->nch != p->nch)
@@ -1056,7 +1055,6 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
   for (int j = 0; ok && j < h->nch; ++j)
     slabs[(size_t)j] = (char*)r->mapped[(size_t)h->slab_alloc[j]] + h->slab_off[j];
   r->slabs_h = slabs;
-  if (ok) ok = cudaIpcOpenEventHandle(&r->ev, h->ev) == cudaSuccess;
   if (ok) ok = cudaMalloc(&r->d_slabs, sizeof(char*) * (size_t)h->nch) == cudaSuccess;
   if (ok)
     ok = cudaMemcpy(r->d_slabs, slabs.data(), sizeof(char*) * (size_t)h->nch,
