@@ -455,7 +455,9 @@ mp_status transmit_precheck(mp_pool* src, mp_pool* dst, uint32_t path, int nj,
 uint64_t new_uid();
 // Make p's data stream wait for every peer that stored into p since the last
 // call (RemotePeer::async_in, recv_join).  Cheap when nothing is pending.
-mp_status remote_apply_waits(mp_pool* p);
+// `skip`: a peer whose one-/two-round-trip inbound copies are NOT joined
+// (its own next copy is ordered behind them by its stream).
+mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip = nullptr);
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
 void remote_close_all(mp_pool* p);
 void host_report_timing();  // MP_HOST_TIMING=1 (api_transfer.cpp)

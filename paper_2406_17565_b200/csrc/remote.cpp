@@ -411,9 +411,12 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         r->has_pending = true;
         // the sender's copy must follow this allocation and every earlier use
         // of the blocks on this pool's streams, including other peers' copies
-        // into them (a block freed and re-allocated); the sender's own
-        // earlier copies are ordered by its stream already
-        s = remote_apply_waits(p);
+        // into them (a block freed and re-allocated) and this peer's STAGED
+        // unpacks (recv_stream); the sender's own earlier FUSED / CE / DRAM
+        // copies are ordered by its stream already, so they are not joined
+        // here -- joining them would chain every copy of a pair behind the
+        // previous one through two flag hops
+        s = remote_apply_waits(p, r);
         if (s == MP_OK) s = meta_fence(p);
         if (s == MP_OK) {
           prep_seq = ++r->prep_seq;
@@ -552,10 +555,10 @@ mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
 
 }  // namespace
 
-mp_status remote_apply_waits(mp_pool* p) {
+mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip) {
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
-    if (!r->recv_join && r->async_in.empty()) continue;
+    if (!r->recv_join && (r->async_in.empty() || r == skip)) continue;
     DevGuard g(p->dev);
     if (r->recv_join) {  // the unpacks of a completed STAGED transfer
       CK(cudaStreamWaitEvent(p->stream, r->recv_ev, 0));
@@ -565,7 +568,7 @@ mp_status remote_apply_waits(mp_pool* p) {
     // issuing right now (join_bound), whose senders started earlier
     bool any = false;
     uint32_t seq = 0;
-    while (!r->async_in.empty() && r->async_in.front().first <= p->join_bound) {
+    while (r != skip && !r->async_in.empty() && r->async_in.front().first <= p->join_bound) {
       seq = r->async_in.front().second;
       r->async_in.pop_front();
       any = true;
