@@ -370,7 +370,7 @@ void stash_priv(DstPrep* st, const void* priv, int64_t priv_len) {
 // ------------------------------------------------- receiver: allocation step
 mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t flags,
                            const mp_addr* given, const void* priv, int64_t priv_len,
-                           DstPrep* st) {
+                           DstPrep* st, bool host_ids) {
   *st = DstPrep{};
   st->kind = 0;
   st->src_inst = src_inst;
@@ -384,14 +384,14 @@ mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t f
   if (!dst_given) {
     DevGuard g(dst->dev);
     if (dst->nfree[MP_HBM] < n) evict_internal(dst, n - dst->nfree[MP_HBM], MP_HBM, nullptr);
-    TRY(alloc_hbm(dst, n, src_inst, &st->dids, &st->d_dst));
+    TRY(alloc_hbm(dst, n, src_inst, &st->dids, &st->d_dst, host_ids));
   }
   return MP_OK;
 }
 
 mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, int64_t n_tok,
                           int64_t m, uint32_t flags, const mp_addr* given, const void* priv,
-                          int64_t priv_len, DstPrep* st) {
+                          int64_t priv_len, DstPrep* st, bool host_ids) {
   *st = DstPrep{};
   st->kind = 1;
   st->src_inst = src_inst;
@@ -432,7 +432,7 @@ mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, 
     DevGuard g(dst->dev);
     if (dst->nfree[MP_HBM] < st->nm)
       evict_internal(dst, st->nm - dst->nfree[MP_HBM], MP_HBM, nullptr);
-    TRY(alloc_hbm(dst, st->nm, src_inst, &st->dids, &st->d_dst));
+    TRY(alloc_hbm(dst, st->nm, src_inst, &st->dids, &st->d_dst, host_ids));
   }
   return MP_OK;
 }

@@ -432,13 +432,17 @@ void unpin_nodes(mp_pool* p, const std::vector<mpi::Node*>& nodes);
 // ---- the receiver's half of the workflow (shared by in-process and remote)
 // (1) allocation: validates everything first (no state change on error),
 // then matches / pins / allocates.  `given`: caller-given destination addrs
-// (MP_XFER_DST_GIVEN) or nullptr.
+// (MP_XFER_DST_GIVEN) or nullptr.  host_ids: the copy takes the destination
+// ids from the host (a remote sender gets them in the reply), so the fresh
+// blocks are claimed in the host shadow and reach the device bitmap with its
+// next stream-ordered update -- no allocation kernel, no device id table
+// (st->d_dst stays null).
 mp_status dst_prepare_xfer(mp_pool* dst, int32_t src_inst, int64_t n, uint32_t flags,
                            const mp_addr* given, const void* priv, int64_t priv_len,
-                           DstPrep* st);
+                           DstPrep* st, bool host_ids = false);
 mp_status dst_prepare_twi(mp_pool* dst, int32_t src_inst, const mp_token* toks, int64_t n_tok,
                           int64_t m, uint32_t flags, const mp_addr* given, const void* priv,
-                          int64_t priv_len, DstPrep* st);
+                          int64_t priv_len, DstPrep* st, bool host_ids = false);
 // (3) insertion + completion: insert (twi), unpin, final addrs, `private`
 // delivery.  final_out: st.ceil_b entries (twi) or st.nm entries (transfer).
 mp_status dst_commit(mp_pool* dst, DstPrep& st, mp_addr* final_out);

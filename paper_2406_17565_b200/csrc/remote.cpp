@@ -402,9 +402,11 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       if (s != MP_OK) {
         // nothing prepared
       } else if (q->type == REQ_TWI)
-        s = dst_prepare_twi(p, r->inst, toks, n_tok, m, flags, given, priv, plen, &r->pending);
+        s = dst_prepare_twi(p, r->inst, toks, n_tok, m, flags, given, priv, plen, &r->pending,
+                            /*host_ids=*/true);
       else
-        s = dst_prepare_xfer(p, r->inst, m, flags, given, priv, plen, &r->pending);
+        s = dst_prepare_xfer(p, r->inst, m, flags, given, priv, plen, &r->pending,
+                             /*host_ids=*/true);
       const uint32_t slot0 = r->in_slot;
       uint32_t prep_seq = 0, done_seq = 0;
       if (s == MP_OK) {
@@ -417,7 +419,8 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         // here -- joining them would chain every copy of a pair behind the
         // previous one through two flag hops
         s = remote_apply_waits(p, r);
-        if (s == MP_OK) s = meta_fence(p);
+        // (no meta fence: with host ids nothing of this allocation runs on
+        // the meta stream, and meta never touches block data)
         if (s == MP_OK) {
           prep_seq = ++r->prep_seq;
           s = stream_write_u32(p->stream, r->in_sync->d + kSyncPrep, prep_seq);
