@@ -594,10 +594,13 @@ def link_probe(torch, dist, role, dev, world, nbytes=1 << 30, reps=8):
 
 def cupti_busy(prof, match="migrate"):
     """(launches, summed duration us, union of the [start, end) intervals us)
-    of the kernels whose name contains `match`, from a torch.profiler run's
-    CUPTI (kineto) activity records -- durations not bracketed by events."""
+    of the device kernels whose name contains `match` (None: every kernel),
+    from a torch.profiler run's CUPTI (kineto) activity records -- durations
+    not bracketed by events."""
+    from torch.autograd import DeviceType
     iv = sorted((ev.time_range.start, ev.time_range.end) for ev in prof.events()
-                if match in ev.name and ev.time_range.end > ev.time_range.start)
+                if ev.device_type == DeviceType.CUDA and (match is None or match in ev.name)
+                and ev.time_range.end > ev.time_range.start)
     if not iv:
         return 0, 0.0, 0.0
     busy, cs, ce = 0.0, iv[0][0], iv[0][1]
@@ -636,8 +639,11 @@ def cupti_share(torch, step, mark_pool, args, first, alg_per_block):
     nl, tot, busy = cupti_busy(prof)
     if not nl:
         return {"error": "no migration kernels in the CUPTI records"}
+    na, tot_all, _ = cupti_busy(prof, None)
     pass_ms = e0.elapsed_time(e1)
     return {"steps": n, "launches": nl, "avg_launch_us": round(tot / nl, 3),
+            "all_kernel_launches": na,
+            "share_of_kernel_time": round(tot / tot_all, 4) if tot_all else None,
             "busy_ms": round(busy / 1e3, 4), "pass_ms": round(pass_ms, 4),
             "share_of_step": round(busy / 1e3 / pass_ms, 4) if pass_ms > 0 else None,
             "payload_blocks": int(moved),

@@ -468,6 +468,50 @@ int sm_count(int device) {
   return v > 0 ? v : 148;
 }
 
+template <int kPieceT, int kStagesT>
+static cudaError_t preload_bulk() {
+  const int smem = kStagesT * kPieceT;
+  void (*ks[4])(Endpoint, Endpoint, int, int, long long, unsigned, unsigned,
+                unsigned long long*, unsigned long long, const InlineIds, int) = {
+      migrate_bulk_kernel<kPieceT, kStagesT, true, true>,
+      migrate_bulk_kernel<kPieceT, kStagesT, true, false>,
+      migrate_bulk_kernel<kPieceT, kStagesT, false, true>,
+      migrate_bulk_kernel<kPieceT, kStagesT, false, false>};
+  for (auto k : ks) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes a;
+    e = cudaFuncGetAttributes(&a, k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t preload_kernels() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::atomic<int> done[64] = {};
+  if (dev < 64 && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+  cudaFuncAttributes a;
+  const void* plain[] = {(const void*)migrate_kernel<true, true>,
+                         (const void*)migrate_kernel<true, false>,
+                         (const void*)migrate_kernel<false, true>,
+                         (const void*)migrate_kernel<false, false>,
+                         (const void*)alloc_kernel, (const void*)free_inline_kernel,
+                         (const void*)free_kernel, (const void*)fill_kernel};
+  for (const void* k : plain)
+    if ((e = cudaFuncGetAttributes(&a, k)) != cudaSuccess) return e;
+  if ((e = preload_bulk<65536, 3>()) != cudaSuccess) return e;
+  if ((e = preload_bulk<32768, 3>()) != cudaSuccess) return e;
+  if ((e = preload_bulk<8192, 6>()) != cudaSuccess) return e;
+  if ((e = preload_bulk<16384, 4>()) != cudaSuccess) return e;
+  if ((e = preload_bulk<32768, 6>()) != cudaSuccess) return e;
+  if ((e = preload_bulk<49152, 4>()) != cudaSuccess) return e;
+  if (dev < 64) done[dev].store(1, std::memory_order_release);
+  return cudaSuccess;
+}
+
 // MP_BULK_SCHED=static turns the dynamic unit claiming off (comparison knob).
 static bool bulk_dynamic() {
   static const bool v = [] {

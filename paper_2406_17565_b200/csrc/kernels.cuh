@@ -89,4 +89,13 @@ cudaError_t launch_fill(char* const* slabs, const int* ids, int n, int nchunks, 
 
 int sm_count(int device);
 
+// Loads every kernel of the library on the current device (and sets the
+// bulk engine's shared-memory attribute) once.  Under lazy module loading
+// (CUDA_MODULE_LOADING=LAZY, the default) a kernel's first launch loads it,
+// and that load can block behind a stream that is already parked on a
+// cross-process flag (cuStreamWaitValue32) -- e.g. the receiver's first
+// STAGED unpack, whose ready flag the sender raises only after the reply the
+// receiver is about to send.  Pools call this at creation.
+cudaError_t preload_kernels();
+
 }  // namespace mpk

@@ -222,9 +222,9 @@ static mp_status harvest_timed(mp_pool* p) {
 
 mp_status drain(mp_pool* p) {
   TRY(remote_apply_waits(p));  // blocks stored by other processes have landed too
-  CK(cudaStreamSynchronize(p->meta));
-  CK(cudaStreamSynchronize(p->stream));
-  CK(cudaStreamSynchronize(p->copy_stream));  // STAGED copy-engine copies issued by p
+  CK(sync_stream_traced(p, p->meta, "drain:meta"));
+  CK(sync_stream_traced(p, p->stream, "drain:stream"));
+  CK(sync_stream_traced(p, p->copy_stream, "drain:copy_stream"));  // STAGED copies issued by p
   track_fence(p->track);  // idle: the window is empty (the next launch opens one)
   TRY(harvest_timed(p));
   p->last_timed_pair = -1;  // no gap across a sync
@@ -798,6 +798,7 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
     return fail(MP_ERR_CONFIG);
   }
   DevGuard g(p->dev);
+  CKC(mpk::preload_kernels());  // no lazy kernel load behind a parked stream (kernels.cuh)
   // The pools of one process on one device share a data stream: a
   // migration between two of them (P -> D, then D -> P) is then ordered by
   // the stream itself instead of a cross-stream event wait per launch, which

@@ -464,6 +464,13 @@ uint64_t new_uid();
 mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip = nullptr);
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
 void remote_close_all(mp_pool* p);
+// MP_REMOTE_TRACE=1 (debugging a stalled cross-process pipeline): blocking
+// waits on a stream / event poll instead, and after 10 s print every remote
+// peer's flag pages and sequence counters to stderr once.
+bool remote_trace_on();
+void remote_dump_state(const mp_pool* p, const char* where);
+cudaError_t sync_stream_traced(const mp_pool* p, cudaStream_t s, const char* where);
+cudaError_t sync_event_traced(const mp_pool* p, cudaEvent_t e, const char* where);
 void host_report_timing();  // MP_HOST_TIMING=1 (api_transfer.cpp)
 bool host_timing_on();
 double host_clock();

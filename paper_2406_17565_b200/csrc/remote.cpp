@@ -309,6 +309,14 @@ void remote_report_timing() {
 }
 
 // ---------------------------------------------------------- receiver side
+#define MP_TRACE(...)                                   \
+  do {                                                  \
+    if (remote_trace_on()) {                            \
+      fprintf(stderr, "[mempool trace %d] ", (int)getpid()); \
+      fprintf(stderr, __VA_ARGS__);                     \
+      fputc('\n', stderr);                              \
+    }                                                   \
+  } while (0)
 namespace {
 
 // Receiver half of a STAGED transfer, enqueued at its allocation step: the
@@ -335,6 +343,7 @@ mp_status staged_recv(mp_pool* p, RemotePeer* r, const DstPrep& st, const uint8_
     CK(cudaEventCreateWithFlags(&r->recv_dep, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&r->recv_ev, cudaEventDisableTiming));
   }
+  MP_TRACE("staged_recv: ring ready");
   std::vector<int32_t> ids;
   for (int64_t i = 0; i < st.nm; ++i)
     if (meds[st.skip + i] == MP_HBM) ids.push_back(st.dids[(size_t)i]);
@@ -357,6 +366,7 @@ mp_status staged_recv(mp_pool* p, RemotePeer* r, const DstPrep& st, const uint8_
                              agg_ep(r->ring + (int64_t)slot * g.slot_bytes, per_block, nullptr),
                              pool_ep(p->d_slabs, nullptr), nb, j0, nj, false, 0, &di));
     TRY(stream_write_u32(r->recv_stream, r->in_sync->d + kSyncFree + slot, q + 1));
+    MP_TRACE("staged_recv: slot %d (q %u, %lld blocks) queued", slot, q, (long long)nb);
   }
   r->in_slot = q;
   return MP_OK;
@@ -409,6 +419,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
                              /*host_ids=*/true);
       const uint32_t slot0 = r->in_slot;
       uint32_t prep_seq = 0, done_seq = 0;
+      MP_TRACE("serve: request type %u prepared: status %d", q->type, (int)s);
       if (s == MP_OK) {
         r->has_pending = true;
         // the sender's copy must follow this allocation and every earlier use
@@ -422,10 +433,24 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         // (no meta fence: with host ids nothing of this allocation runs on
         // the meta stream, and meta never touches block data)
         if (s == MP_OK) {
+          // raised by the data stream once everything before it has run; if
+          // the stream is already idle (nothing queued, the waits above
+          // included) the host raises it now -- no GPU operation, and the
+          // value still only grows: an idle stream has no older prepare
+          // write pending
           prep_seq = ++r->prep_seq;
-          s = stream_write_u32(p->stream, r->in_sync->d + kSyncPrep, prep_seq);
+          const cudaError_t q = cudaStreamQuery(p->stream);
+          if (q == cudaSuccess) {
+            host_raise(r->in_sync->h + kSyncPrep, prep_seq);
+          } else if (q == cudaErrorNotReady) {
+            s = stream_write_u32(p->stream, r->in_sync->d + kSyncPrep, prep_seq);
+          } else {
+            s = MP_ERR_CUDA;
+          }
         }
+        MP_TRACE("serve: prep flag %u enqueued: status %d", prep_seq, (int)s);
         if (s == MP_OK && staged) s = staged_recv(p, r, r->pending, meds, j0, nj);
+        MP_TRACE("serve: staged_recv: status %d", (int)s);
         if (s != MP_OK) {
           dst_abort(p, r->pending);
           r->has_pending = false;
@@ -484,7 +509,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         if (sender_status != MP_OK || !(r->pending.flags & MP_XFER_ASYNC)) {
           // data landed before the receiver says ok; a failed
           // transfer's unpacks finish before its blocks are released
-          if (cudaEventSynchronize(r->recv_ev) != cudaSuccess) {
+          if (sync_event_traced(p, r->recv_ev, "DONE:recv_ev") != cudaSuccess) {
             rstatus = MP_ERR_CUDA;
             break;
           }
@@ -527,6 +552,8 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
       rstatus = MP_ERR_CONFIG;
   }
   if (!wr.ok) rstatus = MP_ERR_BUFFER_TOO_SMALL;
+  MP_TRACE("serve: publish reply %u status %d seq %llu", rtype, (int)rstatus,
+           (unsigned long long)seq);
   publish(c->rep(), rtype, rstatus, wr.len, seq);
   if (timing_on() && (rtype == REP_PREP || rtype == REP_FINAL))
     g_phase.add(rtype == REP_PREP ? 3 : 4, now_s() - t_start);
@@ -538,6 +565,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
 mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
   const double t0 = now_s();
   int spins = 0;
+  bool dumped = false;
   while (__atomic_load_n(&c->rep()->seq, __ATOMIC_ACQUIRE) < seq) {
     int64_t served = 0;
     if (self) {
@@ -547,6 +575,10 @@ mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
     if (!served && ++spins > 64) {
       std::this_thread::yield();
       spins = 0;
+      if (self && !dumped && remote_trace_on() && now_s() - t0 > 10.0) {
+        remote_dump_state(self, "wait_reply");
+        dumped = true;
+      }
       if (now_s() - t0 > kTimeout) {
         set_err("remote peer did not answer (is it inside mp_serve?)");
         return MP_ERR_DST_UNREACHABLE;
@@ -932,6 +964,69 @@ std::string sync_name(uint64_t from, uint64_t to) {
 }
 
 }  // namespace
+
+bool remote_trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("MP_REMOTE_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+void remote_dump_state(const mp_pool* p, const char* where) {
+  fprintf(stderr, "[mempool trace] pool %d stalled in %s (pid %d)\n", p->inst, where,
+          (int)getpid());
+  for (const auto& kv : p->remotes) {
+    const RemotePeer* r = kv.second;
+    fprintf(stderr,
+            "  peer %d: prep_seq(in)=%u in_seq=%u out_slot=%u in_slot=%u async_in=%zu "
+            "(front stamp %llu seq %u) join_bound=%llu prep_stamp=%llu recv_join=%d\n",
+            r->inst, r->prep_seq, r->in_seq, r->out_slot, r->in_slot, r->async_in.size(),
+            r->async_in.empty() ? 0ull : (unsigned long long)r->async_in.front().first,
+            r->async_in.empty() ? 0u : r->async_in.front().second,
+            (unsigned long long)p->join_bound, (unsigned long long)p->prep_stamp,
+            (int)r->recv_join);
+    for (int d = 0; d < 2; ++d) {
+      const SyncPage* s = d ? r->in_sync : r->out_sync;
+      if (!s) continue;
+      const uint32_t* h = s->h;
+      fprintf(stderr, "    %s page: done=%u prep=%u ready=[", d ? "in " : "out",
+              __atomic_load_n(h + kSyncDone, __ATOMIC_ACQUIRE),
+              __atomic_load_n(h + kSyncPrep, __ATOMIC_ACQUIRE));
+      for (int k = 0; k < 8; ++k) fprintf(stderr, "%u ", __atomic_load_n(h + kSyncReady + k, __ATOMIC_ACQUIRE));
+      fprintf(stderr, "] free=[");
+      for (int k = 0; k < 8; ++k) fprintf(stderr, "%u ", __atomic_load_n(h + kSyncFree + k, __ATOMIC_ACQUIRE));
+      fprintf(stderr, "]\n");
+    }
+  }
+}
+
+namespace {
+template <class Q>
+cudaError_t poll_traced(const mp_pool* p, Q query, const char* where) {
+  const double t0 = now_s();
+  bool dumped = false;
+  for (;;) {
+    const cudaError_t e = query();
+    if (e != cudaErrorNotReady) return e;
+    if (!dumped && now_s() - t0 > 10.0) {
+      remote_dump_state(p, where);
+      dumped = true;
+    }
+    std::this_thread::yield();
+  }
+}
+}  // namespace
+
+cudaError_t sync_stream_traced(const mp_pool* p, cudaStream_t s, const char* where) {
+  if (!remote_trace_on()) return cudaStreamSynchronize(s);
+  return poll_traced(p, [&] { return cudaStreamQuery(s); }, where);
+}
+
+cudaError_t sync_event_traced(const mp_pool* p, cudaEvent_t e, const char* where) {
+  if (!remote_trace_on()) return cudaEventSynchronize(e);
+  return poll_traced(p, [&] { return cudaEventQuery(e); }, where);
+}
 
 void remote_close_all(mp_pool* p) {
   if (!p->remotes.empty()) remote_report_timing();

@@ -245,6 +245,7 @@ def main():
     ap.add_argument("--check", action="store_true",
                     help="untimed verification pass (checksums of every transferred block)")
     ap.add_argument("--check-sessions", type=int, default=2)
+    ap.add_argument("--prof", action="store_true", help="cProfile the timed pass (stderr)")
     ap.add_argument("--device", type=int, default=-1)
     ap.add_argument("--dist-backend", default="nccl")
     args = ap.parse_args()
@@ -292,7 +293,16 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         h0 = time.perf_counter()
+        if args.prof:
+            import cProfile
+            import pstats
+            pr = cProfile.Profile()
+            pr.enable()
         run_pass(E, role, args.workload, timed, args.window)
+        if args.prof:
+            pr.disable()
+            print(f"---- rank {rank} ({role.kind})", file=sys.stderr)
+            pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(12)
         pool.sync()
         e1.record()
         torch.cuda.synchronize()

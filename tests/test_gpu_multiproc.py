@@ -8,6 +8,7 @@ after the golden worked example (with and without DEDUP) plus plain
 transfers with `private` payloads."""
 import multiprocessing as mp
 import os
+import time
 
 import numpy as np
 import pytest
@@ -29,6 +30,29 @@ TRANSPORTS = {
     "ce-staged": ({"staging_bytes": 4 * TINY_BLOCK, "staging_slots": 2}, "PATH_STAGED"),
     "ce-per-chunk": ({}, "PATH_CE"),
 }
+
+
+def _collect(q, ps, timeout):
+    """Results of the worker processes; a worker that reports an error makes
+    its peers hang in their next collective, so the first error is raised as
+    soon as it arrives (with what the others did not report)."""
+    import queue
+    res = {}
+    deadline = time.monotonic() + timeout
+    while len(res) < len(ps):
+        try:
+            r, out = q.get(timeout=max(1.0, deadline - time.monotonic()))
+        except queue.Empty:
+            raise AssertionError(f"workers {sorted(set(range(len(ps))) - set(res))} did not "
+                                 f"report within {timeout} s; got {sorted(res)}")
+        res[r] = out
+        if "error" in out:
+            for p in ps:
+                p.kill()
+            raise AssertionError(f"worker {r}: {out['error']}")
+    for p in ps:
+        p.join(timeout=60)
+    return res
 
 
 def _run(rank, port, dedup, q, transport="fused-loopback"):
@@ -113,12 +137,7 @@ def test_two_process_golden(dedup, transport):
     ps = [ctx.Process(target=_run, args=(r, port, dedup, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
-    res = {}
-    for _ in ps:
-        r, out = q.get(timeout=300)
-        res[r] = out
-    for p in ps:
-        p.join(timeout=60)
+    res = _collect(q, ps, 300)
     for r in (0, 1):
         assert "error" not in res[r], res[r].get("error")
     # oracle of the same sequence
@@ -236,12 +255,7 @@ def test_two_process_back_to_back_async(transport):
     ps = [ctx.Process(target=_stress, args=(r, port, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
-    res = {}
-    for _ in ps:
-        r, out = q.get(timeout=300)
-        res[r] = out
-    for p in ps:
-        p.join(timeout=60)
+    res = _collect(q, ps, 300)
     for r in (0, 1):
         assert "error" not in res[r], res[r].get("error")
     sums_p, sums_d = res[0]["sums"], res[1]["sums"]
@@ -346,12 +360,7 @@ def test_fan_in_two_senders_arena_wraps():
     ps = [ctx.Process(target=_fanin, args=(r, port, q, rounds, per_round)) for r in range(3)]
     for p in ps:
         p.start()
-    res = {}
-    for _ in ps:
-        r, out = q.get(timeout=900)
-        res[r] = out
-    for p in ps:
-        p.join(timeout=60)
+    res = _collect(q, ps, 900)
     for r in (0, 1, 2):
         assert "error" not in res[r], res[r].get("error")
     got = res[0]["got"]
@@ -564,12 +573,7 @@ def test_two_process_random_ops(seed, transport):
     ps = [ctx.Process(target=_rand_worker, args=(r, port, seed, q, transport)) for r in range(2)]
     for p in ps:
         p.start()
-    got = {}
-    for _ in ps:
-        r, out = q.get(timeout=600)
-        got[r] = out
-    for p in ps:
-        p.join(timeout=60)
+    got = _collect(q, ps, 600)
     for r in (0, 1):
         assert "error" not in got[r], got[r].get("error")
     P, D, res = _rand_oracle(seed)
@@ -739,12 +743,7 @@ def test_two_process_react_vs_oracle(seed, transport):
           for r in range(2)]
     for p in ps:
         p.start()
-    got = {}
-    for _ in ps:
-        r, out = q.get(timeout=600)
-        got[r] = out
-    for p in ps:
-        p.join(timeout=60)
+    got = _collect(q, ps, 600)
     for r in (0, 1):
         assert "error" not in got[r], got[r].get("error")
     P, D, res = _react_oracle(seed)
