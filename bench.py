@@ -252,6 +252,10 @@ def run_ours(args, rank, world, dist):
 
     host_t = {"match": 0.0, "twi": 0.0, "n": 0}
     xflags = M.XFER_DEDUP | M.XFER_ASYNC | getattr(M, PATHS[args.xfer_path])
+    if role.kind == "P" and not args.no_pipeline:
+        # cross-process: each copy is enqueued at the next call, right after
+        # that call's request went out (overlaps the launch with the round trip)
+        xflags |= M.XFER_PIPELINE
 
     def p_step(bi, io=None):
         """Prefill side of one step."""
@@ -519,6 +523,7 @@ def run_ours(args, rank, world, dist):
             "xfer_path": PATH_NOTES[args.xfer_path],
             "peer_engine": ["auto", "vector LD/ST", "bulk cp.async ring"][args.peer_engine],
             "peer_sched": ["auto", "static split", "dynamic unit claiming"][args.peer_sched],
+            "pipelined_issue": (world > 1 and not args.no_pipeline),
             "pool_blocks_per_instance": n_blocks,
             "batch_blocks": args.batch_blocks,
             "copy_kernel": ["auto (bulk cp.async ring in HBM)", "vector LD/ST",
@@ -1077,6 +1082,8 @@ def main():
                     help="stores into peer memory: 0 auto, 1 vector LD/ST, 2 bulk cp.async")
     ap.add_argument("--peer-sched", type=int, default=0, choices=[0, 1, 2],
                     help="split of peer stores: 0 auto, 1 static, 2 dynamic claiming")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="N>1: enqueue each copy inside its own call (no MP_XFER_PIPELINE)")
     ap.add_argument("--no-probe", action="store_true",
                     help="N>1: skip the in-run peer-copy probe (NVLink peak)")
     args = ap.parse_args()

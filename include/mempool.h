@@ -91,6 +91,15 @@ typedef enum {
 #define MP_XFER_DST_GIVEN (1u << 0) /* dst_addrs is an INPUT: skip the allocation step */
 #define MP_XFER_DEDUP (1u << 1)     /* receiver matches first, moves only what it lacks (R3) */
 #define MP_XFER_ASYNC (1u << 2)     /* return once enqueued; complete with mp_sync (see above) */
+/* With MP_XFER_ASYNC to a peer in ANOTHER process (ignored otherwise): the
+ * call returns after the receiver's allocation reply (its allocation, insert
+ * and `private` delivery are done, the final addrs are returned) and the copy
+ * is enqueued by this pool's NEXT library call -- right after that call's own
+ * request is sent, so the launch overlaps the next round trip -- or by any
+ * call other than mp_match / mp_recv_poll / the getters and dumps, which
+ * enqueue it before anything else.  Until then the peer's later device work
+ * on those blocks waits; a sender that stops calling must call mp_sync. */
+#define MP_XFER_PIPELINE (1u << 3)
 #define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
 #define MP_MATCH_PIN (1u << 5)      /* match: pin matched blocks until mp_unpin (R12) */
 /* Transport selection (benchmarks / comparisons; default AUTO = FUSED). */

@@ -7,7 +7,7 @@ kernels and the transfer / swap engines.  ``mempool`` is a thin ctypes
 binding with the paper's API names.
 """
 from .mempool import (  # noqa: F401
-    HBM, DRAM, MIXED, XFER_DST_GIVEN, XFER_DEDUP, XFER_ASYNC, INS_ERR_ON_CONFLICT, MATCH_PIN,
+    HBM, DRAM, MIXED, XFER_DST_GIVEN, XFER_DEDUP, XFER_ASYNC, XFER_PIPELINE, INS_ERR_ON_CONFLICT, MATCH_PIN,
     PATH_AUTO, PATH_FUSED, PATH_STAGED, PATH_CE, SWAP_ZERO_COPY, SWAP_CE,
     MempoolError, Pool, connect, make_addr, addr_inst, addr_medium, addr_index,
     addr_indices, addr_media, LIB_PATH, SIGNATURES,

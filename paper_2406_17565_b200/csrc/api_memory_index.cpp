@@ -67,6 +67,7 @@ mp_status mp_alloc_mem(mp_pool* p, int64_t n, int32_t type, int32_t requester, m
   const bool stream_ordered = (type & MP_ALLOC_STREAM_ORDERED) != 0;
   type &= ~MP_ALLOC_STREAM_ORDERED;
   if (!p || n < 0 || (n > 0 && !out) || type < MP_HBM || type > MP_MIXED) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   DevGuard g(p->dev);
   const std::vector<mpi::Node*> none;
   int64_t nh = 0, nd = 0;
@@ -100,6 +101,7 @@ mp_status mp_alloc_mem(mp_pool* p, int64_t n, int32_t type, int32_t requester, m
 
 mp_status mp_free_mem(mp_pool* p, const mp_addr* a, int64_t n) {
   if (!p || n < 0 || (n > 0 && !a)) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   const uint32_t g = next_mark(p);
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
@@ -124,6 +126,7 @@ mp_status mp_insert(mp_pool* p, const mp_token* toks, int64_t n_tok, const mp_ad
                     int64_t n_addr, uint32_t flags, int64_t* n_dup) {
   if (!p || n_tok < 0 || (n_tok > 0 && !toks) || n_addr < 0 || (n_addr > 0 && !a))
     return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   return insert_internal(p, toks, n_tok, a, n_addr, flags, n_dup);
 }
 
@@ -139,6 +142,7 @@ mp_status mp_match(mp_pool* p, const mp_token* toks, int64_t n_tok, uint32_t fla
 
 mp_status mp_unpin(mp_pool* p, const mp_addr* a, int64_t n) {
   if (!p || n < 0 || (n > 0 && !a)) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   std::map<std::pair<int, int32_t>, int64_t> need;
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
@@ -179,6 +183,7 @@ mp_status mp_unpin(mp_pool* p, const mp_addr* a, int64_t n) {
 
 mp_status mp_delete(mp_pool* p, const mp_token* toks, int64_t n_tok) {
   if (!p || n_tok < 0 || (n_tok > 0 && !toks)) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   for (const auto& u : p->index->erase_seq(toks, n_tok)) {
     if (u.ref == 0) {
       free_block(p, u.medium, u.idx);
@@ -193,6 +198,7 @@ mp_status mp_delete(mp_pool* p, const mp_token* toks, int64_t n_tok) {
 mp_status mp_evict(mp_pool* p, int64_t n, int32_t medium, mp_addr* out, int64_t* n_freed) {
   if (!p || n < 0 || (medium != MP_HBM && medium != MP_DRAM) || (n > 0 && !out))
     return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   std::vector<int32_t> freed;
   evict_internal(p, n, medium, &freed);
   for (size_t i = 0; i < freed.size(); ++i) out[i] = enc(p, medium, freed[i]);

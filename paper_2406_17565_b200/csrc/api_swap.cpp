@@ -29,6 +29,7 @@ extern "C" {
 mp_status mp_swap_out(mp_pool* p, int64_t n, uint32_t flags, mp_addr* out_old, mp_addr* out_new,
                       int64_t* n_moved) {
   if (!p || n < 0 || (n > 0 && (!out_old || !out_new))) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   DevGuard g(p->dev);
   TRY(flush_involving(p));  // victims may still be the target of a coalesced copy
   std::vector<std::pair<int32_t, int32_t>> pairs;
@@ -120,6 +121,7 @@ mp_status mp_swap_out(mp_pool* p, int64_t n, uint32_t flags, mp_addr* out_old, m
 
 mp_status mp_swap_in(mp_pool* p, const mp_addr* a, int64_t n, uint32_t flags, mp_addr* out) {
   if (!p || n < 0 || (n > 0 && (!a || !out))) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   std::vector<int32_t> dids((size_t)n);
   std::set<int32_t> seen;
   for (int64_t i = 0; i < n; ++i) {
@@ -224,17 +226,20 @@ static mp_status pack_unpack(mp_pool* p, const mp_addr* a, int64_t n, int32_t l0
 
 mp_status mp_pack(mp_pool* p, const mp_addr* a, int64_t n, int32_t l0, int32_t l1,
                   void* staging) {
+  if (p) TRY(remote_flush_tx(p));
   return pack_unpack(p, a, n, l0, l1, staging, true);
 }
 
 mp_status mp_unpack(mp_pool* p, const void* staging, const mp_addr* a, int64_t n, int32_t l0,
                     int32_t l1) {
+  if (p) TRY(remote_flush_tx(p));
   return pack_unpack(p, a, n, l0, l1, const_cast<void*>(staging), false);
 }
 
 // ------------------------------------------------------------ debug / test
 mp_status mp_debug_fill(mp_pool* p, const mp_addr* a, int64_t n, uint64_t seed) {
   if (!p || n < 0 || (n > 0 && !a)) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   std::vector<int32_t> ids((size_t)n);
   for (int64_t i = 0; i < n; ++i) {
     int m = 0;
@@ -262,6 +267,7 @@ mp_status mp_debug_read_block(mp_pool* p, mp_addr a, void* host_out, int64_t cap
   int m = 0;
   int32_t idx = 0;
   if (!p || !host_out) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   if (!decode(p, a, &m, &idx)) return MP_ERR_INVALID_ADDR;
   if (cap < p->Pb) return MP_ERR_BUFFER_TOO_SMALL;
   DevGuard g(p->dev);
@@ -297,6 +303,7 @@ mp_status mp_debug_block_states(mp_pool* p, int32_t medium, uint8_t* out, int64_
 mp_status mp_debug_bitmap(mp_pool* p, uint32_t* out, int64_t cap_words) {
   if (!p || !out) return MP_ERR_CONFIG;
   if (cap_words < p->nwords) return MP_ERR_BUFFER_TOO_SMALL;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first
   DevGuard g(p->dev);
   TRY(sync(p));
   CK(cudaMemcpy(out, p->d_bitmap, sizeof(uint32_t) * p->nwords, cudaMemcpyDeviceToHost));

@@ -512,7 +512,11 @@ mp_status mp_transfer(mp_pool* src, int32_t dst_inst, const mp_addr* sa, int64_t
   mp_pool* dst = peer_of(src, dst_inst);
   RemotePeer* rp = dst ? nullptr : remote_of(src, dst_inst);
   if (!dst && !rp) return MP_ERR_DST_UNREACHABLE;
-  if (dst) TRY(check_compatible(src, dst));
+  if (dst) {
+    TRY(check_compatible(src, dst));
+    TRY(remote_flush_tx(src));  // pipelined cross-process copies of either pool go first
+    TRY(remote_flush_tx(dst));
+  }
   if (!(0 <= l0 && l0 < l1 && l1 <= src->L) || (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
   std::vector<int32_t> sids;
   std::vector<uint8_t> smeds;
@@ -549,7 +553,11 @@ mp_status mp_transfer_with_insert(mp_pool* src, int32_t dst_inst, const mp_token
   mp_pool* dst = peer_of(src, dst_inst);
   RemotePeer* rp = dst ? nullptr : remote_of(src, dst_inst);
   if (!dst && !rp) return MP_ERR_DST_UNREACHABLE;
-  if (dst) TRY(check_compatible(src, dst));
+  if (dst) {
+    TRY(check_compatible(src, dst));
+    TRY(remote_flush_tx(src));  // pipelined cross-process copies of either pool go first
+    TRY(remote_flush_tx(dst));
+  }
   if ((flags & MP_XFER_DST_GIVEN) && (flags & MP_XFER_DEDUP)) return MP_ERR_CONFIG;
   const int64_t B = src->B, ceil_b = (n_tok + B - 1) / B;
   if (m > ceil_b) return MP_ERR_ADDR_COUNT;
@@ -608,6 +616,8 @@ mp_status mp_transfer_heads(mp_pool* src, int32_t dst_inst, const mp_addr* sa, i
   if (!src || n < 0 || (n > 0 && (!sa || !da))) return MP_ERR_CONFIG;
   mp_pool* dst = peer_of(src, dst_inst);
   if (!dst) return remote_of(src, dst_inst) ? MP_ERR_CONFIG : MP_ERR_DST_UNREACHABLE;
+  TRY(remote_flush_tx(src));
+  TRY(remote_flush_tx(dst));
   if (src->L != dst->L || src->B != dst->B || src->D != dst->D || src->elem != dst->elem ||
       !(0 <= l0 && l0 < l1 && l1 <= src->L) || n_heads < 1 || src_head0 < 0 ||
       dst_head0 < 0 || src_head0 + n_heads > src->H || dst_head0 + n_heads > dst->H ||

@@ -674,7 +674,12 @@ const char* mp_last_error(void) { return get_err().c_str(); }
 
 void mp_pool_destroy(mp_pool* p) {
   if (!p) return;
-  if (p->stream) flush_involving(p);
+  if (p->stream) {
+    remote_flush_tx(p);
+    flush_involving(p);
+  }
+  delete p->pend_tx;  // only left on a failed flush
+  p->pend_tx = nullptr;
   remote_close_all(p);
   {
     DevGuard g(p->dev);
@@ -910,6 +915,8 @@ mp_status mp_pool_create(const mp_pool_config* cfg, mp_pool** out) {
 
 mp_status mp_connect(mp_pool* a, mp_pool* b) {
   if (!a || !b || a == b || a->inst == b->inst) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(a));
+  TRY(remote_flush_tx(b));
   // kv_heads may differ: tensor-parallel shards of one model (mp_transfer_heads);
   // whole-block transfers additionally require equal chunk sizes
   if (a->L != b->L || a->B != b->B || a->D != b->D || a->elem != b->elem) {
@@ -971,12 +978,14 @@ mp_status mp_pool_info_get(const mp_pool* p, mp_pool_info* o) {
 mp_status mp_sync(mp_pool* p) {
   if (!p) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
+  TRY(remote_flush_tx(p));
   return sync(p);
 }
 
 mp_status mp_wait_event(mp_pool* p, void* ev) {
   if (!p || !ev) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
+  TRY(remote_flush_tx(p));
   // a pending coalesced copy was issued before the dependency existed: it
   // must not be delayed behind it, nor run before the producer's data below
   TRY(flush_involving(p));
@@ -987,6 +996,7 @@ mp_status mp_wait_event(mp_pool* p, void* ev) {
 mp_status mp_record_event(mp_pool* p, void* ev) {
   if (!p || !ev) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
+  TRY(remote_flush_tx(p));
   TRY(flush_involving(p));
   TRY(remote_apply_waits(p));
   TRY(meta_fence(p));
@@ -997,6 +1007,7 @@ mp_status mp_record_event(mp_pool* p, void* ev) {
 mp_status mp_profile(mp_pool* p, int32_t every) {
   if (!p || every < 0) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
+  TRY(remote_flush_tx(p));
   if (!every && p->profile_every) TRY(drain(p));
   p->profile_every = every;
   p->profile_seen = 0;
@@ -1012,6 +1023,7 @@ mp_status mp_stats_get(const mp_pool* p, mp_stats* o) {
 mp_status mp_stats_reset(mp_pool* p) {
   if (!p) return MP_ERR_CONFIG;
   DevGuard g(p->dev);
+  TRY(remote_flush_tx(p));
   TRY(drain(p));
   p->stats = mp_stats{};
   return MP_OK;

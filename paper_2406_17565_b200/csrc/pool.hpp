@@ -222,6 +222,21 @@ struct RemotePeer {
   std::deque<std::pair<uint64_t, uint32_t>> async_in;
 };
 
+// A cross-process copy whose allocation reply has arrived but which is not
+// enqueued yet (MP_XFER_PIPELINE): it is enqueued before this pool enqueues
+// any other device work or serves any inbound request (remote_flush_tx), so
+// the pool's stream sees the same order as without pipelining.
+struct PendingTx {
+  RemotePeer* r = nullptr;
+  uint32_t path = 0;
+  int j0 = 0, nj = 0;
+  std::vector<int32_t> hs, hd, ds, dd;
+  uint32_t prep_seq = 0, done_seq = 0;
+  uint64_t start_stamp = 0;
+  std::vector<mpi::Node*> pinned;  // indexed sources, pinned until enqueued
+  int64_t nm = 0;
+};
+
 }  // namespace mp
 
 struct mp_pool {
@@ -271,6 +286,7 @@ struct mp_pool {
   // other (remote.cpp)
   uint64_t prep_stamp = 0;
   uint64_t join_bound = ~0ull;
+  mp::PendingTx* pend_tx = nullptr;  // MP_XFER_PIPELINE copy not enqueued yet
   std::vector<cudaEvent_t> pack_ev;  // STAGED (cross-process): slot packed
   cudaEvent_t ev_order = nullptr, ev_meta = nullptr;
   std::vector<cudaEvent_t> slot_ev;
@@ -463,6 +479,8 @@ uint64_t new_uid();
 // (its own next copy is ordered behind them by its stream).
 mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip = nullptr);
 mp_status remote_serve_once(mp_pool* p, int64_t* served);
+// Enqueue the pool's pending MP_XFER_PIPELINE copy, if any (cheap otherwise).
+mp_status remote_flush_tx(mp_pool* p);
 void remote_close_all(mp_pool* p);
 // MP_REMOTE_TRACE=1 (debugging a stalled cross-process pipeline): blocking
 // waits on a stream / event poll instead, and after 10 s print every remote

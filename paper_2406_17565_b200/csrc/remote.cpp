@@ -615,6 +615,7 @@ mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip) {
 
 mp_status remote_serve_once(mp_pool* p, int64_t* served) {
   *served = 0;
+  TRY(remote_flush_tx(p));  // before this pool's stream sees any inbound work
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
     if (!r->in) continue;
@@ -717,7 +718,49 @@ mp_status remote_transmit(mp_pool* src, RemotePeer* r, uint32_t path, int j0, in
   return MP_OK;
 }
 
+// Enqueue the transmission of one transfer and raise the pair's done flag
+// after it (on failure: drain, then raise every flag the peer may wait on
+// from the host).  join_bound = the transfer's start stamp (no wait on an
+// inbound transfer that started later).
+mp_status transmit_step(mp_pool* src, RemotePeer* r, uint32_t path, int j0, int nj,
+                        const std::vector<int32_t>& hs, const std::vector<int32_t>& hd,
+                        const std::vector<int32_t>& ds, const std::vector<int32_t>& dd,
+                        const RingGeom& geom, uint32_t slot0, uint32_t slot_end,
+                        uint32_t prep_seq, uint32_t done_seq, uint64_t start_stamp,
+                        mp_status pre) {
+  DevGuard g(src->dev);
+  mp_status xs = pre;
+  src->join_bound = start_stamp;
+  if (xs == MP_OK) xs = remote_transmit(src, r, path, j0, nj, hs, hd, ds, dd, geom, slot0, prep_seq);
+  src->join_bound = ~0ull;
+  if (xs != MP_OK) {
+    // release the peer's streams: every flag it waits on is raised from
+    // the host once this side's copies are drained (or dead)
+    cudaStreamSynchronize(src->stream);
+    cudaStreamSynchronize(src->copy_stream);
+    cudaGetLastError();
+    for (uint32_t q = slot0; q != slot_end; ++q)
+      host_raise(r->out_sync->h + kSyncReady + q % (uint32_t)geom.S, q + 1);
+    host_raise(r->out_sync->h + kSyncDone, done_seq);
+    return xs;
+  }
+  return stream_write_u32(src->stream, r->out_sync->d + kSyncDone, done_seq);
+}
+
 }  // namespace
+
+mp_status remote_flush_tx(mp_pool* p) {
+  PendingTx* t = p->pend_tx;
+  if (!t) return MP_OK;
+  p->pend_tx = nullptr;
+  const mp_status xs = transmit_step(p, t->r, t->path, t->j0, t->nj, t->hs, t->hd, t->ds, t->dd,
+                                     RingGeom{}, 0, 0, t->prep_seq, t->done_seq, t->start_stamp,
+                                     MP_OK);
+  p->stats.blocks_moved += (uint64_t)t->nm;
+  unpin_nodes(p, t->pinned);
+  delete t;
+  return xs;
+}
 
 mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token* toks,
                           int64_t n_tok, const std::vector<int32_t>& sids,
@@ -780,7 +823,11 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   double t0 = tm ? now_s() : 0.0;
   const uint64_t s1 = ++c->next_req;
   publish(c->req(), kind == 1 ? REQ_TWI : REQ_XFER, 0, wr.len, s1);
+  // the previous call's pipelined copy is launched while the peer prepares
+  // this one (before any inbound request is served: wait_reply may serve)
+  const mp_status fs = remote_flush_tx(src);
   mp_status st = wait_reply(src, c, s1);
+  if (st == MP_OK && fs != MP_OK) st = fs;
   if (tm) {
     const double t = now_s();
     g_phase.add(0, t - t0);
@@ -849,24 +896,30 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
         }
       }
     }
-    src->join_bound = start_stamp;
-    if (xs == MP_OK)
-      xs = remote_transmit(src, r, path, j0, nj, hs, hd, ds_, dd_, geom, slot0, prep_seq);
-    src->join_bound = ~0ull;
-    if (xs != MP_OK) {
-      // release the peer's streams: every flag it waits on is raised from
-      // the host once this side's copies are drained (or dead)
-      cudaStreamSynchronize(src->stream);
-      cudaStreamSynchronize(src->copy_stream);
-      cudaGetLastError();
-      for (uint32_t q = slot0; q != slot_end; ++q)
-        host_raise(r->out_sync->h + kSyncReady + q % (uint32_t)geom.S, q + 1);
-      host_raise(r->out_sync->h + kSyncDone, done_seq);
+    if (one_trip && (flags & MP_XFER_PIPELINE) && xs == MP_OK) {
+      // enqueued by this pool's next call (remote_flush_tx); the indexed
+      // sources stay pinned until then
+      PendingTx* t = new PendingTx();
+      t->r = r;
+      t->path = path;
+      t->j0 = j0;
+      t->nj = nj;
+      t->hs.swap(hs);
+      t->hd.swap(hd);
+      t->ds.swap(ds_);
+      t->dd.swap(dd_);
+      t->prep_seq = prep_seq;
+      t->done_seq = done_seq;
+      t->start_stamp = start_stamp;
+      t->pinned.swap(pinned);
+      t->nm = nm;
+      src->pend_tx = t;
     } else {
-      xs = stream_write_u32(src->stream, r->out_sync->d + kSyncDone, done_seq);
+      xs = transmit_step(src, r, path, j0, nj, hs, hd, ds_, dd_, geom, slot0, slot_end, prep_seq,
+                         done_seq, start_stamp, xs);
       if (xs == MP_OK && !one_trip && !(flags & MP_XFER_ASYNC)) xs = sync(src);
+      src->stats.blocks_moved += (uint64_t)nm;
     }
-    src->stats.blocks_moved += (uint64_t)nm;
   }
   if (tm) {
     const double t = now_s();
@@ -1123,6 +1176,7 @@ mp_status mp_export_handle(mp_pool* p, void* buf, int64_t cap, int64_t* len) {
 
 mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
   if (!p || !buf || len < (int64_t)sizeof(WireHandle)) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));
   WireHandle* h = new WireHandle();
   std::memcpy(h, buf, sizeof(*h));
   auto fail = [&](mp_status s, const char* why) {
@@ -1213,6 +1267,7 @@ mp_status mp_serve(mp_pool* p, int64_t timeout_ms, int32_t until_mark, int64_t* 
 
 mp_status mp_send_mark(mp_pool* p, int32_t dst_instance, int32_t tag) {
   if (!p) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));
   auto it = p->remotes.find(dst_instance);
   if (it == p->remotes.end()) return MP_ERR_DST_UNREACHABLE;
   Channel* c = it->second->out;

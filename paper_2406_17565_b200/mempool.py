@@ -23,6 +23,7 @@ ALLOC_STREAM_ORDERED = 1 << 8
 XFER_DST_GIVEN = 1 << 0
 XFER_DEDUP = 1 << 1
 XFER_ASYNC = 1 << 2
+XFER_PIPELINE = 1 << 3
 INS_ERR_ON_CONFLICT = 1 << 4
 MATCH_PIN = 1 << 5
 PATH_AUTO = 0 << 8

@@ -112,8 +112,13 @@ class Engine:
         if n and not np.array_equal(a, b):
             self.bad += int((a != b).any(1).sum())
 
+    PIPELINE = M.XFER_PIPELINE
+
     def send(self, dst, tokens, src, flags, head):
-        """transfer_with_insert with `private` = header + checksums of src."""
+        """transfer_with_insert with `private` = header + checksums of src;
+        ASYNC sends are pipelined (the copy is enqueued at the next call)."""
+        if flags & M.XFER_ASYNC:
+            flags |= self.PIPELINE
         priv = head + self.sums(src)
         fin, nm = self.p.transfer_with_insert(dst, tokens, src, flags=flags, priv=priv)
         self.moved += nm
@@ -246,10 +251,14 @@ def main():
                     help="untimed verification pass (checksums of every transferred block)")
     ap.add_argument("--check-sessions", type=int, default=2)
     ap.add_argument("--prof", action="store_true", help="cProfile the timed pass (stderr)")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="enqueue each copy inside its own call (no MP_XFER_PIPELINE)")
     ap.add_argument("--device", type=int, default=-1)
     ap.add_argument("--dist-backend", default="nccl")
     args = ap.parse_args()
 
+    if args.no_pipeline:
+        Engine.PIPELINE = 0
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if world < 2:
@@ -357,6 +366,7 @@ def main():
             "value": round(tot * Pb / (tmax * 1e-3) / 1e9, 2), "unit": "GB/s",
             "blocks_per_s": round(tot / (tmax * 1e-3), 1), "blocks_moved": int(tot),
             "ms": round(tmax, 3), "scaling": "weak",
+            "pipelined_issue": not args.no_pipeline,
             "host_ms_max": round(max(r["host_ms"] for r in recs), 3),
             "per_pair": per_pair,
             "check": ({"blocks_checked": sum(c["checked_blocks"] for c in checks),

@@ -29,6 +29,9 @@ TRANSPORTS = {
     # 2 slots of 2 tiny blocks: the ring wraps inside one transfer
     "ce-staged": ({"staging_bytes": 4 * TINY_BLOCK, "staging_slots": 2}, "PATH_STAGED"),
     "ce-per-chunk": ({}, "PATH_CE"),
+    # ASYNC transfers enqueue their copy at the sender's next call
+    # (MP_XFER_PIPELINE), after that call's request went out
+    "fused-pipelined": ({}, "PATH_FUSED|XFER_PIPELINE"),
 }
 
 
@@ -68,7 +71,7 @@ def _run(rank, port, dedup, q, transport="fused-loopback"):
         torch.cuda.set_device(0)
         s = TINY
         kw, pname = TRANSPORTS[transport]
-        path = getattr(M, pname)
+        path = sum(getattr(M, x) for x in pname.split("|"))
         pool = M.Pool(rank, 0, s.layers, s.kv_heads, s.head_dim, s.block_tokens, 64,
                       dram_blocks=16 if rank == 0 else 0, verify=True, **kw)
         blobs = M.exchange_handles(pool)
@@ -199,7 +202,7 @@ def _stress(rank, port, q, transport="fused-loopback"):
         kw, pname = TRANSPORTS[transport]
         if "staging_bytes" in kw:   # 7B blocks: 3 slots of 2 blocks
             kw = {"staging_bytes": 6 * S.block_bytes, "staging_slots": 3}
-        path = getattr(M, pname)
+        path = sum(getattr(M, x) for x in pname.split("|"))
         pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, n,
                       slabs=slabs, verify=True, **kw)
         blobs = M.exchange_handles(pool)
@@ -336,7 +339,9 @@ def _fanin(rank, port, q, rounds, per_round):
                 for _ in range(per_round):
                     k = int(rng.integers(1, 7))
                     sel = np.sort(rng.choice(n, k, replace=False))
-                    pool.transfer(0, src[sel], flags=M.XFER_ASYNC,
+                    # sender 1 pipelines (its copy is enqueued at its next call)
+                    pool.transfer(0, src[sel],
+                                  flags=M.XFER_ASYNC | (M.XFER_PIPELINE if rank == 1 else 0),
                                   priv=sel.astype(np.int32).tobytes())
                 pool.send_mark(0, rnd)
                 dist.barrier()
@@ -435,7 +440,7 @@ def _rand_worker(rank, port, seed, q, transport="fused-loopback"):
         torch.cuda.set_device(0)
         prompts, phases = _rand_ops(seed)
         kw, pname = TRANSPORTS[transport]
-        path = getattr(M, pname)
+        path = sum(getattr(M, x) for x in pname.split("|"))
         pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens,
                       48 if rank == 0 else 24, dram_blocks=12 if rank == 0 else 0, verify=True,
                       **kw)
@@ -564,7 +569,8 @@ def _rand_oracle(seed):
 @pytest.mark.parametrize("seed,transport", [(3, "fused-loopback"), (11, "fused-loopback"),
                                             (29, "fused-loopback"), (5, "fused-vector-static"),
                                             (7, "fused-bulk-dynamic"), (13, "ce-staged"),
-                                            (17, "ce-per-chunk")])
+                                            (17, "ce-per-chunk"), (19, "fused-pipelined"),
+                                            (23, "fused-pipelined")])
 def test_two_process_random_ops(seed, transport):
     import oracle as O
     ctx = mp.get_context("spawn")
@@ -626,7 +632,7 @@ def _react_worker(rank, port, seed, q, transport):
         dist.init_process_group("gloo", rank=rank, world_size=2)
         torch.cuda.set_device(0)
         kw, pname = TRANSPORTS[transport]
-        path = getattr(M, pname)
+        path = sum(getattr(M, x) for x in pname.split("|"))
         pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, 96,
                       verify=True, **kw)
         blobs = M.exchange_handles(pool)
@@ -733,7 +739,8 @@ def _react_oracle(seed):
 
 
 @pytest.mark.parametrize("seed,transport", [(41, "fused-loopback"), (43, "fused-vector-static"),
-                                            (47, "ce-staged"), (53, "ce-per-chunk")])
+                                            (47, "ce-staged"), (53, "ce-per-chunk"),
+                                            (59, "fused-pipelined")])
 def test_two_process_react_vs_oracle(seed, transport):
     import oracle as O
     ctx = mp.get_context("spawn")
