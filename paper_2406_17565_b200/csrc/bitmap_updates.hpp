@@ -21,7 +21,7 @@ namespace mp {
 
 class BitmapUpdates {
  public:
-  enum : uint8_t { kNone = 0, kFree = 1, kClaim = 2 };
+  enum : uint8_t { kNone = 0, kFree = 1, kClaim = 2, kSeen = 0x80 };
 
   void reset(size_t n_blocks) {
     q_.clear();
@@ -37,6 +37,22 @@ class BitmapUpdates {
 
   bool empty() const { return q_.empty(); }
   size_t queued() const { return q_.size(); }  // upper bound (stale entries included)
+
+  // Host only: drops stale and duplicate entries, so the queue holds at most
+  // one entry per block however long the device goes without a scan (a pool
+  // whose allocations all come from the host -- a cross-process receiver --
+  // then never launches a kernel just to bound it).
+  void compact() {
+    size_t k = 0;
+    for (int32_t id : q_) {
+      uint8_t& s = st_[(size_t)id];
+      if (s == kNone || (s & kSeen)) continue;
+      s = (uint8_t)(s | kSeen);
+      q_[k++] = id;
+    }
+    q_.resize(k);
+    for (int32_t id : q_) st_[(size_t)id] = (uint8_t)(st_[(size_t)id] & ~kSeen);
+  }
 
   // Moves the live updates to *out, encoded id (set the bit) or -(id+1)
   // (clear it), and forgets them.

@@ -488,7 +488,10 @@ mp_status alloc_hbm(mp_pool* p, int64_t n, int32_t requester, std::vector<int32_
   if (defer) {
     for (int32_t id : *ids) p->dev_upd.on_claim(id);
     // keep the queue bounded (stale entries and long claim runs)
-    if (p->dev_upd.queued() > (size_t)4 * mpk::kInlineIds) TRY(flush_frees(p));
+    // keep the queue bounded on the host (stale entries and long claim
+    // runs); the device learns the updates at its next scan or sync
+    if (p->dev_upd.queued() > (size_t)4 * mpk::kInlineIds + 2 * (size_t)p->n_hbm)
+      p->dev_upd.compact();
     *d_ids = nullptr;
     return MP_OK;
   }

@@ -17,6 +17,7 @@ void bu_free(void* u) { delete static_cast<mp::BitmapUpdates*>(u); }
 void bu_on_free(void* u, int32_t id) { static_cast<mp::BitmapUpdates*>(u)->on_free(id); }
 void bu_on_claim(void* u, int32_t id) { static_cast<mp::BitmapUpdates*>(u)->on_claim(id); }
 int64_t bu_queued(void* u) { return (int64_t) static_cast<mp::BitmapUpdates*>(u)->queued(); }
+void bu_compact(void* u) { static_cast<mp::BitmapUpdates*>(u)->compact(); }
 // writes the live updates into out (cap entries); returns their count
 int64_t bu_take(void* u, int32_t* out, int64_t cap) {
   std::vector<int32_t> v;

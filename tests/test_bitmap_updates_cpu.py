@@ -35,6 +35,7 @@ def lib(tmp_path_factory):
     L.bu_on_claim.argtypes = [C.c_void_p, C.c_int32]
     L.bu_queued.restype = C.c_int64
     L.bu_queued.argtypes = [C.c_void_p]
+    L.bu_compact.argtypes = [C.c_void_p]
     L.bu_take.restype = C.c_int64
     L.bu_take.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
     return L
@@ -94,9 +95,12 @@ def test_queue_keeps_device_bitmap_equal_to_host_shadow(lib, seed):
             device[dev_pick] = False
             host_free[host_pick] = False
             owned += host_pick.tolist()
-        else:                                 # a sync: the queue is flushed
+        elif rng.random() < 0.5:              # a sync: the queue is flushed
             apply(device, take(lib, u, 4 * n), rng)
             assert np.array_equal(device, host_free)
+        else:                                 # host-side compaction: nothing applied
+            lib.bu_compact(u)
+            assert lib.bu_queued(u) <= n      # one entry per block at most
         assert lib.bu_queued(u) <= 4 * n
     apply(device, take(lib, u, 4 * n), rng)
     assert np.array_equal(device, host_free)
@@ -115,3 +119,24 @@ def test_cancellation_leaves_nothing_to_apply(lib):
     lib.bu_on_claim(u, 7)                     # net: one claim
     assert list(take(lib, u, 16)) == [-8]
     lib.bu_free(u)
+
+
+def test_compaction_keeps_live_updates_once(lib):
+    """compact() (host only) drops stale and duplicate entries: taking after
+    it gives the same updates as taking without it, each id once."""
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        n = 200
+        a, b = lib.bu_new(n), lib.bu_new(n)
+        for _ in range(int(rng.integers(10, 400))):
+            i = int(rng.integers(n))
+            f = lib.bu_on_free if rng.random() < 0.5 else lib.bu_on_claim
+            f(a, i)
+            f(b, i)
+        lib.bu_compact(b)
+        assert lib.bu_queued(b) <= n
+        ta, tb = take(lib, a, 4 * n), take(lib, b, 4 * n)
+        assert sorted(ta.tolist()) == sorted(tb.tolist())
+        assert len(set(np.where(tb >= 0, tb, -tb - 1).tolist())) == len(tb)
+        lib.bu_free(a)
+        lib.bu_free(b)
