@@ -590,9 +590,21 @@ mp_status wait_reply(mp_pool* self, Channel* c, uint64_t seq) {
 
 }  // namespace
 
+// Inbound copies whose done flag the host already sees raised have landed
+// (the flag is written after the copy, with a memory barrier): nothing to
+// join, so they leave the queue without a device wait.  Keeps the queue short
+// on a receiver that never issues device work of its own.
+static void prune_async_in(RemotePeer* r) {
+  if (r->async_in.empty() || !r->in_sync) return;
+  const uint32_t done = __atomic_load_n(r->in_sync->h + kSyncDone, __ATOMIC_ACQUIRE);
+  while (!r->async_in.empty() && (int32_t)(done - r->async_in.front().second) >= 0)
+    r->async_in.pop_front();
+}
+
 mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip) {
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
+    prune_async_in(r);
     if (!r->recv_join && (r->async_in.empty() || r == skip)) continue;
     DevGuard g(p->dev);
     if (r->recv_join) {  // the unpacks of a completed STAGED transfer
