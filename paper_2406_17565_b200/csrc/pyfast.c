@@ -329,6 +329,34 @@ static PyObject* py_wait_event(PyObject* self, PyObject* args) {
   return event_call(args, mp_wait_event, "wait_event");
 }
 
+/* recv_poll(h) -> (kind, src_instance, private bytes, addrs uint64[]) or None:
+ * the size query and the pop in one call from Python. */
+static PyObject* py_recv_poll(PyObject* self, PyObject* h) {
+  mp_pool* p = handle(h);
+  mp_recv_msg m;
+  int st = mp_recv_poll(p, &m, NULL, 0, NULL, 0);
+  if (st == MP_ERR_PRECONDITION) Py_RETURN_NONE;  /* nothing queued */
+  if (st != MP_OK && st != MP_ERR_BUFFER_TOO_SMALL) return raise_status(st, "recv_poll");
+  PyObject* pb = PyBytes_FromStringAndSize(NULL, (Py_ssize_t)m.priv_len);
+  if (!pb) return NULL;
+  npy_intp dims[1] = {(npy_intp)m.n_addrs};
+  PyObject* ad = PyArray_SimpleNew(1, dims, NPY_UINT64);
+  if (!ad) {
+    Py_DECREF(pb);
+    return NULL;
+  }
+  if (st == MP_ERR_BUFFER_TOO_SMALL) {  /* kept: pop it into the sized buffers */
+    st = mp_recv_poll(p, &m, PyBytes_AS_STRING(pb), m.priv_len,
+                      (mp_addr*)PyArray_DATA((PyArrayObject*)ad), m.n_addrs);
+    if (st != MP_OK) {
+      Py_DECREF(pb);
+      Py_DECREF(ad);
+      return raise_status(st, "recv_poll");
+    }
+  }  /* else: an empty message (no private bytes, no addrs) was popped already */
+  return Py_BuildValue("(iiNN)", (int)m.kind, (int)m.src_instance, pb, ad);
+}
+
 /* sync(h) */
 static PyObject* py_sync(PyObject* self, PyObject* h) {
   int st;
@@ -353,6 +381,7 @@ static PyMethodDef methods[] = {
     {"record_event", py_record_event, METH_VARARGS, "mp_record_event"},
     {"wait_event", py_wait_event, METH_VARARGS, "mp_wait_event"},
     {"sync", py_sync, METH_O, "mp_sync"},
+    {"recv_poll", py_recv_poll, METH_O, "mp_recv_poll"},
     {NULL, NULL, 0, NULL},
 };
 

@@ -370,17 +370,8 @@ class Pool:
                                        priv or None, self.B)
 
     def recv_poll(self):
-        m = RecvMsg()
-        st = _lib.mp_recv_poll(self._h, C.byref(m), None, 0, None, 0)
-        if st == -9:
-            return None
-        if st not in (0, -12):
-            _check(st, "recv_poll")
-        pb = C.create_string_buffer(max(m.priv_len, 1))
-        ad = np.zeros(max(m.n_addrs, 1), np.uint64)
-        _check(_lib.mp_recv_poll(self._h, C.byref(m), pb, m.priv_len, _pu64(ad), len(ad)),
-               "recv_poll")
-        return m.kind, m.src_instance, pb.raw[: m.priv_len], ad[: m.n_addrs]
+        """Oldest delivered message (kind, src_instance, private, addrs) or None."""
+        return _F.recv_poll(self._hv)
 
     def transfer_heads(self, dst_instance: int, src_addrs, dst_addrs, src_head0: int,
                        dst_head0: int, n_heads: int, layer_begin: int = 0,
