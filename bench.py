@@ -251,6 +251,15 @@ def run_ours(args, rank, world, dist):
         batches = make_batches(reqs, partials, args.batch_blocks, B)
 
     host_t = {"match": 0.0, "twi": 0.0, "n": 0}
+    # D needs each batch's request count (it retires exactly that batch while
+    # the sender's next requests may already be queued): P tells it once
+    batch_sizes = [len(b) for b in batches] if batches is not None else None
+    if role.kind in ("P", "D"):
+        sizes = [None] * world
+        dist.all_gather_object(sizes, batch_sizes)
+        if role.kind == "D":
+            batch_sizes = sizes[role.partner]
+    pending_msgs = [0]
     xflags = M.XFER_DEDUP | M.XFER_ASYNC | getattr(M, PATHS[args.xfer_path])
     if role.kind == "P" and not args.no_pipeline:
         # cross-process: each copy is enqueued at the next call, right after
@@ -288,6 +297,8 @@ def run_ours(args, rank, world, dist):
             D.delete(prompt)
 
     def step(bi, io=None):
+        if role.kind == "D":
+            pending_msgs[0] = batch_sizes[bi % len(batch_sizes)]
         if role.kind == "PD":
             # no host sync between steps: step k's copies stream on while the
             # host issues step k+1 (stream order keeps every reuse of a block
@@ -303,12 +314,19 @@ def run_ours(args, rank, world, dist):
         if mark != bi:
             raise RuntimeError(f"decode rank {rank}: expected mark {bi}, got {mark}")
         done = []
-        while True:
+        while len(done) < pending_msgs[0]:    # this batch's messages (not the next one's)
             m = D.recv_poll()
             if m is None:
-                break
+                raise RuntimeError(f"decode rank {rank}: batch {bi} short of messages")
             done.append((np.frombuffer(m[2], dtype=np.int32), m[3]))
-        d_retire(done)       # host-side; stream order protects reused blocks
+        # retire the batch (host-side; stream order protects reused blocks),
+        # answering the sender's next requests between prompts, as a serving
+        # engine interleaves its own work with the pool's service loop
+        D.free_mem(np.concatenate([f[len(p) // B:] for p, f in done]))
+        for k, (prompt, _) in enumerate(done):
+            D.delete(prompt)
+            if k % 4 == 3:
+                D.serve(timeout_ms=0, until_mark=False)
         return 0
 
     def barrier():

@@ -235,6 +235,7 @@ struct PendingTx {
   uint64_t start_stamp = 0;
   std::vector<mpi::Node*> pinned;  // indexed sources, pinned until enqueued
   int64_t nm = 0;
+  uint64_t bytes = 0;              // payload of the (merged) copy
 };
 
 }  // namespace mp

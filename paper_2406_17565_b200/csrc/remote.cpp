@@ -664,7 +664,10 @@ mp_status remote_transmit(mp_pool* src, RemotePeer* r, uint32_t path, int j0, in
   // stores into the receiver's fresh blocks follow its allocation and every
   // earlier use of them there (its prepare flag, raised by its data stream
   // before the reply); the STAGED ring is ordered by its slot flags instead
-  if (!staged || !ds.empty())
+  // (no device wait if the host already sees the flag raised: the receiver
+  // raised it from its host, its data stream being idle)
+  if ((!staged || !ds.empty()) &&
+      (int32_t)(__atomic_load_n(r->out_sync->h + kSyncPrep, __ATOMIC_ACQUIRE) - prep_seq) < 0)
     TRY(stream_wait_geq(src->stream, r->out_sync->d + kSyncPrep, prep_seq));
   const int64_t n = (int64_t)hs.size();
   if (n > 0 && (path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED)) {
@@ -836,8 +839,17 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   const uint64_t s1 = ++c->next_req;
   publish(c->req(), kind == 1 ? REQ_TWI : REQ_XFER, 0, wr.len, s1);
   // the previous call's pipelined copy is launched while the peer prepares
-  // this one (before any inbound request is served: wait_reply may serve)
-  const mp_status fs = remote_flush_tx(src);
+  // this one (before any inbound request is served: wait_reply may serve),
+  // unless this transfer may join it (same peer, path and layers, payload
+  // under the pool's coalescing limit, no inbound transfer stamped since it
+  // started -- wait_reply serves only requests stamped after this start)
+  PendingTx* pt = src->pend_tx;
+  const bool may_merge =
+      pt && one_trip && (flags & MP_XFER_PIPELINE) && src->coalesce && pt->r == r &&
+      pt->path == path && (path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED) &&
+      pt->j0 == j0 && pt->nj == nj && pt->start_stamp == start_stamp &&
+      pt->bytes + (uint64_t)n * (uint64_t)nj * (uint64_t)src->chunk <= src->batch_limit;
+  const mp_status fs = may_merge ? MP_OK : remote_flush_tx(src);
   mp_status st = wait_reply(src, c, s1);
   if (st == MP_OK && fs != MP_OK) st = fs;
   if (tm) {
@@ -908,7 +920,32 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
         }
       }
     }
-    if (one_trip && (flags & MP_XFER_PIPELINE) && xs == MP_OK) {
+    PendingTx* pm = src->pend_tx;
+    if (pm && may_merge && xs == MP_OK) {
+      // one launch for both unless a destination block repeats (the peer
+      // freed and re-allocated a block of the pending copy: stream order
+      // between the two copies must decide it)
+      std::vector<int32_t> a(pm->hd);
+      a.insert(a.end(), pm->dd.begin(), pm->dd.end());
+      std::sort(a.begin(), a.end());
+      bool clash = false;
+      for (int32_t d : hd) clash = clash || std::binary_search(a.begin(), a.end(), d);
+      for (int32_t d : dd_) clash = clash || std::binary_search(a.begin(), a.end(), d);
+      if (clash) xs = remote_flush_tx(src);
+    }
+    pm = src->pend_tx;
+    if (pm && xs == MP_OK) {  // merge: the later prepare / done values cover both
+      pm->hs.insert(pm->hs.end(), hs.begin(), hs.end());
+      pm->hd.insert(pm->hd.end(), hd.begin(), hd.end());
+      pm->ds.insert(pm->ds.end(), ds_.begin(), ds_.end());
+      pm->dd.insert(pm->dd.end(), dd_.begin(), dd_.end());
+      pm->prep_seq = prep_seq;
+      pm->done_seq = done_seq;
+      pm->pinned.insert(pm->pinned.end(), pinned.begin(), pinned.end());
+      pinned.clear();
+      pm->nm += nm;
+      pm->bytes += (uint64_t)nm * (uint64_t)nj * (uint64_t)src->chunk;
+    } else if (one_trip && (flags & MP_XFER_PIPELINE) && xs == MP_OK) {
       // enqueued by this pool's next call (remote_flush_tx); the indexed
       // sources stay pinned until then
       PendingTx* t = new PendingTx();
@@ -925,6 +962,7 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
       t->start_stamp = start_stamp;
       t->pinned.swap(pinned);
       t->nm = nm;
+      t->bytes = (uint64_t)nm * (uint64_t)nj * (uint64_t)src->chunk;
       src->pend_tx = t;
     } else {
       xs = transmit_step(src, r, path, j0, nj, hs, hd, ds_, dd_, geom, slot0, slot_end, prep_seq,
