@@ -97,8 +97,12 @@ typedef enum {
  * is enqueued by this pool's NEXT library call -- right after that call's own
  * request is sent, so the launch overlaps the next round trip -- or by any
  * call other than mp_match / mp_recv_poll / the getters and dumps, which
- * enqueue it before anything else.  Until then the peer's later device work
- * on those blocks waits; a sender that stops calling must call mp_sync. */
+ * enqueue it before anything else.  Consecutive pipelined FUSED transfers to
+ * the same peer (same layers, no inbound transfer in between, no destination
+ * block repeated) join the pending copy -- one launch per coalescing limit
+ * (coalesce_mib) instead of one per transfer.  Until it is enqueued the
+ * peer's later device work on those blocks waits; a sender that stops
+ * calling must call mp_sync. */
 #define MP_XFER_PIPELINE (1u << 3)
 #define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
 #define MP_MATCH_PIN (1u << 5)      /* match: pin matched blocks until mp_unpin (R12) */

@@ -627,10 +627,15 @@ mp_status remote_apply_waits(mp_pool* p, const RemotePeer* skip) {
 
 mp_status remote_serve_once(mp_pool* p, int64_t* served) {
   *served = 0;
-  TRY(remote_flush_tx(p));  // before this pool's stream sees any inbound work
   for (auto& kv : p->remotes) {
     RemotePeer* r = kv.second;
     if (!r->in) continue;
+    // a pipelined copy is enqueued before this pool's stream sees any
+    // inbound work (only when a request is actually waiting: an idle poll
+    // inside wait_reply must not break up a merge)
+    if (p->pend_tx &&
+        __atomic_load_n(&r->in->req()->seq, __ATOMIC_ACQUIRE) > r->in->seen_req)
+      TRY(remote_flush_tx(p));
     mp_status s = serve_message(p, r);
     if (s == MP_OK) ++*served;
     else if (s != MP_ERR_PRECONDITION) return s;
@@ -1288,6 +1293,7 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
 mp_status mp_serve(mp_pool* p, int64_t timeout_ms, int32_t until_mark, int64_t* served,
                    int32_t* mark) {
   if (!p) return MP_ERR_CONFIG;
+  TRY(remote_flush_tx(p));  // a pipelined copy goes first (the peer may wait for it)
   const double t0 = now_s();
   int64_t total = 0;
   int spins = 0;
