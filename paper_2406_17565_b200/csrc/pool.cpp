@@ -678,11 +678,9 @@ const char* mp_last_error(void) { return get_err().c_str(); }
 void mp_pool_destroy(mp_pool* p) {
   if (!p) return;
   if (p->stream) {
-    remote_flush_tx(p);
+    remote_flush_tx(p);  // a pipelined copy the peer's stream may wait for
     flush_involving(p);
   }
-  delete p->pend_tx;  // only left on a failed flush
-  p->pend_tx = nullptr;
   remote_close_all(p);
   {
     DevGuard g(p->dev);

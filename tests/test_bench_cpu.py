@@ -97,3 +97,31 @@ def test_per_pair_table_gloo(world):
             assert e["frac_of_nominal_900"] == round(gbs / 900.0, 4)
             assert e["frac_of_probe"] == round(gbs / 700.0, 4)
             assert e["kernel_frac_of_probe"] == round(600.0 / 700.0, 4)
+
+
+def test_cupti_busy_union_of_intervals():
+    """bench.cupti_busy: launches, summed duration and the UNION of the
+    kernels' [start, end) intervals (overlapping PDL grids count once; other
+    kernels and host events are ignored)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from torch.autograd import DeviceType
+
+    class R:
+        def __init__(self, a, b):
+            self.start, self.end = a, b
+
+    class E:
+        def __init__(self, name, a, b, dev=DeviceType.CUDA):
+            self.name, self.time_range, self.device_type = name, R(a, b), dev
+
+    class P:
+        def events(self):
+            return [E("migrate_bulk_kernel<65536>", 0, 10), E("migrate_bulk_kernel<16384>", 8, 12),
+                    E("migrate_kernel", 20, 25), E("alloc_kernel", 12, 30),
+                    E("migrate (host op)", 0, 100, DeviceType.CPU), E("migrate_empty", 40, 40)]
+
+    n, tot, busy = bench.cupti_busy(P())
+    assert (n, tot, busy) == (3, 10 + 4 + 5, 12 + 5)
+    n, tot, busy = bench.cupti_busy(P(), None)
+    assert (n, tot, busy) == (4, 37, 30)
