@@ -927,16 +927,23 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
     }
     PendingTx* pm = src->pend_tx;
     if (pm && may_merge && xs == MP_OK) {
-      // one launch for both unless a destination block repeats (the peer
-      // freed and re-allocated a block of the pending copy: stream order
-      // between the two copies must decide it)
-      std::vector<int32_t> a(pm->hd);
-      a.insert(a.end(), pm->dd.begin(), pm->dd.end());
-      std::sort(a.begin(), a.end());
-      bool clash = false;
-      for (int32_t d : hd) clash = clash || std::binary_search(a.begin(), a.end(), d);
-      for (int32_t d : dd_) clash = clash || std::binary_search(a.begin(), a.end(), d);
-      if (clash) xs = remote_flush_tx(src);
+      // one launch for both only if (1) this transfer's prepare flag is
+      // already up: the merged copy then waits for nothing new (a prepare
+      // still queued on the peer's stream may sit behind a join on another
+      // sender's copy that waits for the pending one -- merging would close
+      // that cycle), and (2) no destination block repeats (the peer evicted
+      // and re-allocated a block of the pending copy: stream order between
+      // the two copies must decide it)
+      bool ok = (int32_t)(__atomic_load_n(r->out_sync->h + kSyncPrep, __ATOMIC_ACQUIRE) -
+                          prep_seq) >= 0;
+      if (ok) {
+        std::vector<int32_t> a(pm->hd);
+        a.insert(a.end(), pm->dd.begin(), pm->dd.end());
+        std::sort(a.begin(), a.end());
+        for (int32_t d : hd) ok = ok && !std::binary_search(a.begin(), a.end(), d);
+        for (int32_t d : dd_) ok = ok && !std::binary_search(a.begin(), a.end(), d);
+      }
+      if (!ok) xs = remote_flush_tx(src);
     }
     pm = src->pend_tx;
     if (pm && xs == MP_OK) {  // merge: the later prepare / done values cover both
