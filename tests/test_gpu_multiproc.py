@@ -765,3 +765,77 @@ def test_two_process_react_vs_oracle(seed, transport):
                 assert np.array_equal(b, pool_o.block_bytes((r, O.HBM, i))), (r, i)
                 n += 1
         assert n > 0, r
+
+
+# ---------------------------------------------------------------------------
+# MP_XFER_PIPELINE contract (include/mempool.h): the call returns after the
+# receiver's reply with the final addrs; the copy is enqueued by the sender's
+# next call -- not by mp_match -- and consecutive pipelined transfers to the
+# same peer merge into one launch; mp_sync enqueues and completes it.
+def _pipe_worker(rank, port, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import TINY as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens, 64, verify=True)
+        blobs = M.exchange_handles(pool)
+        pool.import_peer(blobs[1 - rank][1])
+        dist.barrier()
+        out = {}
+        if rank == 0:
+            src = pool.alloc_mem(12)
+            pool.debug_fill(src, 5)
+            pool.sync()
+            pool.stats_reset()
+            fl = M.XFER_ASYNC | M.XFER_PIPELINE
+            d1 = pool.transfer(1, src[:4], flags=fl)
+            out["after_first"] = pool.stats()["kernel_launches"]
+            pool.match(np.arange(40, dtype=np.int32))          # host only: no flush
+            out["after_match"] = pool.stats()["kernel_launches"]
+            d2 = pool.transfer(1, src[4:9], flags=fl)            # merges (receiver idle)
+            out["after_second"] = pool.stats()["kernel_launches"]
+            pool.sync()                                         # enqueues and completes
+            out["after_sync"] = pool.stats()["kernel_launches"]
+            d3 = pool.transfer(1, src[9:], flags=fl)
+            pool.send_mark(1, 1)                                # any other call flushes
+            out["after_mark"] = pool.stats()["kernel_launches"]
+            out["pairs"] = list(zip(M.addr_indices(src).tolist(),
+                                    M.addr_indices(np.concatenate([d1, d2, d3])).tolist()))
+            out["src"] = {int(i): pool.debug_read_block(a) for i, a in
+                          zip(M.addr_indices(src).tolist(), src)}
+            dist.barrier()
+        else:
+            _s, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+            assert mark == 1
+            pool.sync()                                         # joins the sender's copies
+            out["dst"] = {i: pool.debug_read_block(M.make_addr(1, M.HBM, i)) for i in range(12)}
+            dist.barrier()
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+def test_two_process_pipeline_contract():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30900 + (os.getpid() % 40)
+    ps = [ctx.Process(target=_pipe_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = _collect(q, ps, 300)
+    s = res[0]
+    assert s["after_first"] == 0 and s["after_match"] == 0   # still pending
+    assert s["after_second"] == 0                             # merged, still pending
+    assert s["after_sync"] == 1                               # one launch for both
+    assert s["after_mark"] == 2
+    for si, di in s["pairs"]:
+        assert np.array_equal(res[1]["dst"][di], s["src"][si]), (si, di)
