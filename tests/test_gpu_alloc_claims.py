@@ -53,14 +53,15 @@ def test_claims_cancel_and_overflow_against_device_scan():
 
 
 def test_pending_list_bound_flushes():
-    """More than 4 x kInlineIds claims pending: flushed early through the id
-    arena; the device scan afterwards still sees every claim."""
+    """Thousands of claims pending (past the queue's compaction bound): the
+    queue is compacted on the host, and the device scan afterwards applies
+    every claim and free (through the id arena) and still sees each one."""
     P, D = Twin(0, TINY, 64), Twin(1, TINY, N)
     connect(P, D)
     src = P.alloc(32)
     P.fill(src)
     a = D.alloc(2500, stream_ordered=True)
-    b = D.alloc(2500, stream_ordered=True)      # 5000 pending > 4000: early flush
+    b = D.alloc(2500, stream_ordered=True)      # 5000 pending: compacted on the host
     D.free(a[::3])                              # frees of applied claims
     got = transfer(P, D, src)                   # device scan: lowest free ids
     assert sorted(x[2] for x in got) == sorted(x[2] for x in a[::3])[:32]
