@@ -4,8 +4,8 @@ claim reaches the device bitmap only with the next stream-ordered update,
 while a transfer's receiver allocates on the device (lowest-first scan, R2).
 Seeded sequences drive every case of that bookkeeping -- claims and frees
 that cancel before they are applied, more pending updates than fit in a
-launch's parameters (the id-arena upload), the bounded pending list's early
-flush -- and every receiver allocation is compared with the oracle's
+launch's parameters (the id-arena upload), the pending list's host-side
+compaction -- and every receiver allocation is compared with the oracle's
 lowest-first choice, then the device bitmap with the oracle's free set."""
 import numpy as np
 import pytest
@@ -67,3 +67,30 @@ def test_pending_list_bound_flushes():
     assert sorted(x[2] for x in got) == sorted(x[2] for x in a[::3])[:32]
     D.free(b)
     D.check_state(check_bytes=False)
+
+
+def test_host_compaction_of_a_long_claim_queue():
+    """A small receiver cycled through many stream-ordered alloc / free
+    rounds with no device scan in between: the pending queue passes its bound
+    (4 x kInlineIds + 2 x blocks) several times and is compacted on the host
+    (no kernel); the next device scans still pick the oracle's lowest-first
+    ids and the bitmap equals the oracle's free set."""
+    rng = np.random.default_rng(17)
+    P, D = Twin(0, TINY, 128), Twin(1, TINY, 64)
+    connect(P, D)
+    src = P.alloc(16)
+    P.fill(src)
+    held = []
+    for rnd in range(6):
+        for _ in range(150):                    # ~300 queue entries per 150 cycles
+            k = int(rng.integers(1, 8))
+            if k <= D.o.free_count(0):
+                held += D.alloc(k, stream_ordered=True)
+            if held:
+                take = rng.random(len(held)) < 0.5
+                D.free([a for a, t in zip(held, take) if t])
+                held = [a for a, t in zip(held, take) if not t]
+        n = int(rng.integers(1, 16))
+        if n <= D.o.free_count(0):
+            held += transfer(P, D, src[:n])     # device scan after the compactions
+        D.check_state(check_bytes=False)
