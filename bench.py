@@ -249,6 +249,12 @@ def run_ours(args, rank, world, dist):
     if P is not None:
         reqs, partials = populate_prefill(P, shape, seed, n_blocks)
         batches = make_batches(reqs, partials, args.batch_blocks, B)
+    wire = None
+    if role.kind in ("P", "D"):
+        wire = wire_check(M, torch, dist, role, P if P is not None else D, shape, world, dev,
+                          getattr(M, PATHS[args.xfer_path]))
+        if not wire["ok"]:
+            raise RuntimeError(f"rank {rank}: wire check failed (bytes differ)")
 
     host_t = {"match": 0.0, "twi": 0.0, "n": 0}
     # D needs each batch's request count (it retires exactly that batch while
@@ -566,6 +572,7 @@ def run_ours(args, rank, world, dist):
                                 for k, v in host_t.items() if k != "n"},
         "roofline": roof,
         "per_pair": per_pair,
+        "wire_check": wire,
         "nvlink_peak_measured": ({"GBps_per_pair": [(r["probe"] or {}).get("GBps")
                                                     for r in recs if r["kind"] == "P"],
                                   "nominal_GBps": NVLINK_GBS,
@@ -613,6 +620,45 @@ def link_probe(torch, dist, role, dev, world, nbytes=1 << 30, reps=8):
     del buf
     torch.cuda.empty_cache()
     return out
+
+
+def wire_check(M, torch, dist, role, pool, shape, world, dev, flags, n=8):
+    """Before timing at N > 1: P_i moves n freshly filled blocks to D_i over
+    the bench's transport (synchronous transfer), both sides checksum every
+    chunk of them (weighted int64 sums, same weights on both GPUs), and the
+    sums are compared.  Returns {"blocks", "ok", ...} on every rank."""
+    L2, c, nb = 2 * shape.layers, shape.chunk_bytes, pool.hbm_blocks
+    view = pool._region.view(L2, nb, c).view(torch.int64)
+    g = torch.Generator().manual_seed(11)
+    w = torch.randint(-2**31, 2**31, (c // 8,), generator=g).to(f"cuda:{dev}")
+
+    def sums(addrs):
+        pool.sync()
+        t = torch.as_tensor(M.addr_indices(addrs).astype(np.int64), device=f"cuda:{dev}")
+        return torch.stack([(view[j][t] * w).sum(-1) for j in range(L2)], 1).cpu().tolist()
+
+    mine = None
+    if role.kind == "P":
+        src = pool.alloc_mem(n)
+        pool.debug_fill(src, 4242)
+        pool.transfer(role.d_inst, src, flags=flags)
+        mine = sums(src)
+        pool.send_mark(role.d_inst, 1 << 29)
+        pool.free_mem(src)
+    else:
+        _s, mark = pool.serve(timeout_ms=300_000, until_mark=True)
+        if mark != 1 << 29:
+            raise RuntimeError(f"wire check: unexpected mark {mark}")
+        m = pool.recv_poll()
+        mine = sums(m[3])
+        pool.free_mem(m[3])
+        pool.sync()
+    allsums = [None] * world
+    dist.all_gather_object(allsums, mine)
+    ok = allsums[role.rank] == allsums[role.partner]
+    return {"blocks": n, "ok": bool(ok),
+            "what": "P_i -> D_i transfer of freshly filled blocks over the bench's transport; "
+                    "weighted checksums of every chunk on both GPUs compared"}
 
 
 def cupti_busy(prof, match="migrate"):
