@@ -218,6 +218,32 @@ __device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// The same two copies with an L2 cache-policy hint (createpolicy), for the
+// MP_BULK_HINT measurement knob: the KV is read once and written once.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void bulk_load_hint(void* smem, const void* gmem, uint32_t bytes,
+                                               uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store_hint(void* gmem, const void* smem, uint32_t bytes,
+                                                uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::
+                   "l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
@@ -272,13 +298,15 @@ template <int kPiece, int kStages, bool kSrcPool, bool kDstPool>
 __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     Endpoint src, Endpoint dst, int j0, int nj, long long chunk, unsigned pieces_per_chunk,
     unsigned total_units, unsigned long long* ctr, unsigned long long base,
-    const __grid_constant__ InlineIds sinl, int wait_prev) {
+    const __grid_constant__ InlineIds sinl, int wait_prev, int hint) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   if (threadIdx.x != 0) return;
   for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (wait_prev) pdl_wait();
+  const uint64_t pol = hint ? l2_evict_first() : 0;
+  const bool hl = hint & 1, hs = hint & 2;  // hint the loads / the stores
   UnitSource units{ctr, base, total_units, blockIdx.x, gridDim.x};
   const char* sp;
   char* dp;
@@ -296,7 +324,8 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     dsts[k] = dp;
     lens[k] = bytes;
     mbar_expect_tx(&bars[k], bytes);
-    bulk_load(smem + (size_t)k * kPiece, sp, bytes, &bars[k]);
+    if (hl) bulk_load_hint(smem + (size_t)k * kPiece, sp, bytes, &bars[k], pol);
+    else bulk_load(smem + (size_t)k * kPiece, sp, bytes, &bars[k]);
     u = units.claim();  // in flight while the loads are
   }
   bool released = false;
@@ -309,7 +338,8 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
     const unsigned s = k % kStages;
     if (!live[s]) break;
     mbar_wait(&bars[s], (k / kStages) & 1u);
-    bulk_store(dsts[s], smem + (size_t)s * kPiece, lens[s]);
+    if (hs) bulk_store_hint(dsts[s], smem + (size_t)s * kPiece, lens[s], pol);
+    else bulk_store(dsts[s], smem + (size_t)s * kPiece, lens[s]);
     if (k >= 1) {
       const unsigned r = (k - 1) % kStages;
       live[r] = u != 0xFFFFFFFFu;
@@ -320,7 +350,8 @@ __global__ void __launch_bounds__(kBulkThreads) migrate_bulk_kernel(
         dsts[r] = dp;
         lens[r] = bytes;
         mbar_expect_tx(&bars[r], bytes);
-        bulk_load(smem + (size_t)r * kPiece, sp, bytes, &bars[r]);
+        if (hl) bulk_load_hint(smem + (size_t)r * kPiece, sp, bytes, &bars[r], pol);
+        else bulk_load(smem + (size_t)r * kPiece, sp, bytes, &bars[r]);
         u = units.claim();
         if (u == 0xFFFFFFFFu && !released) {
           pdl_release();
@@ -472,7 +503,7 @@ template <int kPieceT, int kStagesT>
 static cudaError_t preload_bulk() {
   const int smem = kStagesT * kPieceT;
   void (*ks[4])(Endpoint, Endpoint, int, int, long long, unsigned, unsigned,
-                unsigned long long*, unsigned long long, const InlineIds, int) = {
+                unsigned long long*, unsigned long long, const InlineIds, int, int) = {
       migrate_bulk_kernel<kPieceT, kStagesT, true, true>,
       migrate_bulk_kernel<kPieceT, kStagesT, true, false>,
       migrate_bulk_kernel<kPieceT, kStagesT, false, true>,
@@ -552,9 +583,13 @@ static cudaError_t launch_bulk(const Endpoint& src, const Endpoint& dst, int n, 
   }
   const int grid = (int)(total < (unsigned long long)cap ? total : (unsigned long long)cap);
   const bool dyn = sched && sched->ctr && bulk_dynamic();
+  static const int hint = [] {  // MP_BULK_HINT=1: L2 evict_first on loads and stores, 2: loads, 3: stores
+    const char* e = getenv("MP_BULK_HINT");
+    return (e && e[0] >= '1' && e[0] <= '3') ? (e[0] == '1' ? 3 : e[0] == '2' ? 1 : 2) : 0;
+  }();
   const cudaError_t e = launch_pdl(kern, grid, kBulkThreads, smem, stream, src, dst, j0, nj, chunk,
                                    pieces, (unsigned)total, dyn ? sched->ctr : nullptr,
-                                   dyn ? *sched->base : 0ull, sinl, wait_prev ? 1 : 0);
+                                   dyn ? *sched->base : 0ull, sinl, wait_prev ? 1 : 0, hint);
   if (dyn && e == cudaSuccess) *sched->base += total + (unsigned long long)grid;
   return e;
 }
