@@ -32,6 +32,9 @@ TRANSPORTS = {
     # ASYNC transfers enqueue their copy at the sender's next call
     # (MP_XFER_PIPELINE), after that call's request went out
     "fused-pipelined": ({}, "PATH_FUSED|XFER_PIPELINE"),
+    "peer-vector-pipelined": ({"force_peer": True, "peer_engine": 1, "peer_sched": 1},
+                              "PATH_FUSED|XFER_PIPELINE"),
+    "ce-pipelined": ({}, "PATH_CE|XFER_PIPELINE"),
 }
 
 
