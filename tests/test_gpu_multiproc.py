@@ -842,3 +842,100 @@ def test_two_process_pipeline_contract():
     assert s["after_mark"] == 2
     for si, di in s["pairs"]:
         assert np.array_equal(res[1]["dst"][di], s["src"][si]), (si, di)
+
+
+# ---------------------------------------------------------------------------
+# Edge cases of the cross-process protocol, each against the oracle replayed
+# in the parent: an empty transfer, a DEDUP transfer that moves nothing, a
+# receiver out of memory (error, no state change, sequence numbers intact),
+# then ordinary transfers -- synchronous, ASYNC and pipelined.
+_EDGE_FLAGS = [0, "ASYNC", "ASYNC|PIPELINE"]
+
+
+def _edge_worker(rank, port, q, mode):
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2406_17565_b200 import mempool as M
+        from workloads.configs import TINY as S
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        fl = 0 if mode == 0 else sum(getattr(M, "XFER_" + x) for x in mode.split("|"))
+        pool = M.Pool(rank, 0, S.layers, S.kv_heads, S.head_dim, S.block_tokens,
+                      64 if rank == 0 else 16, verify=True)
+        blobs = M.exchange_handles(pool)
+        pool.import_peer(blobs[1 - rank][1])
+        dist.barrier()
+        out = {}
+        if rank == 0:
+            res = []
+            src = pool.alloc_mem(40)
+            pool.debug_fill(src, 3)
+            t = np.arange(3, 3 + 64, dtype=np.int32)           # 4 full blocks
+            res.append(("empty", M.addr_indices(pool.transfer(1, src[:0], flags=fl)).tolist()))
+            fin, nm = pool.transfer_with_insert(1, t, src[:4], flags=fl | M.XFER_DEDUP)
+            res.append(("twi", M.addr_indices(fin).tolist(), nm))
+            fin, nm = pool.transfer_with_insert(1, t, src[:4], flags=fl | M.XFER_DEDUP)
+            res.append(("twi_dedup_all", M.addr_indices(fin).tolist(), nm))
+            try:
+                pool.transfer(1, src[4:24], flags=fl)            # 20 > 12 free at D
+                res.append(("oom", "no error"))
+            except M.MempoolError as e:
+                res.append(("oom", e.name))
+            d = pool.transfer(1, src[24:30], flags=fl)
+            res.append(("after", M.addr_indices(d).tolist()))
+            pool.send_mark(1, 1)
+            out["res"] = res
+            out["src"] = {i: pool.debug_read_block(src[i]) for i in list(range(4)) + list(range(24, 30))}
+        else:
+            _s, mark = pool.serve(timeout_ms=120_000, until_mark=True)
+            assert mark == 1
+            pool.sync()
+            out["states"] = pool.block_states(M.HBM).tolist()
+            out["dump"] = pool.dump_index()
+            out["bytes"] = {i: pool.debug_read_block(M.make_addr(1, M.HBM, i))
+                            for i, st in enumerate(out["states"]) if st}
+        dist.barrier()
+        pool.close()
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except Exception as e:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+@pytest.mark.parametrize("mode", _EDGE_FLAGS)
+def test_two_process_edges_vs_oracle(mode):
+    import oracle as O
+    from workloads.configs import TINY as S
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31100 + (os.getpid() % 30) + 3 * _EDGE_FLAGS.index(mode)
+    ps = [ctx.Process(target=_edge_worker, args=(r, port, q, mode)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = _collect(q, ps, 300)
+    mk = lambda inst, n: O.OraclePool(inst, S.layers, S.kv_heads, S.head_dim,  # noqa: E731
+                                      S.block_tokens, n, seed=3)
+    P, D = mk(0, 64), mk(1, 16)
+    src = P.alloc_mem(40, O.HBM)
+    P.fill(src)
+    t = np.arange(3, 3 + 64, dtype=np.int32)
+    want = [("empty", [a[2] for a in O.transfer(P, D, src[:0])])]
+    for tag in ("twi", "twi_dedup_all"):
+        fin, nm, _ = O.transfer_with_insert(P, D, t, src[:4], flags=O.FLAG_DEDUP)
+        want.append((tag, [a[2] for a in fin], nm))
+    try:
+        O.transfer(P, D, src[4:24])
+        want.append(("oom", "no error"))
+    except O.MPError as e:
+        want.append(("oom", e.name))
+    want.append(("after", [a[2] for a in O.transfer(P, D, src[24:30])]))
+    assert [list(x) for x in got[0]["res"]] == [list(x) for x in want]
+    smap = {O.FREE: 0, O.ACTIVE: 1, O.INDEXED: 2, O.ORPHAN: 3}
+    assert got[1]["states"] == [smap[x] for x in D.state[O.HBM]]
+    assert got[1]["dump"] == D.dump_index()
+    for i, b in got[1]["bytes"].items():
+        assert np.array_equal(b, D.block_bytes((1, O.HBM, i))), i
