@@ -204,6 +204,7 @@ struct RemotePeer {
   char* ring = nullptr;           // receiver side: my inbound ring for this peer
   int64_t ring_bytes = 0;
   uint64_t ring_id = 0;
+  cudaIpcMemHandle_t ring_hnd{};  // taken once, when the ring is allocated
   char* peer_ring = nullptr;      // sender side: the peer's inbound ring for me
   uint64_t peer_ring_id = 0;
   uint32_t out_slot = 0, in_slot = 0;  // slot sequence numbers per direction

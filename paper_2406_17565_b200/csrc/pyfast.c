@@ -131,6 +131,7 @@ static PyObject* py_match(PyObject* self, PyObject* args) {
   unsigned int flags;
   int B;
   if (!PyArg_ParseTuple(args, "OOIi", &h, &t, &flags, &B)) return NULL;
+  if (B <= 0) return raise_status(MP_ERR_CONFIG, "match"); /* block size sizes the output */
   PyArrayObject* ta = as_flat(t, NPY_INT32);
   if (!ta) return NULL;
   const int64_t nt = (int64_t)PyArray_SIZE(ta);
@@ -241,6 +242,7 @@ static PyObject* py_transfer_with_insert(PyObject* self, PyObject* args) {
   unsigned int flags;
   if (!PyArg_ParseTuple(args, "OiOOOIOi", &h, &dst_inst, &t, &s, &d, &flags, &priv, &B))
     return NULL;
+  if (B <= 0) return raise_status(MP_ERR_CONFIG, "transfer_with_insert");
   PyArrayObject* ta = as_flat(t, NPY_INT32);
   if (!ta) return NULL;
   PyArrayObject* sa = as_flat(s, NPY_UINT64);

@@ -338,6 +338,15 @@ mp_status staged_recv(mp_pool* p, RemotePeer* r, const DstPrep& st, const uint8_
   if (!r->ring) {  // first STAGED transfer from this peer: its inbound ring
     r->ring_bytes = std::min(p->staging_bytes, r->staging_bytes);
     CK(cudaMalloc(&r->ring, (size_t)r->ring_bytes));
+    // the handle travels in every STAGED reply: taken here, before anything
+    // is enqueued, so the reply itself cannot fail after the unpacks are
+    if (cudaIpcGetMemHandle(&r->ring_hnd, r->ring) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(r->ring);
+      r->ring = nullptr;
+      set_err("cudaIpcGetMemHandle of the inbound ring failed");
+      return MP_ERR_CUDA;
+    }
     r->ring_id = new_uid();
     CK(cudaStreamCreateWithFlags(&r->recv_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&r->recv_dep, cudaEventDisableTiming));
@@ -477,9 +486,7 @@ mp_status serve_message(mp_pool* p, RemotePeer* r) {
         wr.put<uint32_t>(prep_seq);
         wr.put<uint32_t>(done_seq);
         if (staged) {
-          cudaIpcMemHandle_t hnd;
-          if (cudaIpcGetMemHandle(&hnd, r->ring) != cudaSuccess) rstatus = MP_ERR_CUDA;
-          wr.bytes(&hnd, sizeof(hnd));
+          wr.bytes(&r->ring_hnd, sizeof(r->ring_hnd));
           wr.put<uint64_t>(r->ring_id);
           wr.put<uint32_t>(slot0);
         }
