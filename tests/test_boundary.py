@@ -78,6 +78,9 @@ def test_fast_binding_loads_and_reports_status():
         lambda: F.transfer(0, 1, [1], None, 0, 0, 2, None),
         lambda: F.transfer_with_insert(0, 1, toks, [1, 2, 3], None, 0, b"x", 16),
         lambda: F.sync(0),
+        # a non-positive block size sizes no output: rejected, no division
+        lambda: F.match(0, toks, 0, 0),
+        lambda: F.transfer_with_insert(0, 1, toks, [1], None, 0, None, -16),
     ]
     for c in calls:
         with pytest.raises(M.MempoolError) as e:
