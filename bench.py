@@ -429,8 +429,15 @@ def run_ours(args, rank, world, dist):
                        if st["timed_bytes"] else 0.0)
     payload_per_launch = st["timed_bytes"] / max(st["timed_launches"], 1)
     same_gpu = role.kind == "PD" or args.device >= 0   # --device: every rank on one GPU
-    # engine: auto = the bulk ring within one pool's GPU, vector LD/ST for peer stores
-    bulk = args.copy_kernel == 2 or (args.copy_kernel == 0 and role.kind == "PD")
+    # engine the library picks (pool.cpp launch_migrate_timed): copies within
+    # one GPU's HBM -- loopback, or an IPC peer on the same GPU -- take
+    # copy_kernel (auto = the bulk ring); stores into another GPU take
+    # peer_engine (auto = vector LD/ST unless MP_PEER_ENGINE=bulk)
+    if same_gpu:
+        bulk = args.copy_kernel != 1
+    else:
+        eng = args.peer_engine or args.copy_kernel
+        bulk = eng == 2 or (eng == 0 and os.environ.get("MP_PEER_ENGINE", "").startswith("b"))
     kname = "migrate_bulk_kernel" if bulk else "migrate_kernel"
     if same_gpu:
         # loopback: the kernel reads Pb and writes Pb of HBM per block
@@ -462,7 +469,7 @@ def run_ours(args, rank, world, dist):
         dist.all_gather_object(recs, rec)
     per_pair = pair_table(recs, Pb)
     ratio, ratio_src = (ncu_traffic_ratio("bulk" if bulk else "vector")
-                        if role.kind == "PD" else (None, None))
+                        if same_gpu else (None, None))
     roof.update({
         "achieved": round(achieved, 1) if achieved else None, "unit": "GB/s",
         "frac": round(achieved / roof["peak"], 4) if achieved else None,
