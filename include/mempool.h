@@ -102,7 +102,11 @@ typedef enum {
  * block repeated) join the pending copy -- one launch per coalescing limit
  * (coalesce_mib) instead of one per transfer.  Until it is enqueued the
  * peer's later device work on those blocks waits; a sender that stops
- * calling must call mp_sync. */
+ * calling must call mp_sync.  Cross-process MP_XFER_ASYNC (FUSED / CE)
+ * commits at the receiver in the one round trip, before the copy is
+ * enqueued: if the sender's enqueue then fails (MP_ERR_CUDA, the only way it
+ * can), the receiver's index already names the blocks and both pools are in
+ * the unspecified state of MP_ERR_CUDA (the peer's waits are released). */
 #define MP_XFER_PIPELINE (1u << 3)
 #define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
 #define MP_MATCH_PIN (1u << 5)      /* match: pin matched blocks until mp_unpin (R12) */
