@@ -104,8 +104,8 @@ typedef enum {
  * peer's later device work on those blocks waits; a sender that stops
  * calling must call mp_sync.  Cross-process MP_XFER_ASYNC (FUSED / CE)
  * commits at the receiver in the one round trip, before the copy is
- * enqueued: if the sender's enqueue then fails (MP_ERR_CUDA, the only way it
- * can), the receiver's index already names the blocks and both pools are in
+ * enqueued: if the sender's enqueue then fails (a CUDA error in practice:
+ * the id arena cannot run short), the receiver's index already names the blocks and both pools are in
  * the unspecified state of MP_ERR_CUDA (the peer's waits are released). */
 #define MP_XFER_PIPELINE (1u << 3)
 #define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
