@@ -105,8 +105,9 @@ typedef enum {
  * calling must call mp_sync.  Cross-process MP_XFER_ASYNC (FUSED / CE)
  * commits at the receiver in the one round trip, before the copy is
  * enqueued: if the sender's enqueue then fails (a CUDA error in practice:
- * the id arena cannot run short), the receiver's index already names the blocks and both pools are in
- * the unspecified state of MP_ERR_CUDA (the peer's waits are released). */
+ * the id arena cannot run short), the receiver's index already names the
+ * blocks, and both pools are in the unspecified state of MP_ERR_CUDA (the
+ * peer's waits are released). */
 #define MP_XFER_PIPELINE (1u << 3)
 #define MP_INS_ERR_ON_CONFLICT (1u << 4) /* insert: CONFLICT instead of keep-existing (R4) */
 #define MP_MATCH_PIN (1u << 5)      /* match: pin matched blocks until mp_unpin (R12) */
