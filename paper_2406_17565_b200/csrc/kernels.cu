@@ -389,7 +389,7 @@ static cudaError_t launch_pdl(void (*kern)(Exp...), int grid, int block, size_t 
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
-// Single CTA of 1024 threads: popcount per thread-range of words, block-wide
+// Single CTA (launched with 256 threads): popcount per thread-range of words, block-wide
 // exclusive scan, then every thread emits its lowest set bits in order, so
 // the ids come out ascending (R2 lowest-first).
 // One pending bitmap update: id >= 0 frees (bit := 1), -(id+1) claims (bit := 0).
