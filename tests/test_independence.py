@@ -80,3 +80,14 @@ def test_bench_uses_the_oracle_only_in_its_cpu_legs():
     assert users, "bench.py's cpu_baseline leg should time the oracle"
     for name in users:
         assert re.search(r"cpu|reference|oracle", name, re.I), name
+
+
+def test_missing_native_code_fails_loudly(tmp_path):
+    """No CPU fallback: without the built library or binding the product
+    path raises instead of computing anything."""
+    import pytest
+    from paper_2406_17565_b200 import mempool as M
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        M.load_library(str(tmp_path / "libmempool.so"))
+    with pytest.raises(ImportError, match="_mpfast binding not found"):
+        M.load_fast(str(tmp_path))
