@@ -273,10 +273,13 @@ mp_status transmit_hbm(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
 
 // Sources swapped out to the source's pinned DRAM (memory asymmetry,
 // "the fastest link with the least data copies"): the DRAM block
-// is already aggregated, so one kernel reads it over PCIe and
-// scatters its chunks straight into the destination blocks -- no bounce
-// through the source's HBM.  Runs on the destination's GPU when both pools
-// share it, else on the source's GPU storing over NVLink.
+// is already aggregated, so its chunks cross PCIe once and are
+// scattered straight into the destination blocks -- no swap_in, no index
+// rewrite on the source.  Default: the copy engine moves them into the
+// source's staging and a kernel scatters each slot (dram_ce_scatter, ~55
+// GB/s); without staging room, or with MP_DRAM_SOURCE=sm, one kernel reads
+// the mapped DRAM directly (~51 GB/s).  Runs on the destination's GPU when
+// both pools share it, else on the source's GPU storing over NVLink.
 mp_status transmit_dram(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
                         const std::vector<int32_t>& dids, int j0, int nj) {
   const int64_t n = (int64_t)sids.size();
@@ -293,18 +296,22 @@ mp_status transmit_dram(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& 
     TRY(link(dst, src));
   {
     DevGuard g(ex->dev);
-    int *ds = nullptr, *dd = nullptr;
-    mpk::InlineIds si;
-    TRY(src_ids(ex, sids, &ds, &si));
-    TRY(upload_ids(ex, dids, &dd));
     char** dslabs = dst->d_slabs;
     if (!same_dev) {
       auto it = src->peer_tables.find(dst->inst);
       if (it == src->peer_tables.end()) return MP_ERR_DST_UNREACHABLE;
       dslabs = it->second;
     }
-    TRY(launch_migrate_timed(ex, ex->stream, agg_ep(base, src->Pb, ds), pool_ep(dslabs, dd), n,
-                             j0, nj, /*peer=*/!same_dev, 0, si.n ? &si : nullptr));
+    if (dram_source_ce(src, nj)) {
+      TRY(dram_ce_scatter(src, ex, ex->stream, dslabs, sids, dids, j0, nj, !same_dev));
+    } else {
+      int *ds = nullptr, *dd = nullptr;
+      mpk::InlineIds si;
+      TRY(src_ids(ex, sids, &ds, &si));
+      TRY(upload_ids(ex, dids, &dd));
+      TRY(launch_migrate_timed(ex, ex->stream, agg_ep(base, src->Pb, ds), pool_ep(dslabs, dd),
+                               n, j0, nj, /*peer=*/!same_dev, 0, si.n ? &si : nullptr));
+    }
     ex->stats.blocks_moved += (uint64_t)n;
   }
   return same_dev ? link(dst, src) : link(src, dst);

@@ -389,6 +389,68 @@ mp_status flush_batch(mp_pool* dst) {
   return MP_OK;
 }
 
+// Memory asymmetry ("the fastest link with the least data
+// copies"): the copy engine reads pinned DRAM at ~55 GB/s where SM loads of
+// mapped host memory reach ~51 (profiles/sweep_r02_dram_source*.json), and
+// the staging bounce costs HBM bandwidth only (two passes of Pb at TB/s).
+// MP_DRAM_SOURCE=sm keeps the zero-copy kernel (measurement knob).
+bool dram_source_ce(const mp_pool* src, int nj) {
+  const char* e = getenv("MP_DRAM_SOURCE");
+  if (e && e[0] == 's') return false;
+  return src->staging && src->staging_bytes >= (int64_t)nj * src->chunk;
+}
+
+mp_status dram_ce_scatter(mp_pool* src, mp_pool* ex, cudaStream_t s, char** dslabs,
+                          const std::vector<int32_t>& sids, const std::vector<int32_t>& dids,
+                          int j0, int nj, bool peer) {
+  const int64_t n = (int64_t)sids.size();
+  if (n == 0) return MP_OK;
+  const int64_t per = (int64_t)nj * src->chunk;  // chunks [j0, j0+nj) of a block: one run
+  const int64_t cap = src->staging_bytes / per;
+  if (cap < 1) {
+    set_err("staging smaller than one block");
+    return MP_ERR_CONFIG;
+  }
+  // two slots: the H2D of one overlaps the scatter of the other; a slot of at
+  // most a quarter of the transfer, so the first scatter starts early, and
+  // its destination ids fit the launch parameters
+  const int halves = cap >= 2 ? 2 : 1;
+  const int64_t k = std::min<int64_t>(
+      std::min<int64_t>(cap / halves, std::max<int64_t>(1, (n + 3) / 4)), mpk::kInlineIds);
+  DevGuard g(src->dev);
+  TRY(staging_acquire(src, src->copy_stream));  // earlier STAGED / swap users of the staging
+  // every earlier device op of the source (e.g. a zero-copy swap_out still
+  // writing these DRAM blocks) goes first
+  CK(cudaEventRecord(src->swap_ev[0], src->stream));
+  CK(cudaStreamWaitEvent(src->copy_stream, src->swap_ev[0], 0));
+  const bool whole = j0 == 0 && nj == src->nch;
+  for (int64_t b0 = 0, r = 0; b0 < n; b0 += k, ++r) {
+    const int64_t nb = std::min(n - b0, k);
+    const int h = (int)(r % halves);
+    char* stg = src->staging + (int64_t)h * k * per;
+    if (r >= halves) CK(cudaStreamWaitEvent(src->copy_stream, src->swap_ev[2 + h], 0));
+    for (int64_t i = 0; i < nb;) {
+      int64_t j = i + 1;  // whole blocks: a run of consecutive DRAM blocks is one copy
+      while (whole && j < nb && sids[(size_t)(b0 + j)] == sids[(size_t)(b0 + j - 1)] + 1) ++j;
+      CK(cudaMemcpyAsync(stg + i * per,
+                         src->dram + (int64_t)sids[(size_t)(b0 + i)] * src->Pb +
+                             (int64_t)j0 * src->chunk,
+                         (size_t)(per * (j - i)), cudaMemcpyHostToDevice, src->copy_stream));
+      i = j;
+    }
+    CK(cudaEventRecord(src->swap_ev[h], src->copy_stream));
+    CK(cudaStreamWaitEvent(s, src->swap_ev[h], 0));
+    mpk::InlineIds di;  // source = the slot itself (block i at i * per)
+    di.n = 0;
+    di.nd = (int)nb;
+    std::memcpy(di.ids, dids.data() + b0, (size_t)nb * sizeof(int32_t));
+    TRY(launch_migrate_timed(ex, s, agg_ep(stg, per, nullptr), pool_ep(dslabs, nullptr), nb, j0,
+                             nj, peer, 0, &di, /*meta_dep=*/false));
+    CK(cudaEventRecord(src->swap_ev[2 + h], s));
+  }
+  return MP_OK;
+}
+
 mp_status flush_involving(mp_pool* p) {
   if (p->batch.count) TRY(flush_batch(p));
   for (auto& kv : p->peers)

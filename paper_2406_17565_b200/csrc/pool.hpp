@@ -424,6 +424,16 @@ inline bool pair_inline(const std::vector<int32_t>& sids, const std::vector<int3
   return true;
 }
 
+// Sources in `src`'s pinned DRAM -> destination blocks `dids` (slab table
+// `dslabs`: src's peer pool, or an IPC-mapped one when `peer`), through the
+// copy engine: H2D of the aggregated blocks into src's staging on its copy
+// stream, double-buffered against one scatter per slot on stream `s` of
+// pool `ex` (same device as src).  Used when dram_source_ce(src, nj).
+bool dram_source_ce(const mp_pool* src, int nj);
+mp_status dram_ce_scatter(mp_pool* src, mp_pool* ex, cudaStream_t s, char** dslabs,
+                          const std::vector<int32_t>& sids, const std::vector<int32_t>& dids,
+                          int j0, int nj, bool peer);
+
 // Launch coalescing (same-device fused transfers).
 mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& sids,
                        const std::vector<int32_t>& dids, const int* d_dst, int j0, int nj);

@@ -732,7 +732,11 @@ mp_status remote_transmit(mp_pool* src, RemotePeer* r, uint32_t path, int j0, in
       CK(cudaEventRecord(src->slot_ev[(size_t)slot], src->copy_stream));
     }
   }
-  if (!ds.empty()) {
+  if (!ds.empty() && dram_source_ce(src, nj)) {
+    // copy engine into our staging, scattered into the receiver's blocks
+    TRY(dram_ce_scatter(src, src, src->stream, r->d_slabs, ds, dd, j0, nj,
+                        /*peer=*/!r->same_device));
+  } else if (!ds.empty()) {
     int *d_s = nullptr, *d_d = nullptr;
     mpk::InlineIds si;
     TRY(src_ids(src, ds, &d_s, &si));

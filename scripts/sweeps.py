@@ -181,9 +181,10 @@ def swap_sweep():
 
 def dram_source_sweep():
     """SURVEY f1 (memory asymmetry): historical KV swapped out to the
-    sender's pinned DRAM goes straight into the receiver's HBM (one kernel
-    reading mapped host memory), vs the two-step alternative swap_in + HBM
-    transfer.  Payload GB/s, synchronous calls, loopback receiver."""
+    sender's pinned DRAM goes straight into the receiver's HBM (copy engine
+    into the sender's staging + a scatter per slot, or one kernel reading
+    mapped host memory), vs the two-step alternative swap_in + HBM transfer.
+    Payload GB/s, synchronous calls, loopback receiver."""
     seed = seed_for(4)
     P = pool(0, 1024, dram_blocks=1024)
     D = pool(1, 1024)
@@ -196,18 +197,25 @@ def dram_source_sweep():
     rng = np.random.default_rng(seed)
     out = {"workload": "Llama-2-7B blocks (8 MiB) in the sender's pinned DRAM -> receiver "
                        "HBM on one B200, synchronous calls", "results": []}
-    for n in (1, 16, 128, 256):
-        best = None
-        for _ in range(3):       # direct: the DRAM blocks stay where they are
-            sel = dram[np.sort(rng.permutation(len(dram))[:n])]
-            t0 = time.perf_counter()
-            d = P.transfer(1, sel)
-            t1 = time.perf_counter()
-            D.free_mem(d)
-            best = t1 - t0 if best is None else min(best, t1 - t0)
-        out["results"].append({"mode": "direct_dram_to_peer_hbm", "n": n,
-                               "GBps": round(n * Pb / best / 1e9, 2), "ms": round(best * 1e3, 3)})
-        print(json.dumps(out["results"][-1]), file=sys.stderr)
+    # direct (the DRAM blocks stay where they are): the default copy-engine
+    # path (H2D into the sender's staging, scattered per slot) and the
+    # zero-copy kernel reading mapped DRAM (MP_DRAM_SOURCE=sm)
+    for mode in ("ce", "sm"):
+        os.environ["MP_DRAM_SOURCE"] = mode
+        for n in (1, 16, 128, 256):
+            best = None
+            for _ in range(3):
+                sel = dram[np.sort(rng.permutation(len(dram))[:n])]
+                t0 = time.perf_counter()
+                d = P.transfer(1, sel)
+                t1 = time.perf_counter()
+                D.free_mem(d)
+                best = t1 - t0 if best is None else min(best, t1 - t0)
+            out["results"].append({"mode": f"direct_dram_to_peer_hbm_{mode}", "n": n,
+                                   "GBps": round(n * Pb / best / 1e9, 2),
+                                   "ms": round(best * 1e3, 3)})
+            print(json.dumps(out["results"][-1]), file=sys.stderr)
+    os.environ.pop("MP_DRAM_SOURCE")
     fresh = list(dram)           # the two-step mode consumes DRAM blocks (swap_in frees them)
     for n in (1, 16, 128, 256):
         sel, fresh = np.array(fresh[:n], np.uint64), fresh[n:]

@@ -93,14 +93,20 @@ def test_private_and_transfer_layers():
     assert [M.addr_index(a) for a in kinds[-1][3]] == [x[2] for x in out]
 
 
+@pytest.mark.parametrize("dram_mode,staging", [("ce", 0), ("ce", 2), ("sm", 0)])
 @pytest.mark.parametrize("path", [M.PATH_FUSED, M.PATH_FUSED | M.XFER_ASYNC, M.PATH_STAGED,
                                   M.PATH_CE])
-def test_dram_source_memory_asymmetry(path):
+def test_dram_source_memory_asymmetry(path, dram_mode, staging, monkeypatch):
     """historical KV swapped out to DRAM goes straight from the
     source's pinned DRAM to the receiver's HBM (mixed-media source lists,
-    whole blocks and a by-layer range)."""
-    P = Twin(0, TINY, 32, 16)
-    D = Twin(1, TINY, 32, 16)
+    whole blocks and a by-layer range) -- through the copy engine and the
+    source's staging (default; `staging` blocks of room: 2 forces one-block
+    slots alternating between two halves) or one zero-copy kernel
+    (MP_DRAM_SOURCE=sm)."""
+    monkeypatch.setenv("MP_DRAM_SOURCE", dram_mode)
+    kw = dict(staging_bytes=staging * TINY.block_bytes, staging_slots=staging) if staging else {}
+    P = Twin(0, TINY, 32, 16, **kw)
+    D = Twin(1, TINY, 32, 16, **kw)
     connect(P, D)
     S, p1, p2, p3 = golden_prompts()
     for p in (p1, p2):
