@@ -1154,28 +1154,31 @@ cudaError_t sync_event_traced(const mp_pool* p, cudaEvent_t e, const char* where
   return poll_traced(p, [&] { return cudaEventQuery(e); }, where);
 }
 
+// Releases everything one peer connection opened (mappings, ring, streams,
+// mailboxes, flag pages).
+static void remote_close_one(mp_pool* p, RemotePeer* r) {
+  {
+    DevGuard g(p->dev);
+    if (r->recv_stream) cudaStreamSynchronize(r->recv_stream);
+    if (r->d_slabs) cudaFree(r->d_slabs);
+    for (void* m : r->mapped) cudaIpcCloseMemHandle(m);
+    if (r->peer_ring) cudaIpcCloseMemHandle(r->peer_ring);
+    if (r->ring) cudaFree(r->ring);
+    if (r->recv_dep) cudaEventDestroy(r->recv_dep);
+    if (r->recv_ev) cudaEventDestroy(r->recv_ev);
+    if (r->recv_stream) cudaStreamDestroy(r->recv_stream);
+  }
+  chan_close(r->out, true);
+  chan_close(r->in, true);
+  sync_close(r->out_sync);
+  sync_close(r->in_sync);
+  delete r;
+}
+
 void remote_close_all(mp_pool* p) {
   if (!p->remotes.empty()) remote_report_timing();
   host_report_timing();
-  for (auto& kv : p->remotes) {
-    RemotePeer* r = kv.second;
-    {
-      DevGuard g(p->dev);
-      if (r->recv_stream) cudaStreamSynchronize(r->recv_stream);
-      if (r->d_slabs) cudaFree(r->d_slabs);
-      for (void* m : r->mapped) cudaIpcCloseMemHandle(m);
-      if (r->peer_ring) cudaIpcCloseMemHandle(r->peer_ring);
-      if (r->ring) cudaFree(r->ring);
-      if (r->recv_dep) cudaEventDestroy(r->recv_dep);
-      if (r->recv_ev) cudaEventDestroy(r->recv_ev);
-      if (r->recv_stream) cudaStreamDestroy(r->recv_stream);
-    }
-    chan_close(r->out, true);
-    chan_close(r->in, true);
-    sync_close(r->out_sync);
-    sync_close(r->in_sync);
-    delete r;
-  }
+  for (auto& kv : p->remotes) remote_close_one(p, kv.second);
   p->remotes.clear();
 }
 
@@ -1298,9 +1301,9 @@ mp_status mp_import_peer(mp_pool* p, const void* buf, int64_t len) {
     ok = r->out_sync && r->in_sync;
   }
   if (!ok) {
+    // release what this import opened; the pool's other peers stay connected
     std::string why = std::string("import failed: ") + cudaGetErrorString(cudaGetLastError());
-    p->remotes[r->inst] = r;  // let remote_close_all release what was opened
-    remote_close_all(p);
+    remote_close_one(p, r);
     return fail(MP_ERR_CUDA, why.c_str());
   }
   p->remotes[r->inst] = r;
