@@ -743,6 +743,12 @@ void mp_pool_destroy(mp_pool* p) {
     remote_flush_tx(p);  // a pipelined copy the peer's stream may wait for
     flush_involving(p);
   }
+  {  // copies into peers' IPC-mapped blocks / rings finish before the mappings close
+    DevGuard g(p->dev);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
+    if (p->meta) cudaStreamSynchronize(p->meta);
+  }
   remote_close_all(p);
   {
     DevGuard g(p->dev);
