@@ -28,6 +28,11 @@ modes = [
     ("staged", M.PATH_STAGED, {}),
     ("ce", M.PATH_CE, {}),
     ("fused_swap_zerocopy", M.PATH_FUSED, {"swap_flags": M.SWAP_ZERO_COPY}),
+    # DRAM-resident sources through round 1's zero-copy kernel instead of the
+    # copy engine + staging scatter (env knob, read per call)
+    ("fused_async_dram_sm", M.PATH_FUSED | M.XFER_ASYNC, {"env": {"MP_DRAM_SOURCE": "sm"}}),
+    ("fused_async_small_staging", M.PATH_FUSED | M.XFER_ASYNC,
+     {"staging_blocks": 2}),
 ]
 # chunk shapes: tiny (4 KiB), ragged (1152 B: predicated tails), multi-piece
 # (45056 B = 2.75 bulk pieces / 11 vector units)
@@ -38,9 +43,17 @@ for sname, shape in shapes:
     for name, path, kw in modes:
         if sname != "tiny" and "swap" in name:
             continue
+        kw = dict(kw)
+        env = kw.pop("env", {})
+        if "staging_blocks" in kw:   # two one-block slots: every DRAM-source slot alternates
+            nb = kw.pop("staging_blocks")
+            kw.update(staging_bytes=nb * shape.block_bytes, staging_slots=nb)
+        os.environ.update(env)
         t0 = time.time()
         for s in range(n_seeds):
             T.random_ops(10_000 + 97 * s, shape, 300, path, **kw)
+        for k in env:
+            os.environ.pop(k)
         out["modes"][f"{sname}/{name}"] = {"sequences": n_seeds, "status": "bit-exact",
                                            "seconds": round(time.time() - t0, 1)}
         print(sname, name, "ok", file=sys.stderr)
