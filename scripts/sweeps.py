@@ -116,6 +116,46 @@ def transfer_sweep():
     return out
 
 
+def sm_budget_sweep():
+    """How many SMs a migration needs for a given rate: 128 scattered 7B blocks
+    (1 GiB payload) per launch, loopback, with the grid capped at max_ctas
+    CTAs (the block scheduler spreads small grids one CTA per SM).  Payload
+    GB/s over the launch's own CUDA-event time.  The NVLink question (DESIGN
+    §10: how few SMs still saturate ~775 GB/s per direction) is read off the
+    per-CTA rate while the copy is far from HBM-bound."""
+    seed = seed_for(1)
+    out = {"workload": "128 scattered Llama-2-7B blocks (1 GiB payload) per fused transfer, "
+                       "loopback on one B200, grid capped at max_ctas", "results": []}
+    for name, ck in (("vector", 1), ("bulk", 2)):
+        for cap in (4, 8, 16, 24, 32, 48, 64, 96, 148, 0):
+            P = pool(0, 1024, copy_kernel=ck, coalesce_mib=-1, max_ctas=cap)
+            D = pool(1, 1024, copy_kernel=ck, coalesce_mib=-1, max_ctas=cap)
+            M.connect(P, D)
+            src = P.alloc_mem(1024)
+            rng = np.random.default_rng(seed)
+            for _ in range(2):
+                D.free_mem(P.transfer(1, src[rng.permutation(1024)[:128]]))
+            for x in (P, D):
+                x.stats_reset()
+                x.profile(True)
+            reps = 5
+            for _ in range(reps):
+                D.free_mem(P.transfer(1, src[rng.permutation(1024)[:128]]))
+            for x in (P, D):
+                x.profile(False)
+            st = [x.stats() for x in (P, D)]
+            kms = sum(t["kernel_ms"] for t in st) / max(1, sum(t["timed_launches"] for t in st))
+            gbs = 128 * Pb / (kms * 1e-3) / 1e9
+            row = {"engine": name, "max_ctas": cap or "full wave", "kernel_ms": round(kms, 4),
+                   "payload_GBps": round(gbs, 1),
+                   "payload_GBps_per_cta": round(gbs / cap, 1) if cap else None}
+            out["results"].append(row)
+            print(json.dumps(row), file=sys.stderr)
+            P.close()
+            D.close()
+    return out
+
+
 def swap_sweep():
     seed = seed_for(4)
     B = SHAPE.block_tokens
@@ -533,5 +573,5 @@ def tiny_latency():
 if __name__ == "__main__":
     fn = {"transfer": transfer_sweep, "swap": swap_sweep, "api": api_latency,
           "dram_source": dram_source_sweep, "gs": gs_latency, "chain": chain_sweep,
-          "tiny": tiny_latency, "nccl": nccl_sweep}[sys.argv[1]]
+          "tiny": tiny_latency, "nccl": nccl_sweep, "sms": sm_budget_sweep}[sys.argv[1]]
     print(json.dumps(fn(), indent=1))
