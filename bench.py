@@ -229,7 +229,7 @@ def run_ours(args, rank, world, dist):
     n_blocks = args.pool_blocks
     P = D = None
     knobs = dict(copy_kernel=args.copy_kernel, peer_engine=args.peer_engine,
-                 peer_sched=args.peer_sched)
+                 peer_sched=args.peer_sched, max_ctas=args.max_ctas)
     probe = None
     if role.kind != "PD" and not args.no_probe:
         # before the pools take HBM: the box's own large peer copy P_i -> D_i
@@ -559,6 +559,7 @@ def run_ours(args, rank, world, dist):
             "batch_blocks": args.batch_blocks,
             "copy_kernel": ["auto (bulk cp.async ring in HBM)", "vector LD/ST",
                             "bulk cp.async ring"][args.copy_kernel],
+            "max_ctas": args.max_ctas or "one full wave",
             "blocks_moved_total": int(blocks_all),
             "l2": "inputs larger than L2 (each step moves GiBs of distinct blocks)",
             "step_sync": ("no host sync between steps (stream-ordered); the timed region "
@@ -1149,6 +1150,8 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     ap.add_argument("--xfer-path", default="fused", choices=list(PATHS),
                     help="transport of P -> D transfers (named in config.xfer_path)")
+    ap.add_argument("--max-ctas", type=int, default=0,
+                    help="cap the migration grid at this many CTAs (0: one full wave)")
     ap.add_argument("--peer-engine", type=int, default=0, choices=[0, 1, 2],
                     help="stores into peer memory: 0 auto, 1 vector LD/ST, 2 bulk cp.async")
     ap.add_argument("--peer-sched", type=int, default=0, choices=[0, 1, 2],

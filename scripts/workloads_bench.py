@@ -188,6 +188,8 @@ def main():
                     help="sessions of the untimed CUPTI pass (0: skip)")
     ap.add_argument("--concurrent", type=int, default=1,
                     help="react: sessions in flight, interleaved turn by turn")
+    ap.add_argument("--max-ctas", type=int, default=0,
+                    help="cap the migration grid (0: one full wave)")
     ap.add_argument("--coalesce-mib", type=int, default=0,
                     help="launch coalescing limit (0: library default 1 GiB, <0: off)")
     args = ap.parse_args()
@@ -204,8 +206,10 @@ def main():
     else:
         sessions = traces.react_like(seed, n_sessions=args.sessions or 32)
         fn = react_session
-    P = make_pool(M, torch, 0, 0, S, args.pool_blocks, coalesce_mib=args.coalesce_mib)
-    D = make_pool(M, torch, 1, 0, S, args.pool_blocks, coalesce_mib=args.coalesce_mib)
+    P = make_pool(M, torch, 0, 0, S, args.pool_blocks, coalesce_mib=args.coalesce_mib,
+                  max_ctas=args.max_ctas)
+    D = make_pool(M, torch, 1, 0, S, args.pool_blocks, coalesce_mib=args.coalesce_mib,
+                  max_ctas=args.max_ctas)
     M.connect(P, D)
     clocks = Clocks("/tmp/clocks_wl.csv", 0)
     with clocks:
