@@ -281,8 +281,11 @@ mp_status mp_swap_in(mp_pool* pool, const mp_addr* addrs, int64_t n, uint32_t fl
  * (priv, priv_len bytes) queued at the receiver (mp_recv_poll).  src addrs
  * are allocated blocks of `src` in HBM or -- swapped out, memory asymmetry
  * in its pinned DRAM, each listed once (R13); DRAM blocks go
- * straight from DRAM to the destination's HBM.  The destination is always
- * HBM.  dst_addrs: n entries, output unless DST_GIVEN. */
+ * straight from DRAM to the destination's HBM (no swap_in, no index change
+ * at the source): copy-engine H2D into the source's staging and one scatter
+ * per slot when the staging holds a block (MP_DRAM_SOURCE=sm in the
+ * environment: one kernel reading the mapped DRAM).  The destination is
+ * always HBM.  dst_addrs: n entries, output unless DST_GIVEN. */
 mp_status mp_transfer(mp_pool* src, int32_t dst_instance, const mp_addr* src_addrs, int64_t n,
                       mp_addr* dst_addrs, uint32_t flags, int32_t layer_begin, int32_t layer_end,
                       const void* priv, int64_t priv_len);
