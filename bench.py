@@ -229,7 +229,8 @@ def run_ours(args, rank, world, dist):
     n_blocks = args.pool_blocks
     P = D = None
     knobs = dict(copy_kernel=args.copy_kernel, peer_engine=args.peer_engine,
-                 peer_sched=args.peer_sched, max_ctas=args.max_ctas)
+                 peer_sched=args.peer_sched, max_ctas=args.max_ctas,
+                 coalesce_mib=args.coalesce_mib)
     probe = None
     if role.kind != "PD" and not args.no_probe:
         # before the pools take HBM: the box's own large peer copy P_i -> D_i
@@ -560,6 +561,7 @@ def run_ours(args, rank, world, dist):
             "copy_kernel": ["auto (bulk cp.async ring in HBM)", "vector LD/ST",
                             "bulk cp.async ring"][args.copy_kernel],
             "max_ctas": args.max_ctas or "one full wave",
+            "coalesce_mib": args.coalesce_mib or 4096,
             "blocks_moved_total": int(blocks_all),
             "l2": "inputs larger than L2 (each step moves GiBs of distinct blocks)",
             "step_sync": ("no host sync between steps (stream-ordered); the timed region "
@@ -1150,6 +1152,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     ap.add_argument("--xfer-path", default="fused", choices=list(PATHS),
                     help="transport of P -> D transfers (named in config.xfer_path)")
+    ap.add_argument("--coalesce-mib", type=int, default=0,
+                    help="payload limit of one coalesced migration launch (0: the library default, 4096 MiB; "
+                         "-1: no coalescing)")
     ap.add_argument("--max-ctas", type=int, default=0,
                     help="cap the migration grid at this many CTAs (0: one full wave)")
     ap.add_argument("--peer-engine", type=int, default=0, choices=[0, 1, 2],

@@ -150,7 +150,7 @@ typedef struct {
   int32_t coalesce_mib;  /* launch coalescing of same-device fused transfers into this pool:
                             one launch per batch, flushed when the data stream is idle, at
                             this many MiB, or when anything else touches either pool;
-                            0: 1024 MiB, < 0: off (one launch per transfer) */
+                            0: 4096 MiB, < 0: off (one launch per transfer) */
   int32_t peer_engine;   /* copy engine of stores into a peer's memory (another GPU over
                             NVLink, or another process's IPC-mapped pool): 0 auto (vector
                             LD/ST, or MP_PEER_ENGINE=bulk), 1 vector, 2 bulk cp.async ring */

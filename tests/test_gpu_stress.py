@@ -52,7 +52,7 @@ def test_back_to_back_async_transfers_bytes(copy_kernel):
     D.close()
 
 
-@pytest.mark.parametrize("coalesce_mib", [0, -1, 64])   # default 1 GiB, off, 64 MiB
+@pytest.mark.parametrize("coalesce_mib", [0, -1, 64, 1024])   # default 4 GiB, off, 64 MiB, 1 GiB
 def test_bench_pattern_dedup_retire_bytes(coalesce_mib):
     """bench.py's step at host speed: P.match + DEDUP transfer_with_insert
     (ASYNC) per request, D retires the batch (free partials, delete prompts),
