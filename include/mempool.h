@@ -99,8 +99,9 @@ typedef enum {
  * call other than mp_match / mp_recv_poll / the getters and dumps, which
  * enqueue it before anything else.  Consecutive pipelined FUSED transfers to
  * the same peer (same layers, no inbound transfer in between, no destination
- * block repeated) join the pending copy -- one launch per coalescing limit
- * (coalesce_mib) instead of one per transfer.  Until it is enqueued the
+ * block repeated) join the pending copy while the sender's data stream is
+ * busy -- one launch per coalescing limit (coalesce_mib) instead of one per
+ * transfer; on an idle stream the next transfer enqueues the pending copy.  Until it is enqueued the
  * peer's later device work on those blocks waits; a sender that stops
  * calling must call mp_sync.  Cross-process MP_XFER_ASYNC (FUSED / CE)
  * commits at the receiver in the one round trip, before the copy is

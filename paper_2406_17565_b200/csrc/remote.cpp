@@ -859,12 +859,16 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   // unless this transfer may join it (same peer, path and layers, payload
   // under the pool's coalescing limit, no inbound transfer stamped since it
   // started -- wait_reply serves only requests stamped after this start)
+  // ... and only while the GPU is busy: an idle data stream gets the pending
+  // copy now (like the in-process batches' idle flush), so merging never
+  // holds back work the device could already be doing
   PendingTx* pt = src->pend_tx;
   const bool may_merge =
       pt && one_trip && (flags & MP_XFER_PIPELINE) && src->coalesce && pt->r == r &&
       pt->path == path && (path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED) &&
       pt->j0 == j0 && pt->nj == nj && pt->start_stamp == start_stamp &&
-      pt->bytes + (uint64_t)n * (uint64_t)nj * (uint64_t)src->chunk <= src->batch_limit;
+      pt->bytes + (uint64_t)n * (uint64_t)nj * (uint64_t)src->chunk <= src->batch_limit &&
+      (!src->idle_flush || cudaStreamQuery(src->stream) == cudaErrorNotReady);
   const mp_status fs = may_merge ? MP_OK : remote_flush_tx(src);
   mp_status st = wait_reply(src, c, s1);
   if (st == MP_OK && fs != MP_OK) st = fs;

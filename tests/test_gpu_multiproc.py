@@ -774,9 +774,14 @@ def test_two_process_react_vs_oracle(seed, transport):
 # MP_XFER_PIPELINE contract (include/mempool.h): the call returns after the
 # receiver's reply with the final addrs; the copy is enqueued by the sender's
 # next call -- not by mp_match -- and consecutive pipelined transfers to the
-# same peer merge into one launch; mp_sync enqueues and completes it.
-def _pipe_worker(rank, port, q):
+# same peer merge into one launch while the sender's GPU is busy (size-only
+# batching, MP_COALESCE_NO_IDLE_FLUSH=1, stands in for a busy GPU here); on an
+# idle GPU the next transfer enqueues the pending copy instead of merging;
+# mp_sync enqueues and completes it.
+def _pipe_worker(rank, port, q, idle_flush=False):
     try:
+        if not idle_flush:
+            os.environ["MP_COALESCE_NO_IDLE_FLUSH"] = "1"
         import torch
         import torch.distributed as dist
         from paper_2406_17565_b200 import mempool as M
@@ -800,7 +805,7 @@ def _pipe_worker(rank, port, q):
             out["after_first"] = pool.stats()["kernel_launches"]
             pool.match(np.arange(40, dtype=np.int32))          # host only: no flush
             out["after_match"] = pool.stats()["kernel_launches"]
-            d2 = pool.transfer(1, src[4:9], flags=fl)            # merges (receiver idle)
+            d2 = pool.transfer(1, src[4:9], flags=fl)            # merges (size-only batching)
             out["after_second"] = pool.stats()["kernel_launches"]
             pool.sync()                                         # enqueues and completes
             out["after_sync"] = pool.stats()["kernel_launches"]
@@ -827,19 +832,25 @@ def _pipe_worker(rank, port, q):
         q.put((rank, {"error": traceback.format_exc() + repr(e)}))
 
 
-def test_two_process_pipeline_contract():
+@pytest.mark.parametrize("idle_flush", [False, True])
+def test_two_process_pipeline_contract(idle_flush):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 30900 + (os.getpid() % 40)
-    ps = [ctx.Process(target=_pipe_worker, args=(r, port, q)) for r in range(2)]
+    port = 30900 + (os.getpid() % 40) + (40 if idle_flush else 0)
+    ps = [ctx.Process(target=_pipe_worker, args=(r, port, q, idle_flush)) for r in range(2)]
     for p in ps:
         p.start()
     res = _collect(q, ps, 300)
     s = res[0]
     assert s["after_first"] == 0 and s["after_match"] == 0   # still pending
-    assert s["after_second"] == 0                             # merged, still pending
-    assert s["after_sync"] == 1                               # one launch for both
-    assert s["after_mark"] == 2
+    if idle_flush:   # the sender's GPU is idle: the second call enqueues the first copy
+        assert s["after_second"] == 1
+        assert s["after_sync"] == 2
+        assert s["after_mark"] == 3
+    else:
+        assert s["after_second"] == 0                         # merged, still pending
+        assert s["after_sync"] == 1                           # one launch for both
+        assert s["after_mark"] == 2
     for si, di in s["pairs"]:
         assert np.array_equal(res[1]["dst"][di], s["src"][si]), (si, di)
 
