@@ -330,9 +330,12 @@ mp_status batch_append(mp_pool* src, mp_pool* dst, const std::vector<int32_t>& s
   b.bytes += (uint64_t)n * (uint64_t)nj * (uint64_t)dst->chunk;
   dst->stats.blocks_moved += (uint64_t)n;
   lap(6);
-  // keep the device busy: go now if its data stream has run dry
+  // keep the device busy: go now if the launches queued on its data stream
+  // are about to drain (host estimate) or it has run dry
+  constexpr double kDrainLead = 50e-6;
   const bool go = b.bytes >= dst->batch_limit ||
-                  (dst->idle_flush && cudaStreamQuery(dst->stream) == cudaSuccess);
+                  (dst->idle_flush && (host_clock() + kDrainLead >= dst->track->busy_until ||
+                                       cudaStreamQuery(dst->stream) == cudaSuccess));
   lap(7);
   if (go) TRY(flush_batch(dst));
   lap(8);
@@ -375,6 +378,12 @@ mp_status flush_batch(mp_pool* dst) {
     TRY(launch_migrate_timed(dst, dst->stream, pool_ep(src->d_slabs, inl ? nullptr : dst->bsrc),
                              pool_ep(dst->d_slabs, dinl ? nullptr : dst->bdst), n, b.j0, b.nj,
                              false, 0, inl ? &sinl : nullptr, /*meta_dep=*/!dinl, &lb));
+    {  // queued work estimate: read + write of the batch at ~7 TB/s
+      constexpr double kRate = 7.0e12;
+      const double now = host_clock();
+      dst->track->busy_until = std::max(now, dst->track->busy_until) +
+                               2.0 * (double)b.bytes / kRate;
+    }
     if (!inl || !dinl) {  // the launch reads this batch's id tables: guard their reuse
       CK(cudaEventRecord(dst->btab_ev[b.tab], dst->stream));
       dst->btab_used[b.tab] = true;

@@ -125,6 +125,11 @@ struct LaunchTrack {
   uint32_t gen = 0;
   bool unknown = true;  // the window holds a launch with unknown blocks
   int launches = 0;
+  // host-clock estimate (s) of when the coalesced launches queued on the
+  // stream drain (bytes at a slightly optimistic HBM rate): a batch being
+  // built is launched once less than kDrainLead of queued work remains, so
+  // the GPU has the next launch before it runs dry
+  double busy_until = 0.0;
 };
 // The blocks of one pool -> pool launch (host copies of its id lists).
 struct LaunchBlocks {
