@@ -784,6 +784,14 @@ mp_status remote_flush_tx(mp_pool* p) {
   PendingTx* t = p->pend_tx;
   if (!t) return MP_OK;
   p->pend_tx = nullptr;
+  {  // queued work estimate (LaunchTrack::busy_until): a same-GPU peer's copy
+     // reads and writes HBM (~7 TB/s), a remote one crosses NVLink (900 GB/s
+     // nominal per direction) -- optimistic rates, so merging stops early
+    const double now = host_clock();
+    const double secs = t->r->same_device ? 2.0 * (double)t->bytes / 7.0e12
+                                          : (double)t->bytes / 0.9e12;
+    p->track->busy_until = std::max(now, p->track->busy_until) + secs;
+  }
   const mp_status xs = transmit_step(p, t->r, t->path, t->j0, t->nj, t->hs, t->hd, t->ds, t->dd,
                                      RingGeom{}, 0, 0, t->prep_seq, t->done_seq, t->start_stamp,
                                      MP_OK);
@@ -859,16 +867,18 @@ mp_status remote_transfer(mp_pool* src, RemotePeer* r, int kind, const mp_token*
   // unless this transfer may join it (same peer, path and layers, payload
   // under the pool's coalescing limit, no inbound transfer stamped since it
   // started -- wait_reply serves only requests stamped after this start)
-  // ... and only while the GPU is busy: an idle data stream gets the pending
-  // copy now (like the in-process batches' idle flush), so merging never
-  // holds back work the device could already be doing
+  // ... and only while the GPU is busy for a while yet: an idle data stream,
+  // or one whose queued copies are about to drain (host estimate), gets the
+  // pending copy now (like the in-process batches), so merging never holds
+  // back work the device could already be doing
   PendingTx* pt = src->pend_tx;
   const bool may_merge =
       pt && one_trip && (flags & MP_XFER_PIPELINE) && src->coalesce && pt->r == r &&
       pt->path == path && (path == MP_XFER_PATH_AUTO || path == MP_XFER_PATH_FUSED) &&
       pt->j0 == j0 && pt->nj == nj && pt->start_stamp == start_stamp &&
       pt->bytes + (uint64_t)n * (uint64_t)nj * (uint64_t)src->chunk <= src->batch_limit &&
-      (!src->idle_flush || cudaStreamQuery(src->stream) == cudaErrorNotReady);
+      (!src->idle_flush || (host_clock() + 50e-6 < src->track->busy_until &&
+                            cudaStreamQuery(src->stream) == cudaErrorNotReady));
   const mp_status fs = may_merge ? MP_OK : remote_flush_tx(src);
   mp_status st = wait_reply(src, c, s1);
   if (st == MP_OK && fs != MP_OK) st = fs;
