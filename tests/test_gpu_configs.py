@@ -150,6 +150,44 @@ def test_config4_swap_sweep_7b():
     _close(S)
 
 
+@pytest.mark.parametrize("dram_mode", ["ce", "sm"])
+def test_config4_memory_asymmetric_transfer_7b(dram_mode, monkeypatch):
+    """SURVEY f1 at configs[4]'s shape: historical KV swapped out to the
+    sender's pinned DRAM goes straight into the receiver's HBM --
+    mixed HBM / DRAM source lists of whole sequences (transfer_with_insert,
+    DEDUP) and a by-layer DRAM-only range into given blocks -- through the
+    copy engine and the sender's 256 MiB staging (32 blocks: several
+    alternating slots per call) or the zero-copy kernel (MP_DRAM_SOURCE=sm)."""
+    monkeypatch.setenv("MP_DRAM_SOURCE", dram_mode)
+    from tests.twin import transfer
+    shape, seed = LLAMA2_7B, seed_for(4) + 7
+    B = shape.block_tokens
+    P = Twin(0, shape, 1024, 1024, seed=seed)
+    D = Twin(1, shape, 1024, seed=seed)
+    connect(P, D)
+    rng = np.random.default_rng(seed)
+    seqs = [rng.integers(3, 32000, size=int(rng.integers(40, 97)) * B, dtype=np.int32)
+            for _ in range(6)]
+    for t in seqs:
+        prefill(P, t, B)
+    P.swap_out(300)                                  # most of them now live in DRAM
+    n_dram = 0
+    for t in seqs:
+        _, src = P.match(t)
+        n_dram += sum(a[1] == O.DRAM for a in src)
+        transfer_with_insert(P, D, t[: len(src) * B], src, oflags=O.FLAG_DEDUP, path=ASYNC)
+    assert n_dram >= 200, n_dram
+    # a by-layer range of DRAM-resident blocks into caller-given blocks (A10)
+    _, src = P.match(seqs[0])
+    dram_src = [a for a in src if a[1] == O.DRAM][:40]
+    x = D.alloc(len(dram_src))
+    D.fill(x)
+    transfer(P, D, dram_src, x, oflags=O.FLAG_DST_GIVEN, l0=3, l1=11, path=ASYNC)
+    D.check_state(sample=64, rng=rng)
+    P.check_state(sample=16, rng=rng)
+    _close(P, D)
+
+
 def test_config2_loogle_13b_32k_document_one_launch():
     """configs[2]'s long end: a 32768-token document is 2048 blocks (25 GiB
     at 13B) moved by ONE transfer_with_insert launch, then a question turn
